@@ -1,0 +1,333 @@
+"""ctypes wrapper of ``liboracle.so`` (oracle/sbs_oracle.c).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Argument marshalling
+only: every number is computed in the C oracle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sbs_oracle.c")
+_HDR = os.path.join(_HERE, "sbs_oracle.h")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+MAX_KNOTS = 8
+MAX_D = 12 * MAX_KNOTS
+MAX_FREQ = 8
+MODES = {"mppi": 0, "cem": 1, "naive": 2}
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile the oracle (gcc, -O2 -ffp-contract=off) if stale."""
+    stale = force or not os.path.exists(_LIB) or max(
+        os.path.getmtime(_SRC), os.path.getmtime(_HDR)) > os.path.getmtime(_LIB)
+    if stale:
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math",
+                               "-Wall", "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class OrcConfig(C.Structure):
+    _fields_ = [
+        ("mass", C.c_double), ("inertia", C.c_double * 9), ("gravity", C.c_double * 3),
+        ("mu", C.c_double), ("fz_min", C.c_double), ("fz_max", C.c_double),
+        ("horizon", C.c_int32), ("knots", C.c_int32), ("dt", C.c_double),
+        ("duty_factor", C.c_double), ("phase_offset", C.c_double * 4),
+        ("n_freq", C.c_int32), ("gait_adapt", C.c_int32), ("freq_hz", C.c_double * MAX_FREQ),
+        ("Q", C.c_double * 12), ("R", C.c_double * 12), ("rho", C.c_double),
+        ("f_nominal", C.c_double), ("w_fc", C.c_double),
+        ("mode", C.c_int32), ("elite_preserve", C.c_int32),
+        ("n_samples", C.c_int64), ("n_elite", C.c_int64), ("lambda_", C.c_double),
+        ("sigma", C.c_double * 3), ("sigma_min_frac", C.c_double),
+        ("warm_shift", C.c_int32), ("_pad", C.c_int32), ("seed", C.c_uint64),
+    ]
+
+
+class OrcDiag(C.Structure):
+    _fields_ = [("j_min", C.c_double), ("j_mean", C.c_double), ("omega", C.c_double),
+                ("ess", C.c_double), ("n_diverged", C.c_int64), ("argmin", C.c_int64)]
+
+
+class OrcState(C.Structure):
+    _fields_ = [("mean", C.c_double * MAX_D), ("var", C.c_double * MAX_D),
+                ("freq_idx", C.c_int32), ("iter", C.c_uint32)]
+
+
+class OrcOutput(C.Structure):
+    _fields_ = [("u0", C.c_double * 12), ("contact0", C.c_int32 * 4), ("freq_idx", C.c_int32),
+                ("status", C.c_int32), ("freq_hz", C.c_double), ("diag", OrcDiag)]
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _f64(a, n=None):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if n is not None:
+        assert a.size == n, (a.size, n)
+    return a
+
+
+def make_config(cfg: dict) -> OrcConfig:
+    """Build the oracle's own config struct from a workload dict."""
+    c = OrcConfig()
+    c.mass = cfg["mass"]
+    c.inertia[:] = list(np.asarray(cfg["inertia"], dtype=np.float64).ravel())
+    c.gravity[:] = list(cfg["gravity"])
+    c.mu, c.fz_min, c.fz_max = cfg["mu"], cfg["fz_min"], cfg["fz_max"]
+    c.horizon, c.knots, c.dt = cfg["horizon"], cfg["knots"], cfg["dt"]
+    c.duty_factor = cfg["duty_factor"]
+    c.phase_offset[:] = list(cfg["phase_offset"])
+    f = list(cfg["freq_hz"])
+    c.n_freq = len(f)
+    c.freq_hz[:len(f)] = f
+    c.gait_adapt = int(cfg["gait_adapt"])
+    c.Q[:] = list(cfg["Q"])
+    c.R[:] = list(cfg["R"])
+    c.rho, c.f_nominal, c.w_fc = cfg["rho"], cfg["f_nominal"], cfg["w_fc"]
+    c.mode = MODES[cfg["mode"]]
+    c.elite_preserve = int(cfg["elite_preserve"])
+    c.n_samples = cfg["n_samples"]
+    c.n_elite = cfg["n_elite"]
+    c.lambda_ = cfg["lambda"]
+    c.sigma[:] = list(cfg["sigma"])
+    c.sigma_min_frac = cfg["sigma_min_frac"]
+    c.warm_shift = int(cfg["warm_shift"])
+    c.seed = cfg["seed"]
+    return c
+
+
+@dataclass
+class StepResult:
+    status: int
+    mean: np.ndarray
+    var: np.ndarray
+    freq_idx: int
+    freq_hz: float
+    u0: np.ndarray
+    contact0: np.ndarray
+    j_min: float
+    j_mean: float
+    omega: float
+    ess: float
+    n_diverged: int
+    argmin: int
+    J: np.ndarray | None = None
+    fidx: np.ndarray | None = None
+    theta: np.ndarray | None = None
+    z: np.ndarray | None = None
+    elite: np.ndarray | None = None
+
+
+class Oracle:
+    """Thin marshalling layer over the C oracle."""
+
+    def __init__(self):
+        self.lib = C.CDLL(build_oracle())
+        L = self.lib
+        u32p, dp, i32p = C.POINTER(C.c_uint32), C.POINTER(C.c_double), C.POINTER(C.c_int32)
+        cfgp = C.POINTER(OrcConfig)
+        L.orc_philox4x32_10.argtypes = [u32p, u32p, u32p]
+        L.orc_ln_u24.argtypes = [C.c_uint32]
+        L.orc_ln_u24.restype = C.c_float
+        L.orc_sincos_2pi_u.argtypes = [C.c_uint32, C.POINTER(C.c_float), C.POINTER(C.c_float)]
+        L.orc_normal4.argtypes = [u32p, C.POINTER(C.c_float)]
+        L.orc_sample.argtypes = [cfgp, dp, dp, C.c_int32, C.c_uint32, C.c_uint32, C.c_int64,
+                                 dp, C.POINTER(C.c_float), i32p]
+        L.orc_warm_shift.argtypes = [cfgp, dp, dp]
+        L.orc_phase_inc.argtypes = [C.c_double, C.c_double]
+        L.orc_phase_inc.restype = C.c_uint32
+        L.orc_stance_threshold.argtypes = [C.c_double]
+        L.orc_stance_threshold.restype = C.c_uint64
+        L.orc_contact_sequence.argtypes = [cfgp, C.c_uint32, C.c_double, i32p]
+        L.orc_spline_eval.argtypes = [C.c_int32, dp, C.c_int64, C.c_int64, dp]
+        L.orc_spline_step.argtypes = [cfgp, dp, C.c_int32, dp]
+        L.orc_cone.argtypes = [cfgp, dp, dp, dp]
+        L.orc_dynamics.argtypes = [cfgp, dp, dp, i32p, dp, dp]
+        L.orc_rk4.argtypes = [cfgp, dp, dp, i32p, dp, C.c_double, dp]
+        L.orc_rollout.argtypes = [cfgp, dp, C.c_uint32, dp, dp, dp, dp, C.c_int32, dp]
+        L.orc_rollout.restype = C.c_double
+        L.orc_mppi.argtypes = [C.c_int64, C.c_int32, dp, dp, C.c_double, dp, C.POINTER(OrcDiag)]
+        L.orc_cem_select.argtypes = [C.c_int64, dp, C.c_int64, C.POINTER(C.c_int64)]
+        L.orc_cem_update.argtypes = [C.c_int64, C.c_int32, dp, dp, C.c_int64, dp, C.c_int32,
+                                     dp, dp, C.POINTER(C.c_int64), C.POINTER(OrcDiag)]
+        L.orc_step.argtypes = [cfgp, C.c_uint32, dp, C.c_uint32, dp, dp, dp,
+                               C.POINTER(OrcState), C.POINTER(OrcOutput), dp, i32p, dp,
+                               C.POINTER(C.c_float), C.POINTER(C.c_int64)]
+
+    # ---- noise -----------------------------------------------------------
+    def philox(self, ctr, key):
+        c = (C.c_uint32 * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])
+        k = (C.c_uint32 * 2)(*[int(v) & 0xFFFFFFFF for v in key])
+        o = (C.c_uint32 * 4)()
+        self.lib.orc_philox4x32_10(c, k, o)
+        return [int(v) for v in o]
+
+    def ln_u24(self, w):
+        return float(np.float32(self.lib.orc_ln_u24(int(w))))
+
+    def sincos_2pi_u(self, w):
+        s, c = C.c_float(), C.c_float()
+        self.lib.orc_sincos_2pi_u(int(w), C.byref(s), C.byref(c))
+        return np.float32(s.value), np.float32(c.value)
+
+    def normal4(self, w):
+        ww = (C.c_uint32 * 4)(*[int(v) & 0xFFFFFFFF for v in w])
+        z = (C.c_float * 4)()
+        self.lib.orc_normal4(ww, z)
+        return np.array(z, dtype=np.float32)
+
+    def sample(self, cfg, mu_shift, var, cur_idx, it, robot, k):
+        c = make_config(cfg)
+        D = 12 * cfg["knots"]
+        th = np.zeros(D)
+        z = np.zeros(D, dtype=np.float32)
+        idx = C.c_int32()
+        self.lib.orc_sample(C.byref(c), _dp(_f64(mu_shift, D)), _dp(_f64(var, D)), int(cur_idx),
+                            int(it), int(robot), int(k), _dp(th),
+                            z.ctypes.data_as(C.POINTER(C.c_float)), C.byref(idx))
+        return th, z, idx.value
+
+    def warm_shift(self, cfg, mu):
+        c = make_config(cfg)
+        D = 12 * cfg["knots"]
+        out = np.zeros(D)
+        self.lib.orc_warm_shift(C.byref(c), _dp(_f64(mu, D)), _dp(out))
+        return out
+
+    # ---- gait ------------------------------------------------------------
+    def phase_inc(self, f, dt):
+        return int(self.lib.orc_phase_inc(float(f), float(dt)))
+
+    def stance_threshold(self, duty):
+        return int(self.lib.orc_stance_threshold(float(duty)))
+
+    def contact_sequence(self, cfg, phase0, f):
+        c = make_config(cfg)
+        d = np.zeros((cfg["horizon"], 4), dtype=np.int32)
+        self.lib.orc_contact_sequence(C.byref(c), int(phase0) & 0xFFFFFFFF, float(f),
+                                      d.ctypes.data_as(C.POINTER(C.c_int32)))
+        return d
+
+    # ---- spline / cone ---------------------------------------------------
+    def spline_eval(self, knots, a_num, a_den):
+        kn = _f64(knots)
+        o = C.c_double()
+        self.lib.orc_spline_eval(len(kn), _dp(kn), int(a_num), int(a_den), C.byref(o))
+        return o.value
+
+    def spline_step(self, cfg, theta, j):
+        c = make_config(cfg)
+        g = np.zeros(12)
+        self.lib.orc_spline_step(C.byref(c), _dp(_f64(theta, 12 * cfg["knots"])), int(j), _dp(g))
+        return g
+
+    def cone(self, cfg, raw):
+        c = make_config(cfg)
+        o = np.zeros(3)
+        pen = C.c_double()
+        self.lib.orc_cone(C.byref(c), _dp(_f64(raw, 3)), _dp(o), C.byref(pen))
+        return o, pen.value
+
+    # ---- dynamics --------------------------------------------------------
+    def dynamics(self, cfg, x, gamma, stance, feet):
+        c = make_config(cfg)
+        xd = np.zeros(12)
+        st = np.ascontiguousarray(np.asarray(stance, dtype=np.int32))
+        self.lib.orc_dynamics(C.byref(c), _dp(_f64(x, 12)), _dp(_f64(gamma, 12)),
+                              st.ctypes.data_as(C.POINTER(C.c_int32)), _dp(_f64(feet, 12)), _dp(xd))
+        return xd
+
+    def rk4(self, cfg, x, gamma, stance, feet, h):
+        c = make_config(cfg)
+        xn = np.zeros(12)
+        st = np.ascontiguousarray(np.asarray(stance, dtype=np.int32))
+        self.lib.orc_rk4(C.byref(c), _dp(_f64(x, 12)), _dp(_f64(gamma, 12)),
+                         st.ctypes.data_as(C.POINTER(C.c_int32)), _dp(_f64(feet, 12)), float(h), _dp(xn))
+        return xn
+
+    def rollout(self, cfg, x0, phase0, feet_cur, feet_next, xref, theta, fidx, traj=False):
+        c = make_config(cfg)
+        H = cfg["horizon"]
+        tr = np.zeros((H + 1, 12)) if traj else None
+        J = self.lib.orc_rollout(C.byref(c), _dp(_f64(x0, 12)), int(phase0) & 0xFFFFFFFF,
+                                 _dp(_f64(feet_cur, 12)), _dp(_f64(feet_next, 12)),
+                                 _dp(_f64(xref, H * 12)), _dp(_f64(theta, 12 * cfg["knots"])),
+                                 int(fidx), _dp(tr) if traj else None)
+        return (J, tr) if traj else J
+
+    # ---- updates ---------------------------------------------------------
+    def mppi(self, J, theta, lam):
+        J = _f64(J)
+        th = _f64(theta)
+        K = J.size
+        D = th.size // max(K, 1)
+        mu = np.zeros(D)
+        dg = OrcDiag()
+        rc = self.lib.orc_mppi(K, D, _dp(J), _dp(th), float(lam), _dp(mu), C.byref(dg))
+        return rc, mu, dg
+
+    def cem_select(self, J, K_e):
+        J = _f64(J)
+        e = np.zeros(int(K_e), dtype=np.int64)
+        rc = self.lib.orc_cem_select(J.size, _dp(J), int(K_e), e.ctypes.data_as(C.POINTER(C.c_int64)))
+        assert rc == 0, rc
+        return e
+
+    def cem_update(self, J, theta, K_e, var_floor, update_var, var_in):
+        J = _f64(J)
+        th = _f64(theta)
+        K = J.size
+        D = th.size // K
+        mu = np.zeros(D)
+        var = _f64(var_in, D).copy()
+        e = np.zeros(int(K_e), dtype=np.int64)
+        dg = OrcDiag()
+        rc = self.lib.orc_cem_update(K, D, _dp(J), _dp(th), int(K_e), _dp(_f64(var_floor, D)),
+                                     int(update_var), _dp(mu), _dp(var),
+                                     e.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(dg))
+        return rc, mu, var, e, dg
+
+    # ---- whole iteration -------------------------------------------------
+    def step(self, cfg, robot, inp, state, keep=True):
+        """One Alg. 5 iteration.  ``state`` = dict(mean, var, freq_idx, iter); updated in place."""
+        c = make_config(cfg)
+        K, D, H = cfg["n_samples"], 12 * cfg["knots"], cfg["horizon"]
+        st = OrcState()
+        st.mean[:D] = list(np.asarray(state["mean"], dtype=np.float64))
+        st.var[:D] = list(np.asarray(state["var"], dtype=np.float64))
+        st.freq_idx = int(state["freq_idx"])
+        st.iter = int(state["iter"])
+        out = OrcOutput()
+        J = np.zeros(K) if keep else None
+        fidx = np.zeros(K, dtype=np.int32) if keep else None
+        theta = np.zeros((K, D)) if keep else None
+        z = np.zeros((K, D), dtype=np.float32) if keep else None
+        ke = 1 if cfg["mode"] == "naive" else (cfg["n_elite"] if cfg["mode"] == "cem" else 0)
+        elite = np.zeros(max(ke, 1), dtype=np.int64) if keep and ke else None
+        rc = self.lib.orc_step(
+            C.byref(c), int(robot), _dp(_f64(inp["x0"], 12)), int(inp["phase"]) & 0xFFFFFFFF,
+            _dp(_f64(inp["feet_cur"], 12)), _dp(_f64(inp["feet_next"], 12)),
+            _dp(_f64(inp["xref"], H * 12)), C.byref(st), C.byref(out),
+            _dp(J) if keep else None, fidx.ctypes.data_as(C.POINTER(C.c_int32)) if keep else None,
+            _dp(theta) if keep else None, z.ctypes.data_as(C.POINTER(C.c_float)) if keep else None,
+            elite.ctypes.data_as(C.POINTER(C.c_int64)) if elite is not None else None)
+        state["mean"] = np.array(st.mean[:D])
+        state["var"] = np.array(st.var[:D])
+        state["freq_idx"] = st.freq_idx
+        state["iter"] = st.iter
+        dg = out.diag
+        return StepResult(status=rc, mean=state["mean"].copy(), var=state["var"].copy(),
+                          freq_idx=out.freq_idx, freq_hz=out.freq_hz, u0=np.array(out.u0),
+                          contact0=np.array(out.contact0), j_min=dg.j_min, j_mean=dg.j_mean,
+                          omega=dg.omega, ess=dg.ess, n_diverged=dg.n_diverged, argmin=dg.argmin,
+                          J=J, fidx=fidx, theta=theta, z=z, elite=elite)
