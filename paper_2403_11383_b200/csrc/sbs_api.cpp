@@ -1,0 +1,746 @@
+// sbs_api.cpp -- host runtime behind the C ABI of include/sbs.h.
+//
+// Owns the device state of one or more SBS controllers (R robots), derives the
+// constant tables once at creation (Catmull-Rom weights, warm-shift weights,
+// Q0.32 gait increments, inverse inertia), and enqueues one MPC iteration as
+// 2 (MPPI) or 3 (CEM / Naive) kernel launches on one stream.  With world > 1
+// the MPPI partials of the ranks are exchanged by one NCCL all-gather.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "sbs_internal.h"
+
+using sbs::Params;
+
+namespace {
+
+// ---- minimal NCCL surface, resolved with dlopen (torch ships libnccl.so.2) ----
+typedef struct {
+  char internal[128];
+} nccl_uid;
+typedef void* nccl_comm_t;
+typedef int (*PFN_GetUniqueId)(nccl_uid*);
+typedef int (*PFN_CommInitRank)(nccl_comm_t*, int, nccl_uid, int);
+typedef int (*PFN_AllGather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t);
+typedef int (*PFN_CommDestroy)(nccl_comm_t);
+typedef const char* (*PFN_GetErrorString)(int);
+struct Nccl {
+  void* h = nullptr;
+  PFN_GetUniqueId get_uid = nullptr;
+  PFN_CommInitRank init_rank = nullptr;
+  PFN_AllGather all_gather = nullptr;
+  PFN_CommDestroy destroy = nullptr;
+  PFN_GetErrorString err = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    get_uid = (PFN_GetUniqueId)dlsym(h, "ncclGetUniqueId");
+    init_rank = (PFN_CommInitRank)dlsym(h, "ncclCommInitRank");
+    all_gather = (PFN_AllGather)dlsym(h, "ncclAllGather");
+    destroy = (PFN_CommDestroy)dlsym(h, "ncclCommDestroy");
+    err = (PFN_GetErrorString)dlsym(h, "ncclGetErrorString");
+    return get_uid && init_rank && all_gather && destroy;
+  }
+};
+Nccl g_nccl;
+constexpr int kNcclFloat32 = 7;  // ncclFloat32 in nccl.h
+
+thread_local std::string g_create_err;
+
+}  // namespace
+
+struct sbs_ctx {
+  sbs_config cfg{};
+  Params P{};
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  // device buffers
+  float* d_mean = nullptr;
+  float* d_var = nullptr;
+  int* d_fidx = nullptr;
+  float* d_xref = nullptr;
+  float* d_J = nullptr;
+  float* d_part = nullptr;
+  float* d_gather = nullptr;  // [world][R][kPartStride] (world > 1)
+  int64_t* d_elite = nullptr;
+  int64_t* d_best = nullptr;
+  int* d_status = nullptr;
+  sbs_input* d_in = nullptr;
+  sbs_output* d_out = nullptr;
+  sbs_input* h_in = nullptr;   // pinned
+  sbs_output* h_out = nullptr; // pinned
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<char> ref_set;
+  uint32_t iter = 0;
+  std::string err;
+  // profiling
+  bool profile = false;
+  struct Pending {
+    int kernel;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> free_events;
+  double kt[SBS_NKERNELS] = {0, 0, 0, 0};
+  int64_t kl[SBS_NKERNELS] = {0, 0, 0, 0};
+  // nccl
+  nccl_comm_t comm = nullptr;
+};
+
+namespace {
+
+int fail(sbs_ctx* c, int st, const std::string& msg) {
+  if (c) c->err = msg;
+  else g_create_err = msg;
+  return st;
+}
+
+int cuda_fail(sbs_ctx* c, cudaError_t e, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+  return fail(c, e == cudaErrorMemoryAllocation ? SBS_ERR_OOM : SBS_ERR_CUDA, m);
+}
+
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(c, e_, #call); \
+  } while (0)
+
+bool finite_all(const float* v, int n) {
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
+// Uniform Catmull-Rom weights on the P real knots for the evaluation point
+// tau = num/den (knot units), phantom end knots by linear extrapolation (L7).
+void catmull_rom_row(int P, int64_t num, int64_t den, double* w /*[P]*/) {
+  for (int q = 0; q < P; ++q) w[q] = 0.0;
+  int64_t s = num / den;
+  double u = (double)(num % den) / (double)den;
+  if (s >= P - 1) {
+    s = P - 2;
+    u = 1.0;
+  }
+  const double u2 = u * u, u3 = u2 * u;
+  const double c[4] = {0.5 * (-u3 + 2 * u2 - u), 0.5 * (3 * u3 - 5 * u2 + 2), 0.5 * (-3 * u3 + 4 * u2 + u),
+                       0.5 * (u3 - u2)};
+  for (int t = 0; t < 4; ++t) {
+    const int64_t idx = s - 1 + t;
+    if (idx < 0) {  // phantom k[-1] = 2 k[0] - k[1]
+      w[0] += 2.0 * c[t];
+      w[1] -= c[t];
+    } else if (idx > P - 1) {  // phantom k[P] = 2 k[P-1] - k[P-2]
+      w[P - 1] += 2.0 * c[t];
+      w[P - 2] -= c[t];
+    } else {
+      w[idx] += c[t];
+    }
+  }
+}
+
+uint32_t q32_inc(double f, double dt) { return (uint32_t)(uint64_t)llround((f * dt) * 4294967296.0); }
+
+int validate(const sbs_config* c, std::string& why) {
+  auto bad = [&](const char* m) {
+    why = m;
+    return SBS_ERR_INVALID_ARG;
+  };
+  if (!(c->mass > 0)) return bad("mass must be > 0");
+  const float* I = c->inertia;
+  if (!finite_all(I, 9)) return bad("inertia not finite");
+  if (I[1] != I[3] || I[2] != I[6] || I[5] != I[7]) return bad("inertia not symmetric");
+  const double d1 = I[0], d2 = (double)I[0] * I[4] - (double)I[1] * I[3];
+  const double d3 = I[0] * ((double)I[4] * I[8] - (double)I[5] * I[7]) - I[1] * ((double)I[3] * I[8] - (double)I[5] * I[6]) +
+                    I[2] * ((double)I[3] * I[7] - (double)I[4] * I[6]);
+  if (!(d1 > 0 && d2 > 0 && d3 > 0)) return bad("inertia not positive definite");
+  if (!finite_all(c->gravity, 3) || !(c->gravity[2] < 0)) return bad("gravity[2] must be < 0");
+  if (!(c->mu > 0)) return bad("mu must be > 0");
+  if (!(c->fz_min >= 0 && c->fz_min < c->fz_max)) return bad("need 0 <= fz_min < fz_max");
+  if (c->horizon < 1 || c->horizon > SBS_MAX_HORIZON) return bad("horizon out of range");
+  if (c->knots < 2 || c->knots > SBS_MAX_KNOTS) return bad("knots out of range");
+  if (!(c->dt > 0)) return bad("dt must be > 0");
+  if (!(c->duty_factor > 0 && c->duty_factor <= 1)) return bad("duty_factor must be in (0, 1]");
+  for (int i = 0; i < 4; ++i)
+    if (!(c->phase_offset[i] >= 0 && c->phase_offset[i] < 1)) return bad("phase_offset must be in [0, 1)");
+  if (c->n_freq < 1 || c->n_freq > SBS_MAX_FREQ) return bad("n_freq out of range");
+  for (int i = 0; i < c->n_freq; ++i) {
+    if (!(c->freq_hz[i] > 0)) return bad("freq_hz must be > 0");
+    if (i > 0 && !(c->freq_hz[i] > c->freq_hz[i - 1])) return bad("freq_hz must be strictly increasing");
+  }
+  for (int i = 0; i < 12; ++i)
+    if (!(c->Q[i] >= 0) || !(c->R[i] >= 0)) return bad("Q and R must be >= 0");
+  if (!(c->rho >= 0) || !(c->w_fc >= 0) || !std::isfinite(c->f_nominal)) return bad("bad rho / w_fc / f_nominal");
+  if (c->mode < SBS_MPPI || c->mode > SBS_NAIVE) return bad("bad mode");
+  if (c->n_samples < 1 || c->n_samples > 0x7fffffffLL) return bad("n_samples out of range");
+  if (c->mode == SBS_CEM && (c->n_elite < 1 || c->n_elite > c->n_samples)) return bad("need 1 <= n_elite <= n_samples");
+  if (!(c->lambda > 0)) return bad("lambda must be > 0");
+  for (int a = 0; a < 3; ++a)
+    if (!(c->sigma[a] > 0)) return bad("sigma must be > 0");
+  if (!(c->sigma_min_frac >= 0)) return bad("sigma_min_frac must be >= 0");
+  if (c->n_robots < 1) return bad("n_robots must be >= 1");
+  if (c->robot_offset < 0) return bad("robot_offset must be >= 0");
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad("bad rank / world");
+  if (c->world > 1 && c->mode != SBS_MPPI) return bad("sample sharding (world > 1) is implemented for MPPI only");
+  if (c->world > 1 && c->n_samples < c->world) return bad("n_samples < world");
+  return SBS_OK;
+}
+
+cudaEvent_t take_event(sbs_ctx* c) {
+  if (!c->free_events.empty()) {
+    cudaEvent_t e = c->free_events.back();
+    c->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// launch wrapper with optional per-kernel event timing
+template <class F>
+cudaError_t timed(sbs_ctx* c, int kernel, cudaStream_t s, F&& launch) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->profile) {
+    a = take_event(c);
+    b = take_event(c);
+    cudaEventRecord(a, s);
+  }
+  cudaError_t e = launch();
+  if (c->profile) {
+    cudaEventRecord(b, s);
+    c->pending.push_back({kernel, a, b});
+  }
+  return e;
+}
+
+// enqueue one iteration on stream s with inputs c->P.in and outputs c->P.out
+int enqueue_step(sbs_ctx* c, cudaStream_t s) {
+  Params& P = c->P;
+  P.iter = c->iter;
+  const bool mppi = c->cfg.mode == SBS_MPPI;
+  CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, mppi, s); }));
+  if (mppi) {
+    if (c->cfg.world == 1) {
+      CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_finalize(P, s); }));
+    } else {
+      // rank partial -> all-gather -> merge of the `world` partials in rank order
+      Params Q = P;
+      Q.out = nullptr;
+      CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_merge(Q, c->d_gather + (size_t)c->cfg.rank * P.R * sbs::kPartStride, s); }));
+      const size_t n = (size_t)P.R * sbs::kPartStride;
+      int rc = g_nccl.all_gather(c->d_gather + (size_t)c->cfg.rank * n, c->d_gather, n, kNcclFloat32, c->comm, s);
+      if (rc != 0) return fail(c, SBS_ERR_NCCL, std::string("ncclAllGather: ") + (g_nccl.err ? g_nccl.err(rc) : "?"));
+      Params F = P;
+      F.part = c->d_gather;
+      F.n_cta = c->cfg.world;
+      F.part_c_stride = P.R;  // gathered layout [world][R][stride]
+      CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_finalize(F, s); }));
+    }
+  } else {
+    CK(timed(c, SBS_KERNEL_SELECT, s, [&] { return sbs::launch_select(P, s); }));
+    CK(timed(c, SBS_KERNEL_ELITE, s, [&] { return sbs::launch_elite(P, s); }));
+  }
+  return SBS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sbs_version(void) { return SBS_VERSION; }
+uint64_t sbs_sizeof_config(void) { return sizeof(sbs_config); }
+uint64_t sbs_sizeof_input(void) { return sizeof(sbs_input); }
+uint64_t sbs_sizeof_output(void) { return sizeof(sbs_output); }
+
+const char* sbs_status_str(int st) {
+  switch (st) {
+    case SBS_OK: return "SBS_OK";
+    case SBS_WARN_ALL_DIVERGED: return "SBS_WARN_ALL_DIVERGED";
+    case SBS_ERR_INVALID_ARG: return "SBS_ERR_INVALID_ARG";
+    case SBS_ERR_SINGULAR: return "SBS_ERR_SINGULAR";
+    case SBS_ERR_NONFINITE: return "SBS_ERR_NONFINITE";
+    case SBS_ERR_STATE: return "SBS_ERR_STATE";
+    case SBS_ERR_CUDA: return "SBS_ERR_CUDA";
+    case SBS_ERR_NCCL: return "SBS_ERR_NCCL";
+    case SBS_ERR_OOM: return "SBS_ERR_OOM";
+    default: return "SBS_UNKNOWN_STATUS";
+  }
+}
+
+const char* sbs_last_error(const sbs_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+int sbs_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return SBS_ERR_INVALID_ARG;
+  if (!g_nccl.load()) return fail(nullptr, SBS_ERR_NCCL, "libnccl.so.2 not found");
+  nccl_uid u;
+  int rc = g_nccl.get_uid(&u);
+  if (rc != 0) return fail(nullptr, SBS_ERR_NCCL, "ncclGetUniqueId failed");
+  memcpy(id, u.internal, 128);
+  return SBS_OK;
+}
+
+void sbs_destroy(sbs_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->cfg.device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
+  for (void* p : {(void*)c->d_mean, (void*)c->d_var, (void*)c->d_fidx, (void*)c->d_xref, (void*)c->d_J,
+                  (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status,
+                  (void*)c->d_in, (void*)c->d_out})
+    if (p) cudaFree(p);
+  if (c->h_in) cudaFreeHost(c->h_in);
+  if (c->h_out) cudaFreeHost(c->h_out);
+  for (auto& pd : c->pending) {
+    cudaEventDestroy(pd.a);
+    cudaEventDestroy(pd.b);
+  }
+  for (auto e : c->free_events) cudaEventDestroy(e);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
+  if (!cfg || !out) return fail(nullptr, SBS_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  std::string why;
+  if (validate(cfg, why) != SBS_OK) return fail(nullptr, SBS_ERR_INVALID_ARG, why);
+  sbs_ctx* c = new sbs_ctx();
+  c->cfg = *cfg;
+  auto bail = [&](int st) {
+    g_create_err = c->err;
+    sbs_destroy(c);
+    return st;
+  };
+  int rc;
+#define CKC(call)                                 \
+  do {                                            \
+    cudaError_t e_ = (call);                      \
+    if (e_ != cudaSuccess) {                      \
+      rc = cuda_fail(c, e_, #call);               \
+      return bail(rc);                            \
+    }                                             \
+  } while (0)
+  CKC(cudaSetDevice(cfg->device));
+  CKC(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, cfg->device));
+  CKC(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CKC(cudaEventCreate(&c->ev0));
+  CKC(cudaEventCreate(&c->ev1));
+
+  Params& P = c->P;
+  const int H = cfg->horizon, Pk = cfg->knots, D = 12 * Pk, R = cfg->n_robots;
+  // ---- model and cost constants ----
+  P.inv_mass = (float)(1.0 / (double)cfg->mass);
+  for (int a = 0; a < 3; ++a) P.g[a] = cfg->gravity[a];
+  {
+    const double* dummy = nullptr;
+    (void)dummy;
+    double A[9];
+    for (int i = 0; i < 9; ++i) A[i] = cfg->inertia[i];
+    const double det = A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+                       A[2] * (A[3] * A[7] - A[4] * A[6]);
+    const double inv[9] = {(A[4] * A[8] - A[5] * A[7]) / det, (A[2] * A[7] - A[1] * A[8]) / det,
+                           (A[1] * A[5] - A[2] * A[4]) / det, (A[5] * A[6] - A[3] * A[8]) / det,
+                           (A[0] * A[8] - A[2] * A[6]) / det, (A[2] * A[3] - A[0] * A[5]) / det,
+                           (A[3] * A[7] - A[4] * A[6]) / det, (A[1] * A[6] - A[0] * A[7]) / det,
+                           (A[0] * A[4] - A[1] * A[3]) / det};
+    for (int i = 0; i < 9; ++i) {
+      P.I[i] = cfg->inertia[i];
+      P.Iinv[i] = (float)inv[i];
+    }
+    P.diag_inertia = (A[1] == 0 && A[2] == 0 && A[5] == 0) ? 1 : 0;
+  }
+  P.mu = cfg->mu;
+  P.fz_min = cfg->fz_min;
+  P.fz_max = cfg->fz_max;
+  P.dt = cfg->dt;
+  for (int a = 0; a < 12; ++a) {
+    P.Q[a] = cfg->Q[a];
+    P.Rw[a] = cfg->R[a];
+  }
+  P.rho = cfg->rho;
+  P.f_nominal = cfg->f_nominal;
+  P.w_fc = cfg->w_fc;
+  P.inv_lambda = (float)(1.0 / (double)cfg->lambda);
+  for (int n = 0; n <= 4; ++n) P.urz[n] = (float)(-(double)cfg->mass * (double)cfg->gravity[2] / (double)std::max(1, n));
+  // ---- gait: Q0.32 tables (L22) ----
+  for (int f = 0; f < SBS_MAX_FREQ; ++f) {
+    P.inc[f] = f < cfg->n_freq ? q32_inc((double)cfg->freq_hz[f], (double)cfg->dt) : 0u;
+    P.freq_hz[f] = f < cfg->n_freq ? cfg->freq_hz[f] : 0.f;
+  }
+  for (int i = 0; i < 4; ++i) P.off[i] = (uint32_t)(uint64_t)llround((double)cfg->phase_offset[i] * 4294967296.0);
+  {
+    const uint64_t thr = (uint64_t)llround((double)cfg->duty_factor * 4294967296.0);
+    P.all_stance = thr >= 4294967296ull ? 1 : 0;
+    P.thr = (uint32_t)std::min<uint64_t>(thr, 0xFFFFFFFFull);
+  }
+  P.n_freq = cfg->n_freq;
+  P.gait_adapt = cfg->gait_adapt ? 1 : 0;
+  P.elite_preserve = cfg->elite_preserve ? 1 : 0;
+  P.warm_shift = cfg->warm_shift ? 1 : 0;
+  // ---- spline tables (L7, L20) ----
+  P.H = H;
+  P.P = Pk;
+  P.D = D;
+  double w[SBS_MAX_KNOTS];
+  for (int j = 0; j < H; ++j) {
+    catmull_rom_row(Pk, (int64_t)j * (Pk - 1), H, w);
+    for (int q = 0; q < Pk; ++q) P.W[j][q] = (float)w[q];
+  }
+  for (int p = 0; p < Pk; ++p) {
+    catmull_rom_row(Pk, (int64_t)p * H + (Pk - 1), H, w);
+    for (int q = 0; q < Pk; ++q) P.WS[p][q] = (float)w[q];
+  }
+  // ---- optimiser ----
+  P.mode = cfg->mode;
+  P.n_elite = cfg->mode == SBS_NAIVE ? 1 : (cfg->mode == SBS_CEM ? cfg->n_elite : 0);
+  for (int a = 0; a < 3; ++a) {
+    const double s = (double)cfg->sigma_min_frac * (double)cfg->sigma[a];
+    P.var_floor[a] = (float)(s * s);
+  }
+  P.seed_lo = (uint32_t)(cfg->seed & 0xFFFFFFFFull);
+  P.seed_hi = (uint32_t)(cfg->seed >> 32);
+  P.robot_offset = cfg->robot_offset;
+  // ---- sharding and launch geometry ----
+  P.R = R;
+  P.K_global = cfg->n_samples;
+  P.k_begin = cfg->n_samples * cfg->rank / cfg->world;
+  P.K_local = cfg->n_samples * (cfg->rank + 1) / cfg->world - P.k_begin;
+  P.n_tiles = (int)((P.K_local + sbs::kBlock - 1) / sbs::kBlock);
+  {
+    const int occ = sbs::rollout_occupancy(Pk, cfg->mode == SBS_MPPI);
+    const int64_t slots = (int64_t)occ * c->sm_count;
+    P.n_cta = (int)std::max<int64_t>(1, std::min<int64_t>(P.n_tiles, slots / R));
+  }
+  P.part_c_stride = 1;
+  // ---- device buffers ----
+  const size_t RD = (size_t)R * D;
+  CKC(cudaMalloc(&c->d_mean, RD * sizeof(float)));
+  CKC(cudaMalloc(&c->d_var, RD * sizeof(float)));
+  CKC(cudaMalloc(&c->d_fidx, R * sizeof(int)));
+  CKC(cudaMalloc(&c->d_xref, (size_t)R * H * 12 * sizeof(float)));
+  CKC(cudaMemset(c->d_xref, 0, (size_t)R * H * 12 * sizeof(float)));
+  CKC(cudaMalloc(&c->d_J, (size_t)R * P.K_local * sizeof(float)));
+  CKC(cudaMalloc(&c->d_part, (size_t)R * P.n_cta * sbs::kPartStride * sizeof(float)));
+  if (cfg->world > 1)
+    CKC(cudaMalloc(&c->d_gather, (size_t)cfg->world * R * sbs::kPartStride * sizeof(float)));
+  if (P.n_elite > 0) CKC(cudaMalloc(&c->d_elite, (size_t)R * P.n_elite * sizeof(int64_t)));
+  CKC(cudaMalloc(&c->d_best, R * sizeof(int64_t)));
+  CKC(cudaMalloc(&c->d_status, R * sizeof(int)));
+  CKC(cudaMalloc(&c->d_in, R * sizeof(sbs_input)));
+  CKC(cudaMalloc(&c->d_out, R * sizeof(sbs_output)));
+  CKC(cudaMallocHost(&c->h_in, R * sizeof(sbs_input)));
+  CKC(cudaMallocHost(&c->h_out, R * sizeof(sbs_output)));
+  // initial distribution: mean (0, 0, m|g_z|/4) per leg and knot, var = sigma^2, freq_idx 0
+  {
+    std::vector<float> m(RD), v(RD);
+    const float fz = (float)(-(double)cfg->mass * (double)cfg->gravity[2] / 4.0);
+    for (size_t i = 0; i < RD; ++i) {
+      const int axis = (int)(i % D) % 3;
+      m[i] = axis == 2 ? fz : 0.0f;
+      v[i] = (float)((double)cfg->sigma[axis] * (double)cfg->sigma[axis]);
+    }
+    CKC(cudaMemcpy(c->d_mean, m.data(), RD * sizeof(float), cudaMemcpyHostToDevice));
+    CKC(cudaMemcpy(c->d_var, v.data(), RD * sizeof(float), cudaMemcpyHostToDevice));
+    CKC(cudaMemset(c->d_fidx, 0, R * sizeof(int)));
+  }
+  P.mean = c->d_mean;
+  P.var = c->d_var;
+  P.fidx = c->d_fidx;
+  P.xref = c->d_xref;
+  P.J = c->d_J;
+  P.part = c->d_part;
+  P.elite = c->d_elite;
+  P.best = c->d_best;
+  P.status = c->d_status;
+  c->ref_set.assign(R, 0);
+  // ---- NCCL (sample sharding) ----
+  if (cfg->world > 1) {
+    if (!g_nccl.load()) {
+      c->err = "world > 1 but libnccl.so.2 could not be loaded";
+      return bail(SBS_ERR_NCCL);
+    }
+    nccl_uid u;
+    memcpy(u.internal, cfg->nccl_id, 128);
+    int r2 = g_nccl.init_rank(&c->comm, cfg->world, u, cfg->rank);
+    if (r2 != 0) {
+      c->err = std::string("ncclCommInitRank: ") + (g_nccl.err ? g_nccl.err(r2) : "?");
+      return bail(SBS_ERR_NCCL);
+    }
+  }
+  CKC(cudaDeviceSynchronize());
+  *out = c;
+  return SBS_OK;
+#undef CKC
+}
+
+int sbs_set_reference(sbs_ctx* c, int32_t robot, const float* x_ref) {
+  if (!c || !x_ref) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (robot < 0 || robot >= c->P.R) return fail(c, SBS_ERR_INVALID_ARG, "robot out of range");
+  const int n = c->P.H * 12;
+  if (!finite_all(x_ref, n)) return fail(c, SBS_ERR_NONFINITE, "reference not finite");
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaMemcpyAsync(c->d_xref + (size_t)robot * n, x_ref, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->ref_set[robot] = 1;
+  return SBS_OK;
+}
+
+int sbs_set_reference_device(sbs_ctx* c, const float* d_x_ref, void* stream) {
+  if (!c || !d_x_ref) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaMemcpyAsync(c->d_xref, d_x_ref, (size_t)c->P.R * c->P.H * 12 * sizeof(float), cudaMemcpyDeviceToDevice,
+                     (cudaStream_t)stream));
+  std::fill(c->ref_set.begin(), c->ref_set.end(), 1);
+  return SBS_OK;
+}
+
+int sbs_set_distribution(sbs_ctx* c, int32_t robot, const float* mean, const float* var, int32_t freq_idx) {
+  if (!c || !mean || !var) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (robot < 0 || robot >= c->P.R) return fail(c, SBS_ERR_INVALID_ARG, "robot out of range");
+  if (freq_idx < 0 || freq_idx >= c->cfg.n_freq) return fail(c, SBS_ERR_INVALID_ARG, "freq_idx out of range");
+  const int D = c->P.D;
+  if (!finite_all(mean, D) || !finite_all(var, D)) return fail(c, SBS_ERR_NONFINITE, "distribution not finite");
+  for (int d = 0; d < D; ++d)
+    if (!(var[d] >= 0)) return fail(c, SBS_ERR_INVALID_ARG, "var must be >= 0");
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaMemcpyAsync(c->d_mean + (size_t)robot * D, mean, D * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->d_var + (size_t)robot * D, var, D * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->d_fidx + robot, &freq_idx, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return SBS_OK;
+}
+
+int sbs_get_distribution(sbs_ctx* c, int32_t robot, float* mean, float* var, int32_t* freq_idx) {
+  if (!c) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (robot < 0 || robot >= c->P.R) return fail(c, SBS_ERR_INVALID_ARG, "robot out of range");
+  const int D = c->P.D;
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaStreamSynchronize(c->stream));
+  if (mean) CK(cudaMemcpy(mean, c->d_mean + (size_t)robot * D, D * sizeof(float), cudaMemcpyDeviceToHost));
+  if (var) CK(cudaMemcpy(var, c->d_var + (size_t)robot * D, D * sizeof(float), cudaMemcpyDeviceToHost));
+  if (freq_idx) CK(cudaMemcpy(freq_idx, c->d_fidx + robot, sizeof(int), cudaMemcpyDeviceToHost));
+  return SBS_OK;
+}
+
+uint32_t sbs_get_iter(const sbs_ctx* c) { return c ? c->iter : 0u; }
+int sbs_set_iter(sbs_ctx* c, uint32_t iter) {
+  if (!c) return SBS_ERR_INVALID_ARG;
+  c->iter = iter;
+  return SBS_OK;
+}
+
+int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
+  if (!c || !in || !out) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  const int R = c->P.R;
+  for (int r = 0; r < R; ++r) {
+    if (!c->ref_set[r]) return fail(c, SBS_ERR_STATE, "sbs_set_reference not called for every robot");
+    if (!finite_all(in[r].x0, 12) || !finite_all(in[r].feet_cur, 12) || !finite_all(in[r].feet_next, 12))
+      return fail(c, SBS_ERR_NONFINITE, "non-finite x0 / feet");
+    if (!(fabsf(in[r].x0[7]) < 1.5697963267948966f)) return fail(c, SBS_ERR_SINGULAR, "|pitch(x0)| >= pi/2 - 1e-3");
+  }
+  CK(cudaSetDevice(c->cfg.device));
+  memcpy(c->h_in, in, R * sizeof(sbs_input));
+  cudaStream_t s = c->stream;
+  CK(cudaMemcpyAsync(c->d_in, c->h_in, R * sizeof(sbs_input), cudaMemcpyHostToDevice, s));
+  c->P.in = c->d_in;
+  c->P.out = c->d_out;
+  CK(cudaEventRecord(c->ev0, s));
+  int rc = enqueue_step(c, s);
+  if (rc != SBS_OK) return rc;
+  CK(cudaEventRecord(c->ev1, s));
+  CK(cudaMemcpyAsync(c->h_out, c->d_out, R * sizeof(sbs_output), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  int status = SBS_OK;
+  for (int r = 0; r < R; ++r) {
+    c->h_out[r].device_us = ms * 1000.f;
+    if (c->h_out[r].status == SBS_WARN_ALL_DIVERGED) status = SBS_WARN_ALL_DIVERGED;
+  }
+  memcpy(out, c->h_out, R * sizeof(sbs_output));
+  c->iter += 1;
+  return status;
+}
+
+int sbs_step_device(sbs_ctx* c, const sbs_input* d_in, sbs_output* d_out, void* stream) {
+  if (!c || !d_in || !d_out) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  for (int r = 0; r < c->P.R; ++r)
+    if (!c->ref_set[r]) return fail(c, SBS_ERR_STATE, "reference not set for every robot");
+  CK(cudaSetDevice(c->cfg.device));
+  c->P.in = d_in;
+  c->P.out = d_out;
+  int rc = enqueue_step(c, (cudaStream_t)stream);
+  if (rc != SBS_OK) return rc;
+  c->iter += 1;
+  return SBS_OK;
+}
+
+int sbs_get_state(sbs_ctx* c, void* buf, uint64_t* nbytes) {
+  if (!c || !nbytes) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  const int R = c->P.R, D = c->P.D;
+  const uint64_t need = 32 + (uint64_t)R * (2 * D * sizeof(float) + sizeof(int32_t));
+  if (!buf || *nbytes < need) {
+    *nbytes = need;
+    return buf ? fail(c, SBS_ERR_INVALID_ARG, "buffer too small") : SBS_OK;
+  }
+  *nbytes = need;
+  char* b = (char*)buf;
+  const uint64_t hdr[4] = {0x5342535354415445ull /*"SBSSTATE"*/, (uint64_t)c->iter, c->cfg.seed,
+                           ((uint64_t)R << 32) | (uint64_t)D};
+  memcpy(b, hdr, 32);
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(b + 32, c->d_mean, (size_t)R * D * sizeof(float), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(b + 32 + (size_t)R * D * 4, c->d_var, (size_t)R * D * sizeof(float), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(b + 32 + (size_t)R * D * 8, c->d_fidx, R * sizeof(int), cudaMemcpyDeviceToHost));
+  return SBS_OK;
+}
+
+int sbs_set_state(sbs_ctx* c, const void* buf, uint64_t nbytes) {
+  if (!c || !buf) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  const int R = c->P.R, D = c->P.D;
+  const uint64_t need = 32 + (uint64_t)R * (2 * D * sizeof(float) + sizeof(int32_t));
+  if (nbytes != need) return fail(c, SBS_ERR_INVALID_ARG, "state size mismatch");
+  const char* b = (const char*)buf;
+  uint64_t hdr[4];
+  memcpy(hdr, b, 32);
+  if (hdr[0] != 0x5342535354415445ull || hdr[2] != c->cfg.seed || hdr[3] != (((uint64_t)R << 32) | (uint64_t)D))
+    return fail(c, SBS_ERR_INVALID_ARG, "state does not match this context");
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(c->d_mean, b + 32, (size_t)R * D * sizeof(float), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_var, b + 32 + (size_t)R * D * 4, (size_t)R * D * sizeof(float), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_fidx, b + 32 + (size_t)R * D * 8, R * sizeof(int), cudaMemcpyHostToDevice));
+  c->iter = (uint32_t)hdr[1];
+  return SBS_OK;
+}
+
+int sbs_debug_samples(sbs_ctx* c, int32_t robot, int64_t k0, int64_t n, float* z, float* theta, int32_t* fidx) {
+  if (!c || n < 0 || k0 < 0) return fail(c, SBS_ERR_INVALID_ARG, "bad argument");
+  if (robot < 0 || robot >= c->P.R) return fail(c, SBS_ERR_INVALID_ARG, "robot out of range");
+  if (n == 0) return SBS_OK;
+  CK(cudaSetDevice(c->cfg.device));
+  const int D = c->P.D;
+  float *dz, *dth;
+  int* df;
+  CK(cudaMalloc(&dz, (size_t)n * D * sizeof(float)));
+  CK(cudaMalloc(&dth, (size_t)n * D * sizeof(float)));
+  CK(cudaMalloc(&df, (size_t)n * sizeof(int)));
+  Params P = c->P;
+  P.iter = c->iter;
+  // the debug kernel needs an sbs_input for load_robot: use a zero one
+  sbs_input* din;
+  CK(cudaMalloc(&din, (size_t)c->P.R * sizeof(sbs_input)));
+  CK(cudaMemset(din, 0, (size_t)c->P.R * sizeof(sbs_input)));
+  P.in = din;
+  cudaError_t e = sbs::launch_debug_samples(P, robot, k0, n, dz, dth, df, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && z) e = cudaMemcpy(z, dz, (size_t)n * D * sizeof(float), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && theta) e = cudaMemcpy(theta, dth, (size_t)n * D * sizeof(float), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && fidx) e = cudaMemcpy(fidx, df, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(dz);
+  cudaFree(dth);
+  cudaFree(df);
+  cudaFree(din);
+  if (e != cudaSuccess) return cuda_fail(c, e, "sbs_debug_samples");
+  return SBS_OK;
+}
+
+int sbs_debug_costs(sbs_ctx* c, float* J) {
+  if (!c || !J) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(J, c->d_J, (size_t)c->P.R * c->P.K_local * sizeof(float), cudaMemcpyDeviceToHost));
+  return SBS_OK;
+}
+
+int sbs_debug_elites(sbs_ctx* c, int32_t robot, int64_t* idx) {
+  if (!c || !idx) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (c->P.n_elite < 1) return fail(c, SBS_ERR_STATE, "no elites in MPPI mode");
+  if (robot < 0 || robot >= c->P.R) return fail(c, SBS_ERR_INVALID_ARG, "robot out of range");
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(idx, c->d_elite + (size_t)robot * c->P.n_elite, c->P.n_elite * sizeof(int64_t),
+                cudaMemcpyDeviceToHost));
+  return SBS_OK;
+}
+
+int sbs_debug_select(const float* J, int64_t K, int64_t K_e, int64_t* idx, int32_t device) {
+  sbs_ctx* c = nullptr;
+  if (!J || !idx || K < 1 || K_e < 1 || K_e > K || K > 0x7fffffffLL)
+    return fail(nullptr, SBS_ERR_INVALID_ARG, "bad argument");
+  CK(cudaSetDevice(device));
+  float* dJ;
+  int64_t *di, *db;
+  CK(cudaMalloc(&dJ, K * sizeof(float)));
+  CK(cudaMalloc(&di, K_e * sizeof(int64_t)));
+  CK(cudaMalloc(&db, sizeof(int64_t)));
+  cudaError_t e = cudaMemcpy(dJ, J, K * sizeof(float), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = sbs::launch_select_raw(dJ, K, K_e, di, db, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(idx, di, K_e * sizeof(int64_t), cudaMemcpyDeviceToHost);
+  cudaFree(dJ);
+  cudaFree(di);
+  cudaFree(db);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "sbs_debug_select");
+  return SBS_OK;
+}
+
+int sbs_local_range(const sbs_ctx* c, int64_t* k_begin, int64_t* K_local) {
+  if (!c || !k_begin || !K_local) return SBS_ERR_INVALID_ARG;
+  *k_begin = c->P.k_begin;
+  *K_local = c->P.K_local;
+  return SBS_OK;
+}
+
+int sbs_profile(sbs_ctx* c, int32_t enable) {
+  if (!c) return SBS_ERR_INVALID_ARG;
+  c->profile = enable != 0;
+  return SBS_OK;
+}
+
+int sbs_kernel_times(sbs_ctx* c, double* total_ms, int64_t* launches) {
+  if (!c) return SBS_ERR_INVALID_ARG;
+  CK(cudaSetDevice(c->cfg.device));
+  for (auto& pd : c->pending) {
+    CK(cudaEventSynchronize(pd.b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, pd.a, pd.b));
+    c->kt[pd.kernel] += ms;
+    c->kl[pd.kernel] += 1;
+    c->free_events.push_back(pd.a);
+    c->free_events.push_back(pd.b);
+  }
+  c->pending.clear();
+  for (int k = 0; k < SBS_NKERNELS; ++k) {
+    if (total_ms) total_ms[k] = c->kt[k];
+    if (launches) launches[k] = c->kl[k];
+    c->kt[k] = 0;
+    c->kl[k] = 0;
+  }
+  return SBS_OK;
+}
+
+int sbs_launches_per_step(const sbs_ctx* c) {
+  if (!c) return 0;
+  if (c->cfg.mode == SBS_MPPI) return c->cfg.world > 1 ? 3 : 2;
+  return 3;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// sbs_internal.h -- shared between the host runtime (sbs_api.cpp) and the
+// kernels (sbs_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sbs.h"
+
+namespace sbs {
+
+constexpr int kBlock = 128;         // samples per tile = threads per rollout CTA
+constexpr int kPartStride = 112;    // floats per MPPI partial record (8 header + SBS_MAX_D, padded)
+constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, nfin, pad]
+
+// Everything a kernel needs, passed by value (__grid_constant__, < 4 KB).
+struct Params {
+  // --- model (Eq. 1) ---
+  float inv_mass;
+  float g[3];
+  float I[9], Iinv[9];
+  int diag_inertia;
+  float mu, fz_min, fz_max;
+  float dt;
+  // --- cost ---
+  float Q[12], Rw[12];
+  float rho, f_nominal, w_fc, inv_lambda;
+  float urz[5];               // u^r_z = -m g_z / max(1, n_stance)   (L12)
+  // --- gait ---
+  uint32_t inc[SBS_MAX_FREQ]; // Q0.32 phase increment per step for each frequency option
+  float freq_hz[SBS_MAX_FREQ];
+  uint32_t off[4];            // Q0.32 leg offsets
+  uint32_t thr;               // stance iff phase < thr ...
+  int all_stance;             // ... or always when D_f = 1 (thr = 2^32)
+  int n_freq, gait_adapt, elite_preserve, warm_shift;
+  // --- spline tables ---
+  int H, P, D;
+  float W[SBS_MAX_HORIZON][SBS_MAX_KNOTS];   // Gamma_j = sum_p W[j][p] theta[p]  (Catmull-Rom + phantoms)
+  float WS[SBS_MAX_KNOTS][SBS_MAX_KNOTS];    // warm shift: mu'[p] = sum_q WS[p][q] mu[q]
+  // --- optimiser ---
+  int mode;
+  int64_t n_elite;
+  float var_floor[3];
+  // --- noise ---
+  uint32_t seed_lo, seed_hi;
+  uint32_t iter;
+  int robot_offset;
+  // --- sizes / sharding ---
+  int R;
+  int64_t K_global, k_begin, K_local;
+  int n_tiles, n_cta;         // per robot
+  int part_c_stride;          // 1: CTA partials [R][n_cta]; R: NCCL-gathered rank partials [world][R]
+  // --- device buffers ---
+  float* mean;                // [R][D]
+  float* var;                 // [R][D]
+  int* fidx;                  // [R]
+  const float* xref;          // [R][H][12]
+  const sbs_input* in;        // [R]
+  sbs_output* out;            // [R]
+  float* J;                   // [R][K_local]
+  float* part;                // [R][n_cta][kPartStride]
+  int64_t* elite;             // [R][n_elite]
+  int64_t* best;              // [R] global index of rank-1 sample (CEM/Naive)
+  int* status;                // [R]
+};
+
+// launchers (sbs_kernels.cu); return cudaGetLastError()
+cudaError_t launch_rollout(const Params& p, bool mppi, cudaStream_t s);
+cudaError_t launch_mppi_finalize(const Params& p, cudaStream_t s);
+// merge this rank's CTA partials into one record per robot at dst[R][kPartStride]
+cudaError_t launch_mppi_merge(const Params& p, float* dst, cudaStream_t s);
+cudaError_t launch_select(const Params& p, cudaStream_t s);
+cudaError_t launch_elite(const Params& p, cudaStream_t s);
+cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
+                                 int* fidx, cudaStream_t s);
+cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, int64_t* best,
+                              cudaStream_t s);
+int rollout_occupancy(int P, bool mppi);  // resident CTAs per SM of the rollout kernel
+
+}  // namespace sbs
