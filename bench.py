@@ -35,14 +35,14 @@ H = 12
 # Algorithmic FP32 FLOPs per sample-step of the rollout kernel:
 # FP32 adds/muls/FMAs (FMA = 2) of the round-1 kernel formulation, counted by ncu
 # (sm__sass_thread_inst_executed_op_{fadd,fmul,ffma}_pred_on) at config 2, frozen.
-ALG_FLOP_PER_SAMPLE_STEP = 1008.0
+ALG_FLOP_PER_SAMPLE_STEP = 794.0
 FP32_LANES_PER_SM = 128
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=10000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="sbs", choices=["sbs", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=500)

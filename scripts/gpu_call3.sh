@@ -1,0 +1,10 @@
+set -x
+python bench.py --steps 2000 --warmup 50 > gpurun_out/bench.log 2>&1; echo bench rc=$?
+tail -3 gpurun_out/bench.log
+python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 10 > gpurun_out/plain_small.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 10 > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
+python scripts/profile_step.py --workload c2 > gpurun_out/plain_c2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:sbs_rollout -s 3 -c 1 -o gpurun_out/prof_c2_rollout python scripts/profile_step.py --workload c2 > gpurun_out/ncu_c2.log 2>&1; echo ncu2 rc=$?
+python scripts/profile_step.py --workload c4 --steps 3 > gpurun_out/plain_c4.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:sbs_rollout -s 1 -c 1 -o gpurun_out/prof_c4_rollout python scripts/profile_step.py --workload c4 --steps 3 > gpurun_out/ncu_c4.log 2>&1; echo ncu3 rc=$?
+ls -la gpurun_out
