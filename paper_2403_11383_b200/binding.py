@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsbs.so")
+LIB_PATH = os.environ.get("SBS_LIB_PATH", os.path.join(HERE, "libsbs.so"))  # override: experiments only
 
 SBS_MAX_KNOTS = 8
 SBS_MAX_D = 12 * SBS_MAX_KNOTS

@@ -10,6 +10,8 @@
 #include <math.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <string>
@@ -73,10 +75,12 @@ struct sbs_ctx {
   float* d_xref = nullptr;
   float* d_J = nullptr;
   float* d_part = nullptr;
-  float* d_gather = nullptr;  // [world][R][kPartStride] (world > 1)
+  float* d_gather = nullptr;  // [world][R][part_stride] (world > 1)
   int64_t* d_elite = nullptr;
   int64_t* d_best = nullptr;
   int* d_status = nullptr;
+  int* d_counter = nullptr;
+  float* d_epart = nullptr;
   sbs_input* d_in = nullptr;
   sbs_output* d_out = nullptr;
   sbs_input* h_in = nullptr;   // pinned
@@ -230,26 +234,22 @@ cudaError_t timed(sbs_ctx* c, int kernel, cudaStream_t s, F&& launch) {
 int enqueue_step(sbs_ctx* c, cudaStream_t s) {
   Params& P = c->P;
   P.iter = c->iter;
-  const bool mppi = c->cfg.mode == SBS_MPPI;
-  CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, mppi, s); }));
-  if (mppi) {
-    if (c->cfg.world == 1) {
-      CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_finalize(P, s); }));
-    } else {
-      // rank partial -> all-gather -> merge of the `world` partials in rank order
-      Params Q = P;
-      Q.out = nullptr;
-      CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_merge(Q, c->d_gather + (size_t)c->cfg.rank * P.R * sbs::kPartStride, s); }));
-      const size_t n = (size_t)P.R * sbs::kPartStride;
-      int rc = g_nccl.all_gather(c->d_gather + (size_t)c->cfg.rank * n, c->d_gather, n, kNcclFloat32, c->comm, s);
-      if (rc != 0) return fail(c, SBS_ERR_NCCL, std::string("ncclAllGather: ") + (g_nccl.err ? g_nccl.err(rc) : "?"));
-      Params F = P;
-      F.part = c->d_gather;
-      F.n_cta = c->cfg.world;
-      F.part_c_stride = P.R;  // gathered layout [world][R][stride]
-      CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_finalize(F, s); }));
-    }
-  } else {
+  const int mode = c->cfg.mode;
+  const bool fused = c->cfg.world == 1;
+  CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, mode, fused, s); }));
+  if (mode == SBS_MPPI && !fused) {
+    // rank partial -> all-gather -> merge of the `world` partials in rank order
+    const size_t n = (size_t)P.R * P.part_stride;
+    float* mine = c->d_gather + (size_t)c->cfg.rank * n;
+    CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_merge(P, mine, s); }));
+    int rc = g_nccl.all_gather(mine, c->d_gather, n, kNcclFloat32, c->comm, s);
+    if (rc != 0) return fail(c, SBS_ERR_NCCL, std::string("ncclAllGather: ") + (g_nccl.err ? g_nccl.err(rc) : "?"));
+    Params F = P;
+    F.part = c->d_gather;
+    F.n_cta = c->cfg.world;
+    F.part_c_stride = P.R;  // gathered layout [world][R][stride]
+    CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_finalize(F, s); }));
+  } else if (mode == SBS_CEM) {
     CK(timed(c, SBS_KERNEL_SELECT, s, [&] { return sbs::launch_select(P, s); }));
     CK(timed(c, SBS_KERNEL_ELITE, s, [&] { return sbs::launch_elite(P, s); }));
   }
@@ -298,7 +298,7 @@ void sbs_destroy(sbs_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
   for (void* p : {(void*)c->d_mean, (void*)c->d_var, (void*)c->d_fidx, (void*)c->d_xref, (void*)c->d_J,
-                  (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status,
+                  (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart,
                   (void*)c->d_in, (void*)c->d_out})
     if (p) cudaFree(p);
   if (c->h_in) cudaFreeHost(c->h_in);
@@ -422,11 +422,12 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.K_local = cfg->n_samples * (cfg->rank + 1) / cfg->world - P.k_begin;
   P.n_tiles = (int)((P.K_local + sbs::kBlock - 1) / sbs::kBlock);
   {
-    const int occ = sbs::rollout_occupancy(Pk, cfg->mode == SBS_MPPI);
+    const int occ = sbs::rollout_occupancy(Pk, cfg->mode);
     const int64_t slots = (int64_t)occ * c->sm_count;
     P.n_cta = (int)std::max<int64_t>(1, std::min<int64_t>(P.n_tiles, slots / R));
   }
   P.part_c_stride = 1;
+  P.part_stride = sbs::kPartHdr + D;
   // ---- device buffers ----
   const size_t RD = (size_t)R * D;
   CKC(cudaMalloc(&c->d_mean, RD * sizeof(float)));
@@ -435,12 +436,16 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaMalloc(&c->d_xref, (size_t)R * H * 12 * sizeof(float)));
   CKC(cudaMemset(c->d_xref, 0, (size_t)R * H * 12 * sizeof(float)));
   CKC(cudaMalloc(&c->d_J, (size_t)R * P.K_local * sizeof(float)));
-  CKC(cudaMalloc(&c->d_part, (size_t)R * P.n_cta * sbs::kPartStride * sizeof(float)));
+  CKC(cudaMalloc(&c->d_part, (size_t)R * P.n_cta * P.part_stride * sizeof(float)));
   if (cfg->world > 1)
-    CKC(cudaMalloc(&c->d_gather, (size_t)cfg->world * R * sbs::kPartStride * sizeof(float)));
+    CKC(cudaMalloc(&c->d_gather, (size_t)cfg->world * R * P.part_stride * sizeof(float)));
   if (P.n_elite > 0) CKC(cudaMalloc(&c->d_elite, (size_t)R * P.n_elite * sizeof(int64_t)));
   CKC(cudaMalloc(&c->d_best, R * sizeof(int64_t)));
   CKC(cudaMalloc(&c->d_status, R * sizeof(int)));
+  CKC(cudaMalloc(&c->d_counter, 2 * R * sizeof(int)));
+  CKC(cudaMemset(c->d_counter, 0, 2 * R * sizeof(int)));
+  P.n_eblk = P.n_elite > 0 ? (int)((P.n_elite + 31) / 32) : 1;  // 32 elites per elite-kernel CTA
+  CKC(cudaMalloc(&c->d_epart, (size_t)R * P.n_eblk * sbs::kEPartStride * sizeof(float)));
   CKC(cudaMalloc(&c->d_in, R * sizeof(sbs_input)));
   CKC(cudaMalloc(&c->d_out, R * sizeof(sbs_output)));
   CKC(cudaMallocHost(&c->h_in, R * sizeof(sbs_input)));
@@ -467,6 +472,9 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.elite = c->d_elite;
   P.best = c->d_best;
   P.status = c->d_status;
+  P.counter = c->d_counter;
+  P.ecounter = c->d_counter + R;
+  P.epart = c->d_epart;
   c->ref_set.assign(R, 0);
   // ---- NCCL (sample sharding) ----
   if (cfg->world > 1) {
@@ -687,17 +695,15 @@ int sbs_debug_select(const float* J, int64_t K, int64_t K_e, int64_t* idx, int32
     return fail(nullptr, SBS_ERR_INVALID_ARG, "bad argument");
   CK(cudaSetDevice(device));
   float* dJ;
-  int64_t *di, *db;
+  int64_t* di;
   CK(cudaMalloc(&dJ, K * sizeof(float)));
   CK(cudaMalloc(&di, K_e * sizeof(int64_t)));
-  CK(cudaMalloc(&db, sizeof(int64_t)));
   cudaError_t e = cudaMemcpy(dJ, J, K * sizeof(float), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = sbs::launch_select_raw(dJ, K, K_e, di, db, 0);
+  if (e == cudaSuccess) e = sbs::launch_select_raw(dJ, K, K_e, di, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaMemcpy(idx, di, K_e * sizeof(int64_t), cudaMemcpyDeviceToHost);
   cudaFree(dJ);
   cudaFree(di);
-  cudaFree(db);
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "sbs_debug_select");
   return SBS_OK;
 }
@@ -739,8 +745,8 @@ int sbs_kernel_times(sbs_ctx* c, double* total_ms, int64_t* launches) {
 
 int sbs_launches_per_step(const sbs_ctx* c) {
   if (!c) return 0;
-  if (c->cfg.mode == SBS_MPPI) return c->cfg.world > 1 ? 3 : 2;
-  return 3;
+  if (c->cfg.mode == SBS_MPPI) return c->cfg.world > 1 ? 3 : 1;
+  return c->cfg.mode == SBS_NAIVE ? 1 : 3;
 }
 
 }  // extern "C"

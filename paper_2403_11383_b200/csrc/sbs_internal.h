@@ -9,8 +9,12 @@
 namespace sbs {
 
 constexpr int kBlock = 128;         // samples per tile = threads per rollout CTA
-constexpr int kPartStride = 112;    // floats per MPPI partial record (8 header + SBS_MAX_D, padded)
 constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, nfin, pad]
+constexpr int kEPartStride = 2 * SBS_MAX_D + 4;  // CEM elite-moment record [S1[D], n, S2[D]]
+#ifndef SBS_ROLLOUT_MIN_BLOCKS
+#define SBS_ROLLOUT_MIN_BLOCKS 3
+#endif
+constexpr int kRolloutMinBlocks = SBS_ROLLOUT_MIN_BLOCKS;  // __launch_bounds__ min CTAs per SM
 
 // Everything a kernel needs, passed by value (__grid_constant__, < 4 KB).
 struct Params {
@@ -48,6 +52,7 @@ struct Params {
   int R;
   int64_t K_global, k_begin, K_local;
   int n_tiles, n_cta;         // per robot
+  int part_stride;             // floats per partial record = kPartHdr + D (tight, 16-byte multiple)
   int part_c_stride;          // 1: CTA partials [R][n_cta]; R: NCCL-gathered rank partials [world][R]
   // --- device buffers ---
   float* mean;                // [R][D]
@@ -57,23 +62,27 @@ struct Params {
   const sbs_input* in;        // [R]
   sbs_output* out;            // [R]
   float* J;                   // [R][K_local]
-  float* part;                // [R][n_cta][kPartStride]
+  float* part;                // [R][n_cta][part_stride]
   int64_t* elite;             // [R][n_elite]
   int64_t* best;              // [R] global index of rank-1 sample (CEM/Naive)
   int* status;                // [R]
+  int* counter;               // [R] CTA arrival counters of the fused rollout tail (re-armed to 0)
+  int* ecounter;              // [R] arrival counters of the elite kernel
+  float* epart;               // [R][n_eblk][kEPartStride] CEM elite-moment records
+  int n_eblk;                 // elite blocks per robot
 };
 
 // launchers (sbs_kernels.cu); return cudaGetLastError()
-cudaError_t launch_rollout(const Params& p, bool mppi, cudaStream_t s);
+// mode: SBS_MPPI (fused: merge + finish in the last CTA), SBS_NAIVE (always fused), SBS_CEM (records only)
+cudaError_t launch_rollout(const Params& p, int mode, bool fused, cudaStream_t s);
 cudaError_t launch_mppi_finalize(const Params& p, cudaStream_t s);
-// merge this rank's CTA partials into one record per robot at dst[R][kPartStride]
+// merge this rank's CTA partials into one record per robot at dst[R][part_stride]
 cudaError_t launch_mppi_merge(const Params& p, float* dst, cudaStream_t s);
 cudaError_t launch_select(const Params& p, cudaStream_t s);
 cudaError_t launch_elite(const Params& p, cudaStream_t s);
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                  int* fidx, cudaStream_t s);
-cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, int64_t* best,
-                              cudaStream_t s);
-int rollout_occupancy(int P, bool mppi);  // resident CTAs per SM of the rollout kernel
+cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s);
+int rollout_occupancy(int P, int mode);  // resident CTAs per SM of the rollout kernel
 
 }  // namespace sbs

@@ -101,6 +101,23 @@ __device__ __forceinline__ int draw_sample(const Params& p, uint32_t robot_g, in
   return idx;
 }
 
+// One Philox block q (4 coordinates d = 4q..4q+3) of sample k: theta2 values.
+// Same recipe and rounding as draw_sample, so results are bitwise identical.
+__device__ __forceinline__ void sample_block(const Params& p, uint32_t robot_g, int64_t k, int q,
+                                             const RobotSmem& s, float (&th4)[4]) {
+  if (p.elite_preserve && k == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) th4[i] = s.mu[4 * q + i];
+    return;
+  }
+  const U4 w = philox4x32_10((uint32_t)q, (uint32_t)k, p.iter, robot_g, p.seed_lo, p.seed_hi);
+  float z[4];
+  box_muller(w.x, w.y, z[0], z[1]);
+  box_muller(w.z, w.w, z[2], z[3]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) th4[i] = __fmaf_rn(s.sig[4 * q + i], z[i], s.mu[4 * q + i]);
+}
+
 // Eq. 1 angular part at one RK4 stage (L24): given world torque tau_w,
 //   w' = I^-1 (R^T tau_w - w x I w),  Phi' = E'^-1(Phi) w.
 __device__ __forceinline__ void ang_deriv(const Params& p, float phi, float th, float psi, float wx, float wy,
@@ -287,139 +304,52 @@ __device__ float rollout(const Params& p, const float (&th)[12 * P], int fi, con
   return (bad || !(J <= FLT_MAX)) ? kInf : J;
 }
 
-// (J, k) lexicographic min helpers for argmin with lowest-index tie-break
+
+// (J, k) lexicographic order: argmin with lowest-index tie-break (L4, L5)
 __device__ __forceinline__ bool jk_less(float ja, int ka, float jb, int kb) {
   return ja < jb || (ja == jb && ka < kb);
 }
 
-// ---------------------------------------------------------------------------
-// sbs_rollout_kernel: grid (n_cta, R), block kBlock; CTA c processes tiles
-// c, c + n_cta, ... of its robot's K_local samples.
-// ---------------------------------------------------------------------------
-template <int P, bool MPPI>
-__global__ void __launch_bounds__(kBlock) sbs_rollout_kernel(const __grid_constant__ Params p) {
-  constexpr int D = 12 * P;
-  constexpr int NR = D + 4;  // reduced rows: w theta[D], w, w^2, J (finite), 1 (finite)
-  __shared__ RobotSmem s;
-  extern __shared__ float s_red[];  // [NR][kBlock + 1]   (MPPI only)
-  __shared__ float s_wm[kBlock / 32];
-  __shared__ int s_wk[kBlock / 32], s_wf[kBlock / 32];
-  __shared__ float s_tile_m, s_run_m;
-  __shared__ int s_tile_k, s_tile_f, s_run_k, s_run_f;
-
-  const int r = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  load_robot(p, r, s);
-  if (tid == 0) {
-    s_run_m = kInf;
-    s_run_k = 0x7fffffff;
-    s_run_f = 0;
+__device__ __forceinline__ void warp_argmin(float& m, int& mk, int& mf) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const int k2 = __shfl_xor_sync(0xffffffffu, mk, o);
+    const int f2 = __shfl_xor_sync(0xffffffffu, mf, o);
+    if (jk_less(m2, k2, m, mk)) {
+      m = m2;
+      mk = k2;
+      mf = f2;
+    }
   }
-  __syncthreads();
-  const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
-  float run = 0.0f;  // running partial of row `tid` (MPPI)
+}
 
-  for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-    const int64_t kl = (int64_t)tile * kBlock + tid;
-    const bool valid = kl < p.K_local;
-    const int64_t k = p.k_begin + kl;
-    float th[D];
-    float J = kInf;
-    int fi = 0;
-    if (valid) {
-      fi = draw_sample<P, false>(p, robot_g, k, s, th);
-      J = rollout<P>(p, th, fi, s);
-      p.J[(size_t)r * p.K_local + kl] = J;
-    }
-    if (!MPPI) continue;
-    // ---- step a5, per tile: min, weights, sums (online softmax merge) ----
-    float m = J;
-    int mk = valid ? (int)k : 0x7fffffff, mf = fi;
+// Partial record of (robot r, part c): CTA partials [R][n_cta] (part_c_stride = 1)
+// or NCCL-gathered rank partials [world][R] (part_c_stride = R, n_cta = world).
+//   [0] min J  [1] k_argmin  [2] theta1 of argmin  [3] S = sum w  [4] S2 = sum w^2
+//   [5] sum of finite J  [6] number finite  [7] 0  [8 ..] V = sum w theta2
+__device__ __forceinline__ const float* part_rec(const Params& p, int r, int c) {
+  return p.part_c_stride == 1 ? p.part + ((size_t)r * p.n_cta + c) * p.part_stride
+                              : p.part + ((size_t)c * p.part_c_stride + r) * p.part_stride;
+}
+
+// cooperative copy of n floats (n % 4 == 0, 16-byte aligned) from L2 to shared
+// memory, 4 independent 16-byte loads in flight per thread
+__device__ __forceinline__ void stage_copy(float* dst, const float* src, int n) {
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  const int n4 = n >> 2;
+  for (int i0 = threadIdx.x; i0 < n4; i0 += 4 * blockDim.x) {
+    float4 v[4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-      const int k2 = __shfl_xor_sync(0xffffffffu, mk, o);
-      const int f2 = __shfl_xor_sync(0xffffffffu, mf, o);
-      if (jk_less(m2, k2, m, mk)) {
-        m = m2;
-        mk = k2;
-        mf = f2;
-      }
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n4) v[u] = __ldcg(s4 + i);
     }
-    if (lane == 0) {
-      s_wm[warp] = m;
-      s_wk[warp] = mk;
-      s_wf[warp] = mf;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      float bm = s_wm[0];
-      int bk = s_wk[0], bf = s_wf[0];
-      for (int w = 1; w < kBlock / 32; ++w)
-        if (jk_less(s_wm[w], s_wk[w], bm, bk)) {
-          bm = s_wm[w];
-          bk = s_wk[w];
-          bf = s_wf[w];
-        }
-      s_tile_m = bm;
-      s_tile_k = bk;
-      s_tile_f = bf;
-    }
-    __syncthreads();
-    const float mt = s_tile_m;
-    const bool fin = J < kInf;
-    const float w = fin ? __expf((mt - J) * p.inv_lambda) : 0.0f;
-    if (valid) {
 #pragma unroll
-      for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = w * th[d];
-    } else {
-#pragma unroll
-      for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = 0.0f;
-    }
-    s_red[(D + 0) * (kBlock + 1) + tid] = w;
-    s_red[(D + 1) * (kBlock + 1) + tid] = w * w;
-    s_red[(D + 2) * (kBlock + 1) + tid] = fin ? J : 0.0f;
-    s_red[(D + 3) * (kBlock + 1) + tid] = fin ? 1.0f : 0.0f;
-    __syncthreads();
-    const float mr = s_run_m;
-    const float mn = fminf(mr, mt);
-    if (tid < NR) {
-      const float* row = &s_red[tid * (kBlock + 1)];
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 8
-      for (int i = 0; i < kBlock; i += 4) {
-        a0 += row[i];
-        a1 += row[i + 1];
-        a2 += row[i + 2];
-        a3 += row[i + 3];
-      }
-      const float v = (a0 + a1) + (a2 + a3);
-      const float sa = (mr < kInf) ? __expf((mn - mr) * p.inv_lambda) : 0.0f;
-      const float sb = (mt < kInf) ? __expf((mn - mt) * p.inv_lambda) : 0.0f;
-      if (tid < D + 1) run = fmaf(run, sa, v * sb);
-      else if (tid == D + 1) run = fmaf(run, sa * sa, v * (sb * sb));
-      else run += v;
-    }
-    __syncthreads();
-    if (tid == 0 && jk_less(mt, s_tile_k, s_run_m, s_run_k)) {
-      s_run_m = mt;
-      s_run_k = s_tile_k;
-      s_run_f = s_tile_f;
-    }
-    __syncthreads();
-  }
-  if (MPPI) {
-    float* out = p.part + ((size_t)r * p.n_cta + blockIdx.x) * kPartStride;
-    if (tid < D) out[kPartHdr + tid] = run;
-    else if (tid == D) out[3] = run;
-    else if (tid == D + 1) out[4] = run;
-    else if (tid == D + 2) out[5] = run;
-    else if (tid == D + 3) out[6] = run;
-    if (tid == 0) {
-      out[0] = s_run_m;
-      out[1] = __int_as_float(s_run_k);
-      out[2] = __int_as_float(s_run_f);
-      out[7] = 0.0f;
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n4) d4[i] = v[u];
     }
   }
 }
@@ -462,111 +392,371 @@ __device__ void write_output(const Params& p, int r, int status, const float* me
   }
 }
 
-// ---------------------------------------------------------------------------
-// sbs_mppi_finalize: grid R, block 128.  beta = min over CTA partials; each
-// partial rescaled by exp(-(m_c - beta)/lambda) (Alg. 4 UpdateMean).
-// ---------------------------------------------------------------------------
-// Partial records: CTA partials [R][n_cta] (part_c_stride = 1) or the rank
-// partials gathered by NCCL [world][R] (part_c_stride = R, n_cta = world).
-__device__ __forceinline__ const float* part_rec(const Params& p, int r, int c) {
-  return p.part_c_stride == 1 ? p.part + ((size_t)r * p.n_cta + c) * kPartStride
-                              : p.part + ((size_t)c * p.part_c_stride + r) * kPartStride;
-}
-
-template <bool EMIT>
-__global__ void __launch_bounds__(128) sbs_mppi_finalize(const __grid_constant__ Params p, float* emit) {
-  const int r = blockIdx.x, tid = threadIdx.x, D = p.D;
-  __shared__ float s_m[4];
-  __shared__ int s_k[4], s_f[4];
-  __shared__ float s_row[SBS_MAX_D + 4];
-  __shared__ float s_mean[SBS_MAX_D], s_var[SBS_MAX_D];
+// Block-wide argmin over the partial headers of robot r.
+struct Best {
+  float m;
+  int k, f;
+};
+__device__ Best merge_argmin(const Params& p, int r) {
+  __shared__ float s_m[32];
+  __shared__ int s_k[32], s_f[32];
   float m = kInf;
   int mk = 0x7fffffff, mf = 0;
-  for (int c = tid; c < p.n_cta; c += blockDim.x) {
+  for (int c = threadIdx.x; c < p.n_cta; c += blockDim.x) {
     const float* pc = part_rec(p, r, c);
-    const float mc = pc[0];
-    const int kc = __float_as_int(pc[1]);
+    const float mc = __ldcg(pc);
+    const int kc = __float_as_int(__ldcg(pc + 1));
     if (jk_less(mc, kc, m, mk)) {
       m = mc;
       mk = kc;
-      mf = __float_as_int(pc[2]);
+      mf = __float_as_int(__ldcg(pc + 2));
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-    const int k2 = __shfl_xor_sync(0xffffffffu, mk, o);
-    const int f2 = __shfl_xor_sync(0xffffffffu, mf, o);
-    if (jk_less(m2, k2, m, mk)) {
-      m = m2;
-      mk = k2;
-      mf = f2;
-    }
-  }
-  if ((tid & 31) == 0) {
-    s_m[tid >> 5] = m;
-    s_k[tid >> 5] = mk;
-    s_f[tid >> 5] = mf;
+  warp_argmin(m, mk, mf);
+  if ((threadIdx.x & 31) == 0) {
+    s_m[threadIdx.x >> 5] = m;
+    s_k[threadIdx.x >> 5] = mk;
+    s_f[threadIdx.x >> 5] = mf;
   }
   __syncthreads();
-  float beta = s_m[0];
-  int bk = s_k[0], bf = s_f[0];
-  for (int w = 1; w < 4; ++w)
-    if (jk_less(s_m[w], s_k[w], beta, bk)) {
-      beta = s_m[w];
-      bk = s_k[w];
-      bf = s_f[w];
-    }
-  // rows: 0..D-1 -> V, D -> S, D+1 -> S2, D+2 -> sumJ, D+3 -> nfin
-  if (tid < D + 4) {
-    const int col = tid < D ? kPartHdr + tid : 3 + (tid - D);
-    float acc = 0.0f;
-    for (int c = 0; c < p.n_cta; ++c) {
-      const float* pc = part_rec(p, r, c);
-      const float mc = pc[0];
-      float sc = (mc < kInf) ? __expf((beta - mc) * p.inv_lambda) : 0.0f;
-      if (tid == D + 1) sc = sc * sc;
-      if (tid >= D + 2) sc = 1.0f;
-      acc = fmaf(pc[col], sc, acc);
-    }
-    s_row[tid] = acc;
-  }
+  Best b{s_m[0], s_k[0], s_f[0]};
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+    if (jk_less(s_m[w], s_k[w], b.m, b.k)) b = Best{s_m[w], s_k[w], s_f[w]};
   __syncthreads();
-  if (EMIT) {  // this rank's merged partial, relative to its own beta
-    float* o = emit + (size_t)r * kPartStride;
-    if (tid < D) o[kPartHdr + tid] = s_row[tid];
-    else if (tid < D + 4) o[3 + tid - D] = s_row[tid];
+  return b;
+}
+
+// ---------------------------------------------------------------------------
+// MPPI UpdateMean (Alg. 4) over the partial records of robot r:
+// beta = min_c m_c; every record is rescaled by exp(-(m_c - beta)/lambda);
+// theta_new = sum V / sum S.  EMIT: write the merged record (rank partial)
+// instead of finishing.  blockDim.x = 128; rows split over two column groups.
+// ---------------------------------------------------------------------------
+template <bool EMIT>
+__device__ void mppi_merge_block(const Params& p, int r, float* emit, float* stage, int stage_floats) {
+  const int tid = threadIdx.x, D = p.D, NR = D + 4, RL = p.part_stride;
+  __shared__ float s_row[1][SBS_MAX_D + 4];
+  __shared__ float s_sc[128];
+  __shared__ float s_mean[SBS_MAX_D], s_var[SBS_MAX_D];
+  const Best b = merge_argmin(p, r);
+  const float beta = b.m;
+  const int nc = p.n_cta;
+  const int CH = min(128, max(1, stage_floats / RL));
+  float acc = 0.f;  // thread tid < NR owns row tid: 0..D-1 V, D S, D+1 S2, D+2 sumJ, D+3 nfin
+  for (int c0 = 0; c0 < nc; c0 += CH) {
+    const int n = min(CH, nc - c0);
+    if (p.part_c_stride == 1) {
+      stage_copy(stage, part_rec(p, r, c0), n * RL);  // records of a robot are contiguous
+    } else {
+      for (int c = 0; c < n; ++c) stage_copy(stage + c * RL, part_rec(p, r, c0 + c), RL);
+    }
+    __syncthreads();
+    for (int c = tid; c < n; c += blockDim.x) {
+      const float mc = stage[c * RL];
+      s_sc[c] = (mc < kInf) ? __expf((beta - mc) * p.inv_lambda) : 0.0f;
+    }
+    __syncthreads();
+    if (tid < NR) {
+      const int col = tid < D ? kPartHdr + tid : 3 + (tid - D);
+      const int kind = tid < D + 1 ? 0 : (tid == D + 1 ? 1 : 2);
+      float a0 = 0.f, a1 = 0.f;
+      int c = 0;
+      for (; c + 1 < n; c += 2) {
+        float s0 = s_sc[c], s1 = s_sc[c + 1];
+        if (kind == 1) { s0 *= s0; s1 *= s1; }
+        if (kind == 2) { s0 = 1.f; s1 = 1.f; }
+        a0 = fmaf(stage[c * RL + col], s0, a0);
+        a1 = fmaf(stage[(c + 1) * RL + col], s1, a1);
+      }
+      if (c < n) {
+        float s0 = kind == 2 ? 1.f : s_sc[c];
+        if (kind == 1) s0 *= s0;
+        a0 = fmaf(stage[c * RL + col], s0, a0);
+      }
+      acc += a0 + a1;
+    }
+    __syncthreads();
+  }
+  if (tid < NR) s_row[0][tid] = acc;
+  __syncthreads();
+  if (EMIT) {  // this rank's merged record, relative to its own beta
+    float* o = emit + (size_t)r * p.part_stride;
+    if (tid < D) o[kPartHdr + tid] = s_row[0][tid];
+    else if (tid < NR) o[3 + tid - D] = s_row[0][tid];
     if (tid == 0) {
       o[0] = beta;
-      o[1] = __int_as_float(bk);
-      o[2] = __int_as_float(bf);
+      o[1] = __int_as_float(b.k);
+      o[2] = __int_as_float(b.f);
       o[7] = 0.0f;
     }
     return;
   }
   const bool all_div = !(beta < kInf);
-  const float S = s_row[D], S2 = s_row[D + 1], sumJ = s_row[D + 2], nfin = s_row[D + 3];
+  const float S = s_row[0][D], S2 = s_row[0][D + 1], sumJ = s_row[0][D + 2], nfin = s_row[0][D + 3];
   float* mean = p.mean + (size_t)r * D;
   const float* var = p.var + (size_t)r * D;
   for (int d = tid; d < D; d += blockDim.x) {
-    s_mean[d] = all_div ? mean[d] : s_row[d] / S;
+    s_mean[d] = all_div ? mean[d] : s_row[0][d] / S;
     s_var[d] = var[d];
   }
+  const int fi = all_div ? p.fidx[r] : b.f;
   __syncthreads();
   for (int d = tid; d < D; d += blockDim.x) mean[d] = s_mean[d];
-  const int fi = all_div ? p.fidx[r] : bf;
-  __syncthreads();
   if (tid == 0) p.fidx[r] = fi;
-  const float K = (float)p.K_global;
   write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, beta,
-               nfin > 0.f ? sumJ / nfin : kInf, S, all_div ? 0.f : S * S / S2, (int)(K - nfin));
+               nfin > 0.f ? sumJ / nfin : kInf, S, all_div ? 0.f : S * S / S2, (int)((float)p.K_global - nfin));
+}
+
+// Naive UpdateMean (Alg. 3): the best sample theta* becomes the mean,
+// regenerated from the counter RNG; C unchanged.
+template <int P>
+__device__ void naive_finalize_block(const Params& p, int r, const RobotSmem& s) {
+  constexpr int D = 12 * P;
+  __shared__ float s_mean[D], s_var[D];
+  __shared__ float s_sum[2];
+  const int tid = threadIdx.x;
+  const Best b = merge_argmin(p, r);
+  if (tid < 32) {
+    float sj = 0.f, nf = 0.f;
+    for (int c = tid; c < p.n_cta; c += 32) {
+      const float* pc = part_rec(p, r, c);
+      sj += __ldcg(pc + 5);
+      nf += __ldcg(pc + 6);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sj += __shfl_xor_sync(0xffffffffu, sj, o);
+      nf += __shfl_xor_sync(0xffffffffu, nf, o);
+    }
+    if (tid == 0) {
+      s_sum[0] = sj;
+      s_sum[1] = nf;
+    }
+  }
+  const bool all_div = !(b.m < kInf);
+  float* mean = p.mean + (size_t)r * D;
+  if (!all_div && tid < D / 4) {  // theta* regenerated, one Philox block per thread
+    float th4[4];
+    sample_block(p, (uint32_t)(p.robot_offset + r), b.k, tid, s, th4);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s_mean[4 * tid + i] = th4[i];
+  }
+  __syncthreads();
+  for (int d = tid; d < D; d += blockDim.x) {
+    if (all_div) s_mean[d] = mean[d];
+    s_var[d] = p.var[(size_t)r * D + d];
+  }
+  const int fi = all_div ? p.fidx[r] : b.f;
+  __syncthreads();
+  for (int d = tid; d < D; d += blockDim.x) mean[d] = s_mean[d];
+  if (tid == 0) {
+    p.fidx[r] = fi;
+    p.elite[r] = (int64_t)b.k;
+    p.best[r] = (int64_t)b.k;
+  }
+  const float nf = s_sum[1];
+  write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, b.m,
+               nf > 0.f ? s_sum[0] / nf : kInf, all_div ? 0.f : 1.f, all_div ? 0.f : 1.f,
+               (int)((float)p.K_global - nf));
+}
+
+// last CTA of a grid row (robot) to arrive returns true (threadfence pattern)
+__device__ __forceinline__ bool arrive_last(int* counter, int n) {
+  __shared__ int s_last;
+  __syncthreads();  // the CTA's record writes happen-before thread 0's fence (fences are cumulative)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = (atomicAdd(counter, 1) == n - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *counter = 0;  // re-arm for the next launch (stream-ordered)
+  }
+  return s_last;
+}
+
+// ---------------------------------------------------------------------------
+// sbs_rollout_kernel: grid (n_cta, R), block kBlock.  CTA c processes tiles c,
+// c + n_cta, ... of its robot's K_local samples and leaves one partial record.
+//   EPI_MPPI:   online (min, sum w, sum w^2, sum w theta) over its samples
+//   EPI_ARGMIN: (J, k) argmin + finite-cost sum/count (Naive, CEM)
+// FUSED: the last CTA of each robot merges the records and finishes the
+// iteration (MPPI, Naive): one launch per MPC iteration.
+// ---------------------------------------------------------------------------
+enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
+
+template <int P, int EPI, bool FUSED>
+__global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(const __grid_constant__ Params p) {
+  constexpr int D = 12 * P;
+  constexpr int NR = D + 4;  // reduced rows (MPPI): w theta[D], w, w^2, J (finite), 1 (finite)
+  __shared__ RobotSmem s;
+  extern __shared__ float s_red[];  // [NR][kBlock + 1]   (MPPI only)
+  __shared__ float s_wm[kBlock / 32], s_ws[kBlock / 32], s_wn[kBlock / 32];
+  __shared__ int s_wk[kBlock / 32], s_wf[kBlock / 32];
+  __shared__ float s_tile_m, s_run_m, s_run_sj, s_run_nf;
+  __shared__ int s_tile_k, s_tile_f, s_run_k, s_run_f;
+
+  const int r = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  load_robot(p, r, s);
+  if (tid == 0) {
+    s_run_m = kInf;
+    s_run_k = 0x7fffffff;
+    s_run_f = 0;
+    s_run_sj = 0.f;
+    s_run_nf = 0.f;
+  }
+  __syncthreads();
+  const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
+  float run = 0.0f;  // running partial of row `tid` (MPPI)
+
+  for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    const int64_t kl = (int64_t)tile * kBlock + tid;
+    const bool valid = kl < p.K_local;
+    const int64_t k = p.k_begin + kl;
+    float th[D];
+    float J = kInf;
+    int fi = 0;
+    if (valid) {
+      fi = draw_sample<P, false>(p, robot_g, k, s, th);
+      J = rollout<P>(p, th, fi, s);
+      p.J[(size_t)r * p.K_local + kl] = J;
+    }
+    // ---- per-tile argmin (J, k) ----
+    float m = J;
+    int mk = valid ? (int)k : 0x7fffffff, mf = fi;
+    warp_argmin(m, mk, mf);
+    const bool fin = J < kInf;
+    if (EPI == EPI_ARGMIN) {
+      float sj = fin ? J : 0.f, nf = fin ? 1.f : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sj += __shfl_xor_sync(0xffffffffu, sj, o);
+        nf += __shfl_xor_sync(0xffffffffu, nf, o);
+      }
+      if (lane == 0) {
+        s_wm[warp] = m;
+        s_wk[warp] = mk;
+        s_wf[warp] = mf;
+        s_ws[warp] = sj;
+        s_wn[warp] = nf;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 0; w < kBlock / 32; ++w) {
+          if (jk_less(s_wm[w], s_wk[w], s_run_m, s_run_k)) {
+            s_run_m = s_wm[w];
+            s_run_k = s_wk[w];
+            s_run_f = s_wf[w];
+          }
+          s_run_sj += s_ws[w];
+          s_run_nf += s_wn[w];
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+    // ---- step a5 (MPPI), per tile: weights relative to the tile min, then an
+    //      online-softmax merge into this CTA's running record ----
+    if (lane == 0) {
+      s_wm[warp] = m;
+      s_wk[warp] = mk;
+      s_wf[warp] = mf;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      float bm = s_wm[0];
+      int bk = s_wk[0], bf = s_wf[0];
+      for (int w = 1; w < kBlock / 32; ++w)
+        if (jk_less(s_wm[w], s_wk[w], bm, bk)) {
+          bm = s_wm[w];
+          bk = s_wk[w];
+          bf = s_wf[w];
+        }
+      s_tile_m = bm;
+      s_tile_k = bk;
+      s_tile_f = bf;
+    }
+    __syncthreads();
+    const float mt = s_tile_m;
+    const float w = fin ? __expf((mt - J) * p.inv_lambda) : 0.0f;
+    if (valid) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = w * th[d];
+    } else {
+#pragma unroll
+      for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = 0.0f;
+    }
+    s_red[(D + 0) * (kBlock + 1) + tid] = w;
+    s_red[(D + 1) * (kBlock + 1) + tid] = w * w;
+    s_red[(D + 2) * (kBlock + 1) + tid] = fin ? J : 0.0f;
+    s_red[(D + 3) * (kBlock + 1) + tid] = fin ? 1.0f : 0.0f;
+    __syncthreads();
+    const float mr = s_run_m;
+    const float mn = fminf(mr, mt);
+    if (tid < NR) {
+      const float* rowp = &s_red[tid * (kBlock + 1)];
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 8
+      for (int i = 0; i < kBlock; i += 4) {
+        a0 += rowp[i];
+        a1 += rowp[i + 1];
+        a2 += rowp[i + 2];
+        a3 += rowp[i + 3];
+      }
+      const float v = (a0 + a1) + (a2 + a3);
+      const float sa = (mr < kInf) ? __expf((mn - mr) * p.inv_lambda) : 0.0f;
+      const float sb = (mt < kInf) ? __expf((mn - mt) * p.inv_lambda) : 0.0f;
+      if (tid < D + 1) run = fmaf(run, sa, v * sb);
+      else if (tid == D + 1) run = fmaf(run, sa * sa, v * (sb * sb));
+      else run += v;
+    }
+    __syncthreads();
+    if (tid == 0 && jk_less(mt, s_tile_k, s_run_m, s_run_k)) {
+      s_run_m = mt;
+      s_run_k = s_tile_k;
+      s_run_f = s_tile_f;
+    }
+    __syncthreads();
+  }
+  float* out = p.part + ((size_t)r * p.n_cta + blockIdx.x) * p.part_stride;
+  if (EPI == EPI_MPPI) {
+    if (tid < D) out[kPartHdr + tid] = run;
+    else if (tid < NR) out[3 + tid - D] = run;
+  } else if (tid == 0) {
+    out[3] = 0.f;
+    out[4] = 0.f;
+    out[5] = s_run_sj;
+    out[6] = s_run_nf;
+  }
+  if (tid == 0) {
+    out[0] = s_run_m;
+    out[1] = __int_as_float(s_run_k);
+    out[2] = __int_as_float(s_run_f);
+    out[7] = 0.0f;
+  }
+  if (FUSED) {
+    if (arrive_last(p.counter + r, gridDim.x)) {
+      if (EPI == EPI_MPPI) mppi_merge_block<false>(p, r, nullptr, s_red, NR * (kBlock + 1));
+      else naive_finalize_block<P>(p, r, s);
+    }
+  }
+}
+
+// stand-alone merge (world > 1: rank partial before / final merge after the all-gather)
+template <bool EMIT>
+__global__ void __launch_bounds__(128) sbs_mppi_finalize(const __grid_constant__ Params p, float* emit) {
+  __shared__ float stage[4096];
+  mppi_merge_block<EMIT>(p, blockIdx.x, emit, stage, 4096);
 }
 
 // ---------------------------------------------------------------------------
 // Elite selection (a6; Alg. 1 lines 3-5, L4): the K_e smallest keys (J, k).
-// Radix select on order-preserving 32-bit keys of J (NaN -> +inf, -0 -> +0),
-// four 8-bit passes in shared memory, then an index-ordered compaction that
-// takes all keys < T and the lowest-index ties == T.  One CTA per robot.
+// Radix select on order-preserving 32-bit keys of J (NaN -> +inf, -0 -> +0):
+// four 8-bit passes with warp-aggregated shared-memory histograms and a
+// parallel digit search, then an index-ordered compaction that takes all
+// keys < T and the lowest-index ties == T.  One CTA per robot.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t cost_key(float J) {
   if (J != J) J = kInf;
@@ -576,241 +766,371 @@ __device__ __forceinline__ uint32_t cost_key(float J) {
 }
 
 constexpr int kSelBlock = 1024;
-constexpr int kEliteBlock = 512;  // <= 128 registers per thread: theta[D] and acc[D] stay resident
+constexpr int kHistPad = 257;                       // per-warp histogram stride (bank-conflict free)
+constexpr int kSelHistWords = (kSelBlock / 32) * kHistPad;
+constexpr int kSelSmemBytes = 200 * 1024;           // dynamic shared memory of the select kernels
+constexpr int kSelSmemKeys = kSelSmemBytes / 4 - kSelHistWords;
 
-// returns via smem: elite[0..K_e) ascending global indices, best (rank-1),
-// diag[0..2] = (J_min, mean finite J, n diverged)
+// smem: [kSelHistWords] per-warp histograms, then the keys when K <= kSelSmemKeys
 __device__ void select_block(const float* J, int64_t K, int64_t K_e, int64_t k_begin, int64_t* elite,
-                             int64_t* best, float* diag) {
-  __shared__ uint32_t hist[256];
+                             uint32_t* smem) {
   __shared__ uint32_t s_prefix, s_want;
   __shared__ uint32_t s_wsum[kSelBlock / 32];
-  __shared__ unsigned long long s_best;
-  __shared__ float s_sum[kSelBlock / 32];
-  __shared__ int s_nf[kSelBlock / 32];
+  uint32_t* whist = smem;
+  uint32_t* keys = smem + kSelHistWords;
+  const bool staged = K <= kSelSmemKeys;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = blockDim.x >> 5;
   if (tid == 0) {
     s_prefix = 0;
     s_want = (uint32_t)K_e;
-    s_best = ~0ull;
   }
-  // diagnostics + best
-  unsigned long long b = ~0ull;
-  float sj = 0.f;
-  int nf = 0;
-  for (int64_t k = tid; k < K; k += blockDim.x) {
-    const float j = J[k];
-    const unsigned long long kk = ((unsigned long long)cost_key(j) << 32) | (unsigned long long)k;
-    b = kk < b ? kk : b;
-    if (j < kInf) {
-      sj += j;
-      nf += 1;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, b, o);
-    b = b2 < b ? b2 : b;
-    sj += __shfl_xor_sync(0xffffffffu, sj, o);
-    nf += __shfl_xor_sync(0xffffffffu, nf, o);
-  }
-  if (lane == 0) {
-    s_sum[warp] = sj;
-    s_nf[warp] = nf;
-  }
-  __syncthreads();
-  if (lane == 0) atomicMin(&s_best, b);
-  if (tid == 0) {
-    float t = 0.f;
-    int n = 0;
-    for (int w = 0; w < kSelBlock / 32; ++w) {
-      t += s_sum[w];
-      n += s_nf[w];
-    }
-    diag[1] = n > 0 ? t / n : kInf;
-    diag[2] = (float)(K - n);
-  }
-  // four radix passes, most significant digit first
+  if (staged)
+    for (int64_t k = tid; k < K; k += blockDim.x) keys[k] = cost_key(J[k]);
   for (int pass = 0; pass < 4; ++pass) {
     const int shift = 24 - 8 * pass;
     const uint32_t hmask = pass == 0 ? 0u : (0xFFFFFFFFu << (shift + 8));
-    for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+    for (int i = tid; i < nw * kHistPad; i += blockDim.x) whist[i] = 0;
     __syncthreads();
-    const uint32_t prefix = s_prefix;
-    for (int64_t k = tid; k < K; k += blockDim.x) {
-      const uint32_t key = cost_key(J[k]);
-      if ((key & hmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    const uint32_t prefix = s_prefix, want = s_want;
+    uint32_t* my = whist + warp * kHistPad;
+    const int64_t K_round = ((K + 31) / 32) * 32;
+    for (int64_t k = tid; k < K_round; k += blockDim.x) {
+      uint32_t dgt = 0xFFFFFFFFu;
+      if (k < K) {
+        const uint32_t key = staged ? keys[k] : cost_key(J[k]);
+        if ((key & hmask) == prefix) dgt = (key >> shift) & 255u;
+      }
+      // up to 3 leader rounds absorb the dominant digits with one atomic each (costs
+      // cluster in a few bins in the high passes), the rest add directly
+      unsigned act = __ballot_sync(0xffffffffu, dgt != 0xFFFFFFFFu);
+#pragma unroll
+      for (int it = 0; it < 3 && act; ++it) {
+        const int leader = __ffs(act) - 1;
+        const uint32_t d = __shfl_sync(0xffffffffu, dgt, leader);
+        const unsigned m = __ballot_sync(0xffffffffu, dgt == d) & act;
+        if (lane == leader) atomicAdd(&my[d], (uint32_t)__popc(m));
+        if (m & (1u << lane)) dgt = 0xFFFFFFFFu;
+        act &= ~m;
+      }
+      if (dgt != 0xFFFFFFFFu) atomicAdd(&my[dgt], 1u);
     }
     __syncthreads();
-    if (tid == 0) {
-      uint32_t want = s_want, cum = 0;
-      int dgt = 0;
-      for (; dgt < 256; ++dgt) {
-        if (cum + hist[dgt] >= want) break;
-        cum += hist[dgt];
+    // sum the warp histograms per bin, inclusive scan over the 256 bins, find the bin of rank `want`
+    if (tid < 256) {
+      uint32_t h = 0;
+      for (int w = 0; w < nw; ++w) h += whist[w * kHistPad + tid];
+      uint32_t x = h;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
       }
-      s_want = want - cum;
-      s_prefix = prefix | ((uint32_t)dgt << shift);
+      if (lane == 31) s_wsum[warp] = x;
+      whist[tid] = x - h;  // exclusive prefix within the warp (bins of warp 0's histogram are no longer needed)
+      whist[256] = 0;
+    }
+    __syncthreads();
+    if (tid < 256) {
+      uint32_t off = 0;
+      for (int w = 0; w < warp; ++w) off += s_wsum[w];
+      const uint32_t excl = whist[tid] + off;
+      const uint32_t incl = (tid & 31) == 31 ? s_wsum[warp] + off : whist[tid + 1] + off;
+      if (excl < want && want <= incl) {  // exactly one bin
+        s_prefix = prefix | ((uint32_t)tid << shift);
+        s_want = want - excl;
+      }
     }
     __syncthreads();
   }
   const uint32_t T = s_prefix;
   const uint32_t n_eq = s_want;  // ties at T to take, lowest indices first
-  // index-ordered compaction
   uint32_t sel_base = 0, eq_base = 0;
   for (int64_t base = 0; base < K; base += blockDim.x) {
     const int64_t k = base + tid;
-    uint32_t key = 0xFFFFFFFFu;
     bool lt = false, eq = false;
     if (k < K) {
-      key = cost_key(J[k]);
+      const uint32_t key = staged ? keys[k] : cost_key(J[k]);
       lt = key < T;
       eq = key == T;
     }
-    // exclusive scan of eq within the block
     const unsigned eqb = __ballot_sync(0xffffffffu, eq);
-    if (lane == 0) s_wsum[warp] = __popc(eqb);
+    const unsigned ltb = __ballot_sync(0xffffffffu, lt);
+    if (lane == 0) s_wsum[warp] = __popc(eqb) | ((uint32_t)__popc(ltb) << 16);
     __syncthreads();
     uint32_t eq_before = eq_base + __popc(eqb & ((1u << lane) - 1u));
-    uint32_t eq_tot = 0;
-    for (int w = 0; w < kSelBlock / 32; ++w) {
+    uint32_t lt_before = __popc(ltb & ((1u << lane) - 1u));
+    uint32_t eq_tot = 0, lt_tot = 0;
+    for (int w = 0; w < nw; ++w) {
       const uint32_t c = s_wsum[w];
-      if (w < warp) eq_before += c;
-      eq_tot += c;
+      if (w < warp) {
+        eq_before += c & 0xFFFFu;
+        lt_before += c >> 16;
+      }
+      eq_tot += c & 0xFFFFu;
+      lt_tot += c >> 16;
     }
+    // selected = lt, or eq within the first n_eq ties; position = number selected before me
+    const uint32_t eq_sel_chunk0 = eq_base < n_eq ? eq_base : n_eq;
+    const uint32_t eq_sel_before_me = (eq_before < n_eq ? eq_before : n_eq) - eq_sel_chunk0;
     const bool sel = lt || (eq && eq_before < n_eq);
-    __syncthreads();
-    const unsigned sb = __ballot_sync(0xffffffffu, sel);
-    if (lane == 0) s_wsum[warp] = __popc(sb);
-    __syncthreads();
-    uint32_t pos = sel_base + __popc(sb & ((1u << lane) - 1u));
-    uint32_t sel_tot = 0;
-    for (int w = 0; w < kSelBlock / 32; ++w) {
-      const uint32_t c = s_wsum[w];
-      if (w < warp) pos += c;
-      sel_tot += c;
-    }
-    if (sel) elite[pos] = k_begin + k;
-    sel_base += sel_tot;
-    eq_base += eq_tot;
+    if (sel) elite[sel_base + lt_before + eq_sel_before_me] = k_begin + k;
+    const uint32_t eq_end = eq_base + eq_tot;
+    sel_base += lt_tot + ((eq_end < n_eq ? eq_end : n_eq) - eq_sel_chunk0);
+    eq_base = eq_end;
     __syncthreads();
   }
-  if (tid == 0) {
-    const unsigned long long bb = s_best;
-    *best = k_begin + (int64_t)(bb & 0xFFFFFFFFull);
-    const uint32_t key = (uint32_t)(bb >> 32);
-    const uint32_t u = (key & 0x80000000u) ? (key & 0x7FFFFFFFu) : ~key;
-    diag[0] = __uint_as_float(u);
+}
+
+// Fast path for K <= kSelSmallMax: every thread keeps a contiguous run of at most
+// 16 keys in registers.  Two passes over 16-bit digits (65536 packed 16-bit
+// counters in 128 KB of shared memory) give the exact K_e-th smallest key T and
+// the number of ties at T to take; one block scan of per-thread (lt, eq) counts
+// then places the elites in index order.
+constexpr int kSelSmallMax = 16384;
+constexpr int kSelKPT = kSelSmallMax / kSelBlock;
+constexpr int kSelSmallSmemBytes = 32768 * 4;
+
+// exclusive block scan of v over kSelBlock threads; returns the total in *tot
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_w, uint32_t* tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = s_w[lane];
+    uint32_t wx = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wx, o);
+      if (lane >= o) wx += y;
+    }
+    s_w[lane] = wx - w;       // exclusive warp offsets
+    if (lane == 31) s_w[32] = wx;
   }
   __syncthreads();
+  const uint32_t r = s_w[warp] + x - v;
+  *tot = s_w[32];
+  __syncthreads();
+  return r;
+}
+
+// 16-bit digit pass: count keys with (key & pmask) == pref by digit (key >> sh) & 0xFFFF,
+// find digit B with rank `want` inside; returns B and the count strictly below it.
+__device__ void digit16_pass(const uint32_t (&key)[kSelKPT], int nk, uint32_t pmask, uint32_t pref, int sh,
+                             uint32_t want, uint32_t* hist, uint32_t* s_w, uint32_t* s_res) {
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 32768; i += kSelBlock) hist[i] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kSelKPT; ++i)
+    if (i < nk && (key[i] & pmask) == pref) {
+      const uint32_t d = (key[i] >> sh) & 0xFFFFu;
+      atomicAdd(&hist[d >> 1], 1u << ((d & 1u) << 4));
+    }
+  __syncthreads();
+  // thread t owns digits [64 t, 64 t + 64)
+  uint32_t loc = 0;
+  for (int w = 0; w < 32; ++w) {
+    const uint32_t h = hist[tid * 32 + ((w + tid) & 31)];  // rotated start: no bank conflicts
+    loc += (h & 0xFFFFu) + (h >> 16);
+  }
+  uint32_t tot;
+  const uint32_t base = block_excl_scan(loc, s_w, &tot);
+  if (base < want && want <= base + loc) {
+    uint32_t cum = base;
+    for (int w = 0; w < 32; ++w) {
+      const uint32_t h = hist[tid * 32 + w];
+      const uint32_t c0 = h & 0xFFFFu, c1 = h >> 16;
+      if (cum + c0 >= want) {
+        s_res[0] = (uint32_t)(tid * 64 + 2 * w);
+        s_res[1] = cum;
+        break;
+      }
+      cum += c0;
+      if (cum + c1 >= want) {
+        s_res[0] = (uint32_t)(tid * 64 + 2 * w + 1);
+        s_res[1] = cum;
+        break;
+      }
+      cum += c1;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void select_block_small(const float* J, int K, int K_e, int64_t k_begin, int64_t* elite, uint32_t* hist) {
+  __shared__ uint32_t s_w[33];
+  __shared__ uint32_t s_res[2];
+  const int tid = threadIdx.x;
+  const int per = (K + kSelBlock - 1) / kSelBlock;
+  const int k0 = tid * per;
+  const int nk = max(0, min(per, K - k0));
+  uint32_t key[kSelKPT];
+#pragma unroll
+  for (int i = 0; i < kSelKPT; ++i) key[i] = i < nk ? cost_key(J[k0 + i]) : 0xFFFFFFFFu;
+  digit16_pass(key, nk, 0u, 0u, 16, (uint32_t)K_e, hist, s_w, s_res);
+  const uint32_t hi = s_res[0], below_hi = s_res[1];
+  digit16_pass(key, nk, 0xFFFF0000u, hi << 16, 0, (uint32_t)K_e - below_hi, hist, s_w, s_res);
+  const uint32_t T = (hi << 16) | s_res[0];
+  const uint32_t n_eq = (uint32_t)K_e - below_hi - s_res[1];  // ties at T to take, lowest indices first
+  uint32_t lt = 0, eq = 0;
+#pragma unroll
+  for (int i = 0; i < kSelKPT; ++i)
+    if (i < nk) {
+      lt += key[i] < T;
+      eq += key[i] == T;
+    }
+  uint32_t t1, t2;
+  const uint32_t lt_before = block_excl_scan(lt, s_w, &t1);
+  uint32_t eq_before = block_excl_scan(eq, s_w, &t2);
+  uint32_t pos = lt_before + min(eq_before, n_eq);
+#pragma unroll
+  for (int i = 0; i < kSelKPT; ++i)
+    if (i < nk) {
+      const bool take = key[i] < T || (key[i] == T && eq_before++ < n_eq);
+      if (take) elite[pos++] = k_begin + k0 + i;
+    }
 }
 
 __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_constant__ Params p) {
+  extern __shared__ uint32_t sel_smem[];
   const int r = blockIdx.x;
-  select_block(p.J + (size_t)r * p.K_local, p.K_local, p.n_elite, p.k_begin, p.elite + (size_t)r * p.n_elite,
-               p.best + r, p.part + (size_t)r * kPartStride);
+  if (p.K_local <= kSelSmallMax)
+    select_block_small(p.J + (size_t)r * p.K_local, (int)p.K_local, (int)p.n_elite, p.k_begin,
+                       p.elite + (size_t)r * p.n_elite, sel_smem);
+  else
+    select_block(p.J + (size_t)r * p.K_local, p.K_local, p.n_elite, p.k_begin, p.elite + (size_t)r * p.n_elite,
+                 sel_smem);
 }
 
 __global__ void __launch_bounds__(kSelBlock) sbs_select_raw_kernel(const float* J, int64_t K, int64_t K_e,
-                                                                   int64_t* idx, int64_t* best, float* diag) {
-  select_block(J, K, K_e, 0, idx, best, diag);
+                                                                   int64_t* idx) {
+  extern __shared__ uint32_t sel_smem[];
+  if (K <= kSelSmallMax)
+    select_block_small(J, (int)K, (int)K_e, 0, idx, sel_smem);
+  else
+    select_block(J, K, K_e, 0, idx, sel_smem);
 }
 
 // ---------------------------------------------------------------------------
-// sbs_elite_kernel: grid R, block kEliteBlock.  Elite moments from theta
-// regenerated with the counter RNG (no theta buffer in HBM).
+// sbs_elite_kernel (CEM, Alg. 1 UpdateMean / UpdateCov, L17): grid (n_eblk, R),
+// block 32 x 3P: warp q regenerates Philox block q (coordinates 4q..4q+3) of
+// the CTA's 32 elites from the counter RNG (no theta buffer in HBM), then
+// reduces shifted moments about mu' over its lanes: S1 = sum (theta - mu'),
+// S2 = sum (theta - mu')^2.  The last CTA of a robot merges the records in
+// order and finishes: mean = mu' + S1/n, var = max(S2/n - (S1/n)^2, floor).
 // ---------------------------------------------------------------------------
-template <int P>
-__device__ void block_sum_rows(float (&v)[12 * P], float* s_acc /*[32][12P]*/, float* out /*[12P]*/) {
-  constexpr int D = 12 * P;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    float x = v[d];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) s_acc[warp * D + d] = x;
-  }
-  __syncthreads();
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    float t = 0.f;
-    for (int w = 0; w < nw; ++w) t += s_acc[w * D + d];
-    out[d] = t;
-  }
-  __syncthreads();
-}
+constexpr int kEliteGroup = 32;  // elites per CTA
 
 template <int P>
-__global__ void __launch_bounds__(kEliteBlock) sbs_elite_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_constant__ Params p) {
   constexpr int D = 12 * P;
   __shared__ RobotSmem s;
-  __shared__ float s_acc[(kEliteBlock / 32) * D];
-  __shared__ float s_mean[D], s_var[D], s_sum[D];
-  __shared__ int s_n[kEliteBlock / 32];
-  __shared__ int s_best_f;
-  const int r = blockIdx.x, tid = threadIdx.x;
+  __shared__ float s_mean[D], s_var[D];
+  __shared__ float s_tot[2 * D + 1];
+  __shared__ __align__(16) float s_stage[16 * kEPartStride];
+  __shared__ float s_diag[2];
+  const int r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
   load_robot(p, r, s);
   __syncthreads();
   const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
-  const int64_t* el = p.elite + (size_t)r * p.n_elite;
+  const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
   const float* Jr = p.J + (size_t)r * p.K_local;
-  const float* diag = p.part + (size_t)r * kPartStride;
-  const int64_t kb = p.best[r];
-  const bool cem = p.mode == SBS_CEM;
-  const bool all_div = !(Jr[kb - p.k_begin] < kInf);
-  float th[D];
-  float acc[D];
-  // pass 1: elite sum and count of finite elites
+  float dev[4] = {0.f, 0.f, 0.f, 0.f};
+  float n = 0.f;
+  if (e < p.n_elite) {
+    const int64_t k = p.elite[(size_t)r * p.n_elite + e];
+    if (Jr[k - p.k_begin] < kInf) {  // diverged samples never enter the moments (L17)
+      float th4[4];
+      sample_block(p, robot_g, k, q, s, th4);
 #pragma unroll
-  for (int d = 0; d < D; ++d) acc[d] = 0.f;
-  int n = 0;
-  for (int64_t e = tid; e < p.n_elite; e += blockDim.x) {
-    const int64_t k = el[e];
-    if (!(Jr[k - p.k_begin] < kInf)) continue;  // diverged samples never enter the moments (L17)
-    draw_sample<P, false>(p, robot_g, k, s, th);
-#pragma unroll
-    for (int d = 0; d < D; ++d) acc[d] += th[d];
-    ++n;
-  }
-  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-  if ((tid & 31) == 0) s_n[tid >> 5] = n;
-  block_sum_rows<P>(acc, s_acc, s_sum);
-  int ntot = 0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) ntot += s_n[w];
-  for (int d = tid; d < D; d += blockDim.x) s_mean[d] = all_div ? p.mean[(size_t)r * D + d] : s_sum[d] / (float)ntot;
-  __syncthreads();
-  if (cem && !all_div) {
-    // pass 2: diagonal population variance about the elite mean, floored (L17)
-#pragma unroll
-    for (int d = 0; d < D; ++d) acc[d] = 0.f;
-    for (int64_t e = tid; e < p.n_elite; e += blockDim.x) {
-      const int64_t k = el[e];
-      if (!(Jr[k - p.k_begin] < kInf)) continue;
-      draw_sample<P, false>(p, robot_g, k, s, th);
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        const float dv = th[d] - s_mean[d];
-        acc[d] = fmaf(dv, dv, acc[d]);
-      }
+      for (int i = 0; i < 4; ++i) dev[i] = th4[i] - s.mu[4 * q + i];
+      n = 1.f;
     }
-    block_sum_rows<P>(acc, s_acc, s_sum);
-    for (int d = tid; d < D; d += blockDim.x) s_var[d] = fmaxf(s_sum[d] / (float)ntot, p.var_floor[d % 3]);
-  } else {
-    for (int d = tid; d < D; d += blockDim.x) s_var[d] = p.var[(size_t)r * D + d];
   }
-  if (tid == 0) {
-    int f = s.cur_idx;
-    if (!all_div) f = draw_sample<P, false>(p, robot_g, kb, s, th);  // theta1 of the rank-1 sample (L16)
-    s_best_f = f;
+  float* rec = p.epart + ((size_t)r * gridDim.x + blockIdx.x) * kEPartStride;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float a = dev[i], b2 = dev[i] * dev[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b2 += __shfl_xor_sync(0xffffffffu, b2, o);
+    }
+    if (lane == 0) {
+      rec[4 * q + i] = a;
+      rec[D + 1 + 4 * q + i] = b2;
+    }
+  }
+  if (q == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) rec[D] = n;
+  }
+  if (!arrive_last(p.ecounter + r, gridDim.x)) return;
+  // ---- last CTA: merge the elite records in order, finish the iteration ----
+  {
+    float a0 = 0.f;  // row tid (2D + 1 <= blockDim = 3D / 4 * 32 / 12 ... = 8D)
+    for (int b0 = 0; b0 < (int)gridDim.x; b0 += 16) {
+      const int nb = min(16, (int)gridDim.x - b0);
+      stage_copy(s_stage, p.epart + ((size_t)r * gridDim.x + b0) * kEPartStride, nb * kEPartStride);
+      __syncthreads();
+      if (tid < 2 * D + 1)
+        for (int b = 0; b < nb; ++b) a0 += s_stage[b * kEPartStride + tid];
+      __syncthreads();
+    }
+    if (tid < 2 * D + 1) s_tot[tid] = a0;
+  }
+  const Best b = merge_argmin(p, r);  // rank-1 sample and diagnostics from the rollout records
+  if (tid < 32) {
+    float sj = 0.f, nf = 0.f;
+    for (int c = tid; c < p.n_cta; c += 32) {
+      const float* pc = part_rec(p, r, c);
+      sj += __ldcg(pc + 5);
+      nf += __ldcg(pc + 6);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sj += __shfl_xor_sync(0xffffffffu, sj, o);
+      nf += __shfl_xor_sync(0xffffffffu, nf, o);
+    }
+    if (tid == 0) {
+      s_diag[0] = sj;
+      s_diag[1] = nf;
+    }
   }
   __syncthreads();
+  const float ne = s_tot[D];
+  const bool all_div = !(ne > 0.f);
+  const float inv = all_div ? 0.f : 1.0f / ne;
+  for (int d = tid; d < D; d += blockDim.x) {
+    if (all_div) {
+      s_mean[d] = p.mean[(size_t)r * D + d];
+      s_var[d] = p.var[(size_t)r * D + d];
+    } else {
+      const float m1 = s_tot[d] * inv;
+      s_mean[d] = s.mu[d] + m1;
+      s_var[d] = fmaxf(fmaf(-m1, m1, s_tot[D + 1 + d] * inv), p.var_floor[d % 3]);
+    }
+  }
+  __syncthreads();
+  const int fi = all_div ? s.cur_idx : b.f;
   for (int d = tid; d < D; d += blockDim.x) {
     p.mean[(size_t)r * D + d] = s_mean[d];
     p.var[(size_t)r * D + d] = s_var[d];
   }
-  if (tid == 0) p.fidx[r] = s_best_f;
-  write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, s_best_f, diag[0], diag[1],
-               (float)ntot, (float)ntot, (int)diag[2]);
+  if (tid == 0) {
+    p.fidx[r] = fi;
+    p.best[r] = b.k;
+  }
+  write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, b.m,
+               s_diag[1] > 0.f ? s_diag[0] / s_diag[1] : kInf, ne, ne, (int)((float)p.K_global - s_diag[1]));
 }
 
 // ---------------------------------------------------------------------------
@@ -837,28 +1157,36 @@ __global__ void __launch_bounds__(128) sbs_debug_samples_kernel(const __grid_con
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-template <int P, bool MPPI>
+template <int P, int EPI, bool FUSED>
 static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
   constexpr int D = 12 * P;
-  const size_t smem = MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : 0;
+  const size_t smem = EPI == EPI_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : 0;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(sbs_rollout_kernel<P, MPPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     attr = true;
   }
   dim3 grid(p.n_cta, p.R);
-  sbs_rollout_kernel<P, MPPI><<<grid, kBlock, smem, s>>>(p);
+  sbs_rollout_kernel<P, EPI, FUSED><<<grid, kBlock, smem, s>>>(p);
   return cudaGetLastError();
 }
 
-template <int P, bool MPPI>
-static int occupancy_t() {
+template <int P>
+static cudaError_t launch_rollout_p(const Params& p, int mode, bool fused, cudaStream_t s) {
+  if (mode == SBS_MPPI) return fused ? launch_rollout_t<P, EPI_MPPI, true>(p, s) : launch_rollout_t<P, EPI_MPPI, false>(p, s);
+  if (mode == SBS_NAIVE) return launch_rollout_t<P, EPI_ARGMIN, true>(p, s);
+  return launch_rollout_t<P, EPI_ARGMIN, false>(p, s);  // CEM: select + elite kernels follow
+}
+
+template <int P>
+static int occupancy_t(int mode) {
   constexpr int D = 12 * P;
-  const size_t smem = MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : 0;
-  cudaFuncSetAttribute(sbs_rollout_kernel<P, MPPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  const size_t smem = mode == SBS_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : 0;
+  const void* f = mode == SBS_MPPI ? (const void*)sbs_rollout_kernel<P, EPI_MPPI, true>
+                                   : (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false>;
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sbs_rollout_kernel<P, MPPI>, kBlock, smem) != cudaSuccess)
-    return 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, kBlock, smem) != cudaSuccess) return 1;
   return n > 0 ? n : 1;
 }
 
@@ -874,38 +1202,20 @@ static int occupancy_t() {
     default: return cudaErrorInvalidValue; \
   }
 
-cudaError_t launch_rollout(const Params& p, bool mppi, cudaStream_t s) {
-  if (mppi) {
-    SBS_DISPATCH_P(p.P, return (launch_rollout_t<PP, true>(p, s)));
-  } else {
-    SBS_DISPATCH_P(p.P, return (launch_rollout_t<PP, false>(p, s)));
-  }
+cudaError_t launch_rollout(const Params& p, int mode, bool fused, cudaStream_t s) {
+  SBS_DISPATCH_P(p.P, return launch_rollout_p<PP>(p, mode, fused, s));
 }
 
-int rollout_occupancy(int P, bool mppi) {
-  auto f = [&]() -> int {
-    if (mppi) {
-      switch (P) {
-        case 2: return occupancy_t<2, true>();
-        case 3: return occupancy_t<3, true>();
-        case 4: return occupancy_t<4, true>();
-        case 5: return occupancy_t<5, true>();
-        case 6: return occupancy_t<6, true>();
-        case 7: return occupancy_t<7, true>();
-        default: return occupancy_t<8, true>();
-      }
-    }
-    switch (P) {
-      case 2: return occupancy_t<2, false>();
-      case 3: return occupancy_t<3, false>();
-      case 4: return occupancy_t<4, false>();
-      case 5: return occupancy_t<5, false>();
-      case 6: return occupancy_t<6, false>();
-      case 7: return occupancy_t<7, false>();
-      default: return occupancy_t<8, false>();
-    }
-  };
-  return f();
+int rollout_occupancy(int P, int mode) {
+  switch (P) {
+    case 2: return occupancy_t<2>(mode);
+    case 3: return occupancy_t<3>(mode);
+    case 4: return occupancy_t<4>(mode);
+    case 5: return occupancy_t<5>(mode);
+    case 6: return occupancy_t<6>(mode);
+    case 7: return occupancy_t<7>(mode);
+    default: return occupancy_t<8>(mode);
+  }
 }
 
 cudaError_t launch_mppi_finalize(const Params& p, cudaStream_t s) {
@@ -918,13 +1228,25 @@ cudaError_t launch_mppi_merge(const Params& p, float* dst, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+static size_t select_smem(int64_t K) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sbs_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
+    cudaFuncSetAttribute(sbs_select_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
+    attr = true;
+  }
+  if (K <= kSelSmallMax) return (size_t)kSelSmallSmemBytes;
+  return (size_t)(kSelHistWords + (K <= kSelSmemKeys ? K : 0)) * 4;
+}
+
 cudaError_t launch_select(const Params& p, cudaStream_t s) {
-  sbs_select_kernel<<<p.R, kSelBlock, 0, s>>>(p);
+  sbs_select_kernel<<<p.R, kSelBlock, select_smem(p.K_local), s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_elite(const Params& p, cudaStream_t s) {
-  SBS_DISPATCH_P(p.P, (sbs_elite_kernel<PP><<<p.R, kEliteBlock, 0, s>>>(p)); return cudaGetLastError());
+  dim3 grid(p.n_eblk, p.R);
+  SBS_DISPATCH_P(p.P, (sbs_elite_kernel<PP><<<grid, 32 * 3 * PP, 0, s>>>(p)); return cudaGetLastError());
 }
 
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
@@ -934,15 +1256,9 @@ cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t
                  return cudaGetLastError());
 }
 
-cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, int64_t* best,
-                              cudaStream_t s) {
-  float* diag = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&diag, 4 * sizeof(float), s);
-  if (e != cudaSuccess) return e;
-  sbs_select_raw_kernel<<<1, kSelBlock, 0, s>>>(J, K, K_e, idx, best, diag);
-  e = cudaGetLastError();
-  cudaFreeAsync(diag, s);
-  return e;
+cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s) {
+  sbs_select_raw_kernel<<<1, kSelBlock, select_smem(K), s>>>(J, K, K_e, idx);
+  return cudaGetLastError();
 }
 
 }  // namespace sbs

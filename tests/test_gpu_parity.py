@@ -140,6 +140,12 @@ def test_config2_mppi_paper_settings(B, orc):
     _run_pair(B, orc, cfg, inputs, n_steps=2)
 
 
+@pytest.mark.parametrize("mode", ["cem", "naive"])
+def test_config3_three_iterations(B, orc, mode):
+    cfg, inputs = W.config3(mode, K=3000)
+    _run_pair(B, orc, cfg, inputs, n_steps=3)
+
+
 @pytest.mark.parametrize("K", [1, 2, 127, 128, 129, 1000, 4097])
 def test_ragged_sample_counts(B, orc, K):
     cfg, inputs = W.config2(K=K)
