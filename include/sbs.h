@@ -149,8 +149,10 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out);
 void sbs_destroy(sbs_ctx* ctx);
 
 /* State reference x^r_j, j = 0..H-1 (Alg. 2 "x^r_i"; L13).
- * _reference: one robot, host [H][12].  _reference_device: all robots,
- * device [R][H][12], stream-ordered. */
+ * _reference: one robot, host [H][12]; copied into pinned staging before the
+ * call returns (the caller's buffer is free again) and uploaded in order on the
+ * context's stream, ahead of the next sbs_step.  _reference_device: all robots,
+ * device [R][H][12], copied on `stream`. */
 int sbs_set_reference(sbs_ctx* ctx, int32_t robot, const float* x_ref);
 int sbs_set_reference_device(sbs_ctx* ctx, const float* d_x_ref, void* stream);
 

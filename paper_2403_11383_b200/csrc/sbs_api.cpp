@@ -85,6 +85,8 @@ struct sbs_ctx {
   sbs_output* d_out = nullptr;
   sbs_input* h_in = nullptr;   // pinned
   sbs_output* h_out = nullptr; // pinned
+  float* h_xref = nullptr;     // pinned [R][H][12] staging of sbs_set_reference
+  std::vector<cudaEvent_t> ref_ev;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<char> ref_set;
   uint32_t iter = 0;
@@ -303,6 +305,8 @@ void sbs_destroy(sbs_ctx* c) {
     if (p) cudaFree(p);
   if (c->h_in) cudaFreeHost(c->h_in);
   if (c->h_out) cudaFreeHost(c->h_out);
+  if (c->h_xref) cudaFreeHost(c->h_xref);
+  for (auto e : c->ref_ev) cudaEventDestroy(e);
   for (auto& pd : c->pending) {
     cudaEventDestroy(pd.a);
     cudaEventDestroy(pd.b);
@@ -414,6 +418,10 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   }
   P.seed_lo = (uint32_t)(cfg->seed & 0xFFFFFFFFull);
   P.seed_hi = (uint32_t)(cfg->seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    P.rk[r][0] = P.seed_lo + (uint32_t)r * 0x9E3779B9u;
+    P.rk[r][1] = P.seed_hi + (uint32_t)r * 0xBB67AE85u;
+  }
   P.robot_offset = cfg->robot_offset;
   // ---- sharding and launch geometry ----
   P.R = R;
@@ -450,6 +458,12 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaMalloc(&c->d_out, R * sizeof(sbs_output)));
   CKC(cudaMallocHost(&c->h_in, R * sizeof(sbs_input)));
   CKC(cudaMallocHost(&c->h_out, R * sizeof(sbs_output)));
+  CKC(cudaMallocHost(&c->h_xref, (size_t)R * H * 12 * sizeof(float)));
+  c->ref_ev.assign(R, nullptr);
+  for (int r = 0; r < R; ++r) {
+    CKC(cudaEventCreateWithFlags(&c->ref_ev[r], cudaEventDisableTiming));
+    CKC(cudaEventRecord(c->ref_ev[r], c->stream));
+  }
   // initial distribution: mean (0, 0, m|g_z|/4) per leg and knot, var = sigma^2, freq_idx 0
   {
     std::vector<float> m(RD), v(RD);
@@ -502,8 +516,13 @@ int sbs_set_reference(sbs_ctx* c, int32_t robot, const float* x_ref) {
   const int n = c->P.H * 12;
   if (!finite_all(x_ref, n)) return fail(c, SBS_ERR_NONFINITE, "reference not finite");
   CK(cudaSetDevice(c->cfg.device));
-  CK(cudaMemcpyAsync(c->d_xref + (size_t)robot * n, x_ref, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  // stage in this robot's pinned slot (the caller's buffer is free on return) and
+  // copy asynchronously; the slot is reused only after its previous copy completed
+  CK(cudaEventSynchronize(c->ref_ev[robot]));
+  float* slot = c->h_xref + (size_t)robot * n;
+  memcpy(slot, x_ref, n * sizeof(float));
+  CK(cudaMemcpyAsync(c->d_xref + (size_t)robot * n, slot, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaEventRecord(c->ref_ev[robot], c->stream));
   c->ref_set[robot] = 1;
   return SBS_OK;
 }

@@ -12,7 +12,7 @@ constexpr int kBlock = 128;         // samples per tile = threads per rollout CT
 constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, nfin, pad]
 constexpr int kEPartStride = 2 * SBS_MAX_D + 4;  // CEM elite-moment record [S1[D], n, S2[D]]
 #ifndef SBS_ROLLOUT_MIN_BLOCKS
-#define SBS_ROLLOUT_MIN_BLOCKS 3
+#define SBS_ROLLOUT_MIN_BLOCKS 4
 #endif
 constexpr int kRolloutMinBlocks = SBS_ROLLOUT_MIN_BLOCKS;  // __launch_bounds__ min CTAs per SM
 
@@ -46,6 +46,7 @@ struct Params {
   float var_floor[3];
   // --- noise ---
   uint32_t seed_lo, seed_hi;
+  uint32_t rk[10][2];         // Philox round keys (seed_lo + r 0x9E3779B9, seed_hi + r 0xBB67AE85)
   uint32_t iter;
   int robot_offset;
   // --- sizes / sharding ---

@@ -33,12 +33,18 @@ struct RobotSmem {
   float x0[12];
   float feet_cur[12];
   float feet_next[12];
-  float xref[SBS_MAX_HORIZON * 12];
+  float xref[SBS_MAX_HORIZON * 12];  // per step, kernel order (px,py, vx,vy, pz,vz, roll,pitch, yaw,wx, wy,wz)
+  uint8_t ctab[SBS_MAX_FREQ][SBS_MAX_HORIZON];  // bits 0-3: stance of leg i at step j; bits 4-7: leg i touched down
   uint32_t phase0;
   int cur_idx;
 };
 
-// step a0: mu'[p] = S_mu(min(t_p + dt, T)); std = sqrt(var)
+// state-vector index in the kernel's pair order for each index of x = (p, v, Phi, w)
+__device__ __forceinline__ int xref_slot(int a) { return a == 2 ? 4 : (a == 3 ? 2 : (a == 4 ? 3 : a)); }
+
+// step a0: mu'[p] = S_mu(min(t_p + dt, T)); std = sqrt(var).
+// Also the contact table of every frequency option (O7, L22, L23) from the
+// Q0.32 phase: one byte per (theta1, step).
 __device__ void load_robot(const Params& p, int r, RobotSmem& s) {
   const int D = p.D, P = p.P;
   const float* mean = p.mean + (size_t)r * D;
@@ -61,21 +67,60 @@ __device__ void load_robot(const Params& p, int r, RobotSmem& s) {
     s.feet_next[a] = in->feet_next[a];
   }
   const float* xr = p.xref + (size_t)r * p.H * 12;
-  for (int a = threadIdx.x; a < p.H * 12; a += blockDim.x) s.xref[a] = xr[a];
+  for (int a = threadIdx.x; a < p.H * 12; a += blockDim.x) {
+    const int j = a / 12, c = a - 12 * j;
+    s.xref[12 * j + xref_slot(c)] = xr[a];
+  }
+  const uint32_t ph0 = in->phase_q32;
+  for (int f = threadIdx.x; f < p.n_freq; f += blockDim.x) {
+    uint32_t ph[4];
+    uint32_t prev = 0, td = 0;
+    for (int i = 0; i < 4; ++i) ph[i] = ph0 + p.off[i];
+    for (int j = 0; j < p.H; ++j) {
+      uint32_t st = 0;
+      for (int i = 0; i < 4; ++i) {
+        if (p.all_stance || ph[i] < p.thr) st |= 1u << i;
+        ph[i] += p.inc[f];
+      }
+      if (j > 0) td |= st & ~prev;  // first swing -> stance transition inside the horizon
+      prev = st;
+      s.ctab[f][j] = (uint8_t)(st | (td << 4));
+    }
+  }
   if (threadIdx.x == 0) {
-    s.phase0 = in->phase_q32;
+    s.phase0 = ph0;
     s.cur_idx = p.fidx[r];
   }
+}
+
+// theta2 of one sample in registers, organised per leg: (x, y) knot pairs for
+// packed FP32x2 arithmetic and the z knots; element d = (p*4 + leg)*3 + axis.
+template <int P>
+struct Theta {
+  float2 xy[P][4];
+  float z[P][4];
+};
+template <int P>
+__device__ __forceinline__ void theta_set(Theta<P>& t, int d, float v) {  // d is a compile-time constant here
+  const int pk = d / 12, c = d % 12, leg = c / 3, ax = c % 3;
+  if (ax == 0) t.xy[pk][leg].x = v;
+  else if (ax == 1) t.xy[pk][leg].y = v;
+  else t.z[pk][leg] = v;
+}
+template <int P>
+__device__ __forceinline__ float theta_get(const Theta<P>& t, int d) {
+  const int pk = d / 12, c = d % 12, leg = c / 3, ax = c % 3;
+  return ax == 0 ? t.xy[pk][leg].x : (ax == 1 ? t.xy[pk][leg].y : t.z[pk][leg]);
 }
 
 // step a1: theta2 = mu' + sigma z, theta1 index
 template <int P, bool WITH_Z>
 __device__ __forceinline__ int draw_sample(const Params& p, uint32_t robot_g, int64_t k, const RobotSmem& s,
-                                           float (&th)[12 * P], float* z_out = nullptr) {
+                                           Theta<P>& th, float* z_out = nullptr) {
   constexpr int D = 12 * P;
   if (p.elite_preserve && k == 0) {  // L21
 #pragma unroll
-    for (int d = 0; d < D; ++d) th[d] = s.mu[d];
+    for (int d = 0; d < D; ++d) theta_set(th, d, s.mu[d]);
     if (WITH_Z)
       for (int d = 0; d < D; ++d) z_out[d] = 0.0f;
     return s.cur_idx;
@@ -83,19 +128,19 @@ __device__ __forceinline__ int draw_sample(const Params& p, uint32_t robot_g, in
   const uint32_t kk = (uint32_t)k;
 #pragma unroll
   for (int q = 0; q < D / 4; ++q) {
-    const U4 w = philox4x32_10((uint32_t)q, kk, p.iter, robot_g, p.seed_lo, p.seed_hi);
+    const U4 w = philox4x32_10_rk((uint32_t)q, kk, p.iter, robot_g, p.rk);
     float z[4];
     box_muller(w.x, w.y, z[0], z[1]);
     box_muller(w.z, w.w, z[2], z[3]);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      th[4 * q + i] = __fmaf_rn(s.sig[4 * q + i], z[i], s.mu[4 * q + i]);
+      theta_set(th, 4 * q + i, __fmaf_rn(s.sig[4 * q + i], z[i], s.mu[4 * q + i]));
       if (WITH_Z) z_out[4 * q + i] = z[i];
     }
   }
   int idx = s.cur_idx;
   if (p.gait_adapt) {
-    const U4 w = philox4x32_10(0x80000000u, kk, p.iter, robot_g, p.seed_lo, p.seed_hi);
+    const U4 w = philox4x32_10_rk(0x80000000u, kk, p.iter, robot_g, p.rk);
     idx = (int)__umulhi(w.x, (uint32_t)p.n_freq);  // (w * n) >> 32
   }
   return idx;
@@ -110,7 +155,7 @@ __device__ __forceinline__ void sample_block(const Params& p, uint32_t robot_g, 
     for (int i = 0; i < 4; ++i) th4[i] = s.mu[4 * q + i];
     return;
   }
-  const U4 w = philox4x32_10((uint32_t)q, (uint32_t)k, p.iter, robot_g, p.seed_lo, p.seed_hi);
+  const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k, p.iter, robot_g, p.rk);
   float z[4];
   box_muller(w.x, w.y, z[0], z[1]);
   box_muller(w.z, w.w, z[2], z[3]);
@@ -118,192 +163,167 @@ __device__ __forceinline__ void sample_block(const Params& p, uint32_t robot_g, 
   for (int i = 0; i < 4; ++i) th4[i] = __fmaf_rn(s.sig[4 * q + i], z[i], s.mu[4 * q + i]);
 }
 
-// Eq. 1 angular part at one RK4 stage (L24): given world torque tau_w,
-//   w' = I^-1 (R^T tau_w - w x I w),  Phi' = E'^-1(Phi) w.
-__device__ __forceinline__ void ang_deriv(const Params& p, float phi, float th, float psi, float wx, float wy,
-                                          float wz, float tx, float ty, float tz, float& dphi, float& dth,
-                                          float& dpsi, float& dwx, float& dwy, float& dwz) {
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+
+// Eq. 1 angular part at one RK4 stage (L24): given the world torque tau,
+//   w' = I^-1 (R^T tau - w x I w),  Phi' = E'^-1(Phi) w.
+// Angular state in three pairs: A = (roll, pitch), B = (yaw, w_x), C = (w_y, w_z).
+__device__ __forceinline__ void ang_deriv(const Params& p, float2 A, float2 B, float2 C, float tx, float ty, float tz,
+                                          float2& dA, float2& dB, float2& dC) {
   float sr, cr, sp, cp, sy, cy;
-  __sincosf(phi, &sr, &cr);
-  __sincosf(th, &sp, &cp);
-  __sincosf(psi, &sy, &cy);
+  __sincosf(A.x, &sr, &cr);
+  __sincosf(A.y, &sp, &cp);
+  __sincosf(B.x, &sy, &cy);
+  const float wx = B.y, wy = C.x, wz = C.y;
   // R^T tau = Rx^T Ry^T Rz^T tau  (R = Rz(yaw) Ry(pitch) Rx(roll))
   const float t1x = fmaf(cy, tx, sy * ty), t1y = fmaf(cy, ty, -sy * tx);
   const float bx = fmaf(cp, t1x, -sp * tz), t2z = fmaf(sp, t1x, cp * tz);
   const float by = fmaf(cr, t1y, sr * t2z), bz = fmaf(cr, t2z, -sr * t1y);
-  float Lx, Ly, Lz;
+  float dwx;
+  float2 dwyz;
   if (p.diag_inertia) {
-    Lx = p.I[0] * wx;
-    Ly = p.I[4] * wy;
-    Lz = p.I[8] * wz;
-  } else {
-    Lx = fmaf(p.I[0], wx, fmaf(p.I[1], wy, p.I[2] * wz));
-    Ly = fmaf(p.I[3], wx, fmaf(p.I[4], wy, p.I[5] * wz));
-    Lz = fmaf(p.I[6], wx, fmaf(p.I[7], wy, p.I[8] * wz));
-  }
-  const float rx = bx - fmaf(wy, Lz, -wz * Ly);
-  const float ry = by - fmaf(wz, Lx, -wx * Lz);
-  const float rz = bz - fmaf(wx, Ly, -wy * Lx);
-  if (p.diag_inertia) {
+    const float Lx = p.I[0] * wx;
+    const float2 Lyz = fmul2(f2(p.I[4], p.I[8]), C);
+    // r = b - w x L = b + L x w
+    const float rx = bx + fmaf(Lyz.x, wz, -Lyz.y * wy);
+    const float2 ryz = fadd2(f2(by, bz), f2(fmaf(Lyz.y, wx, -Lx * wz), fmaf(Lx, wy, -Lyz.x * wx)));
     dwx = p.Iinv[0] * rx;
-    dwy = p.Iinv[4] * ry;
-    dwz = p.Iinv[8] * rz;
+    dwyz = fmul2(f2(p.Iinv[4], p.Iinv[8]), ryz);
   } else {
+    const float Lx = fmaf(p.I[0], wx, fmaf(p.I[1], wy, p.I[2] * wz));
+    const float Ly = fmaf(p.I[3], wx, fmaf(p.I[4], wy, p.I[5] * wz));
+    const float Lz = fmaf(p.I[6], wx, fmaf(p.I[7], wy, p.I[8] * wz));
+    const float rx = bx - fmaf(wy, Lz, -wz * Ly);
+    const float ry = by - fmaf(wz, Lx, -wx * Lz);
+    const float rz = bz - fmaf(wx, Ly, -wy * Lx);
     dwx = fmaf(p.Iinv[0], rx, fmaf(p.Iinv[1], ry, p.Iinv[2] * rz));
-    dwy = fmaf(p.Iinv[3], rx, fmaf(p.Iinv[4], ry, p.Iinv[5] * rz));
-    dwz = fmaf(p.Iinv[6], rx, fmaf(p.Iinv[7], ry, p.Iinv[8] * rz));
+    dwyz = f2(fmaf(p.Iinv[3], rx, fmaf(p.Iinv[4], ry, p.Iinv[5] * rz)),
+              fmaf(p.Iinv[6], rx, fmaf(p.Iinv[7], ry, p.Iinv[8] * rz)));
   }
   const float rc = __fdividef(1.0f, cp);
   const float a = fmaf(sr, wy, cr * wz);
-  dphi = fmaf(sp * rc, a, wx);
-  dth = fmaf(cr, wy, -sr * wz);
-  dpsi = a * rc;
+  dA = f2(fmaf(sp * rc, a, wx), fmaf(cr, wy, -sr * wz));
+  dB = f2(a * rc, dwx);
+  dC = dwyz;
 }
 
-// steps a2-a4: Rollout(theta_k, x0), Alg. 2 with policy pi
+// steps a2-a4: Rollout(theta_k, x0), Alg. 2 with policy pi.
+// Per-leg work sits behind the stance bit: with a fixed gait every lane of a warp
+// shares the contact schedule, so swing legs cost nothing.
 template <int P>
-__device__ float rollout(const Params& p, const float (&th)[12 * P], int fi, const RobotSmem& s) {
-  float px = s.x0[0], py = s.x0[1], pz = s.x0[2];
-  float vx = s.x0[3], vy = s.x0[4], vz = s.x0[5];
-  float an0 = s.x0[6], an1 = s.x0[7], an2 = s.x0[8];
-  float wx = s.x0[9], wy = s.x0[10], wz = s.x0[11];
+__device__ float rollout(const Params& p, const Theta<P>& th, int fi, const RobotSmem& s) {
+  float2 pxy = f2(s.x0[0], s.x0[1]), vxy = f2(s.x0[3], s.x0[4]);
+  float pz = s.x0[2], vz = s.x0[5];
+  float2 A = f2(s.x0[6], s.x0[7]), Bq = f2(s.x0[8], s.x0[9]), C = f2(s.x0[10], s.x0[11]);
   const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt * (1.0f / 6.0f);
   const float dt2h = 0.5f * p.dt * p.dt, dt2q = 0.25f * p.dt * p.dt;
-  const uint32_t inc = p.inc[fi];
-  uint32_t ph[4];
-  bool prev[4], td[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    ph[i] = s.phase0 + p.off[i];
-    prev[i] = false;
-    td[i] = false;
-  }
+  const float2 dt_2 = f2(dt, dt), hdt_2 = f2(hdt, hdt), dt6_2 = f2(dt6, dt6), two_2 = f2(2.f, 2.f);
+  const float2 dt2h_2 = f2(dt2h, dt2h), dt2q_2 = f2(dt2q, dt2q);
+  const float2 Qp = f2(p.Q[0], p.Q[1]), Qv = f2(p.Q[3], p.Q[4]), Qz = f2(p.Q[2], p.Q[5]);
+  const float2 QA = f2(p.Q[6], p.Q[7]), QB = f2(p.Q[8], p.Q[9]), QC = f2(p.Q[10], p.Q[11]);
+  const float2 im_2 = f2(p.inv_mass, p.inv_mass), gxy = f2(p.g[0], p.g[1]);
+  const uint8_t* ct = s.ctab[fi];
   float J = 0.0f;
   bool bad = false;
   for (int j = 0; j < p.H; ++j) {
-    // --- contact sequence delta_j (O7, L22) and touchdown (L23) ---
-    bool st[4];
-    int nst = 0;
+    const uint32_t fl = ct[j];
+    const float urz = p.urz[__popc(fl & 0xFu)];
+    const float* Wj = p.W[j];
+    float2 F = f2(0.f, 0.f), effxy = f2(0.f, 0.f);
+    float Fz = 0.f, Mx = 0.f, My = 0.f, Mz = 0.f, pen = 0.f, effz = 0.f;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      st[i] = p.all_stance || (ph[i] < p.thr);
-      td[i] = td[i] || (j > 0 && st[i] && !prev[i]);
-      prev[i] = st[i];
-      nst += st[i] ? 1 : 0;
-      ph[i] += inc;
+    for (int leg = 0; leg < 4; ++leg) {
+      if (fl & (1u << leg)) {
+        // --- Gamma_j = sigma(theta2, t_j) for this stance leg, cone, penalty (O8-O9) ---
+        float2 g = fmul2(f2(Wj[0], Wj[0]), th.xy[0][leg]);
+        float gz = Wj[0] * th.z[0][leg];
+#pragma unroll
+        for (int q = 1; q < P; ++q) {
+          g = ffma2(f2(Wj[q], Wj[q]), th.xy[q][leg], g);
+          gz = fmaf(Wj[q], th.z[q][leg], gz);
+        }
+        const float fzc = fminf(fmaxf(gz, p.fz_min), p.fz_max);
+        const float l = p.mu * fzc;
+        const float vzv = fmaxf(p.fz_min - gz, 0.0f) + fmaxf(gz - p.fz_max, 0.0f);
+        const float vxv = fmaxf(fabsf(g.x) - l, 0.0f), vyv = fmaxf(fabsf(g.y) - l, 0.0f);
+        pen += fmaf(vzv, vzv, fmaf(vxv, vxv, vyv * vyv));
+        const float2 c = f2(fminf(fmaxf(g.x, -l), l), fminf(fmaxf(g.y, -l), l));
+        // effort (u - u^r)^T R (u - u^r), u^r = (0, 0, m|g|/n_stance) (L12)
+        effxy = ffma2(fmul2(f2(p.Rw[3 * leg], p.Rw[3 * leg + 1]), c), c, effxy);
+        const float ez = fzc - urz;
+        effz = fmaf(p.Rw[3 * leg + 2] * ez, ez, effz);
+        // net force and moment about the origin; feet switch at touchdown (L23)
+        F = fadd2(F, c);
+        Fz += fzc;
+        const float* ft = (fl & (16u << leg)) ? &s.feet_next[3 * leg] : &s.feet_cur[3 * leg];
+        const float fx = ft[0], fy = ft[1], fzz = ft[2];
+        Mx += fmaf(fy, fzc, -fzz * c.y);
+        My += fmaf(fzz, c.x, -fx * fzc);
+        Mz += fmaf(fx, c.y, -fy * c.x);
+      }
     }
-    // --- Gamma_j = sigma(theta2, t_j), mask, cone, penalty (O8-O9) ---
-    float G[12];
-    float pen = 0.0f;
-#pragma unroll
-    for (int c = 0; c < 12; ++c) {
-      float v = 0.0f;
-#pragma unroll
-      for (int q = 0; q < P; ++q) v = fmaf(p.W[j][q], th[q * 12 + c], v);
-      G[c] = v;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float fx = G[3 * i], fy = G[3 * i + 1], fz = G[3 * i + 2];
-      const float fzc = fminf(fmaxf(fz, p.fz_min), p.fz_max);
-      const float l = p.mu * fzc;
-      const float vzv = fmaxf(p.fz_min - fz, 0.0f) + fmaxf(fz - p.fz_max, 0.0f);
-      const float vxv = fmaxf(fabsf(fx) - l, 0.0f), vyv = fmaxf(fabsf(fy) - l, 0.0f);
-      const float pl = fmaf(vzv, vzv, fmaf(vxv, vxv, vyv * vyv));
-      pen += st[i] ? pl : 0.0f;
-      G[3 * i] = st[i] ? fminf(fmaxf(fx, -l), l) : 0.0f;
-      G[3 * i + 1] = st[i] ? fminf(fmaxf(fy, -l), l) : 0.0f;
-      G[3 * i + 2] = st[i] ? fzc : 0.0f;
-    }
-    // --- stage cost r(u_j, x_j, x^r_j) ---
+    // --- stage cost r(u_j, x_j, x^r_j), packed pairs ---
     const float* xr = &s.xref[12 * j];
-    float e8 = an2 - xr[8];
-    e8 = fmaf(-kTwoPi, rintf(e8 * kInvTwoPi), e8);  // yaw wrapped to [-pi, pi]
-    const float e[12] = {px - xr[0], py - xr[1], pz - xr[2], vx - xr[3], vy - xr[4], vz - xr[5],
-                         an0 - xr[6], an1 - xr[7], e8,        wx - xr[9], wy - xr[10], wz - xr[11]};
-    float stage = 0.0f;
-#pragma unroll
-    for (int a = 0; a < 12; ++a) stage = fmaf(p.Q[a] * e[a], e[a], stage);
-    const float urz = p.urz[nst];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float ez = G[3 * i + 2] - urz;
-      float t = fmaf(p.Rw[3 * i] * G[3 * i], G[3 * i], fmaf(p.Rw[3 * i + 1] * G[3 * i + 1], G[3 * i + 1],
-                                                              p.Rw[3 * i + 2] * ez * ez));
-      stage += st[i] ? t : 0.0f;
+    const float2 e0 = fadd2(pxy, f2(-xr[0], -xr[1]));
+    const float2 e1 = fadd2(vxy, f2(-xr[2], -xr[3]));
+    const float2 e2 = fadd2(f2(pz, vz), f2(-xr[4], -xr[5]));
+    const float2 e3 = fadd2(A, f2(-xr[6], -xr[7]));
+    float2 e4 = fadd2(Bq, f2(-xr[8], -xr[9]));
+    e4.x = fmaf(-kTwoPi, rintf(e4.x * kInvTwoPi), e4.x);  // yaw wrapped to [-pi, pi]
+    const float2 e5 = fadd2(C, f2(-xr[10], -xr[11]));
+    float2 acc = fmul2(fmul2(Qp, e0), e0);
+    acc = ffma2(fmul2(Qv, e1), e1, acc);
+    acc = ffma2(fmul2(Qz, e2), e2, acc);
+    acc = ffma2(fmul2(QA, e3), e3, acc);
+    acc = ffma2(fmul2(QB, e4), e4, acc);
+    acc = ffma2(fmul2(QC, e5), e5, acc);
+    acc = fadd2(acc, effxy);
+    J += (acc.x + acc.y) + fmaf(p.w_fc, pen, effz);
+    // --- x_{j+1}: v' = F/m + g is constant over the step, so RK4 on (p, v) is
+    //     exact and the stage positions are closed-form; tau = M - p_stage x F ---
+    const float2 axy = ffma2(F, im_2, gxy);
+    const float az = fmaf(Fz, p.inv_mass, p.g[2]);
+    float2 k1A, k1B, k1C, k2A, k2B, k2C, k3A, k3B, k3C, k4A, k4B, k4C;
+    ang_deriv(p, A, Bq, C, Mx - fmaf(pxy.y, Fz, -pz * F.y), My - fmaf(pz, F.x, -pxy.x * Fz),
+              Mz - fmaf(pxy.x, F.y, -pxy.y * F.x), k1A, k1B, k1C);
+    {
+      const float2 q = ffma2(hdt_2, vxy, pxy);
+      const float qz = fmaf(hdt, vz, pz);
+      ang_deriv(p, ffma2(hdt_2, k1A, A), ffma2(hdt_2, k1B, Bq), ffma2(hdt_2, k1C, C),
+                Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
+                k2A, k2B, k2C);
     }
-    J += fmaf(p.w_fc, pen, stage);
-    // --- per-step force and moment about the world origin (Gamma, feet held: L8, L25) ---
-    float Fx = 0.f, Fy = 0.f, Fz = 0.f, Mx = 0.f, My = 0.f, Mz = 0.f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float fx = td[i] ? s.feet_next[3 * i] : s.feet_cur[3 * i];
-      const float fy = td[i] ? s.feet_next[3 * i + 1] : s.feet_cur[3 * i + 1];
-      const float fz = td[i] ? s.feet_next[3 * i + 2] : s.feet_cur[3 * i + 2];
-      const float gx = G[3 * i], gy = G[3 * i + 1], gz = G[3 * i + 2];
-      Fx += gx;
-      Fy += gy;
-      Fz += gz;
-      Mx += fmaf(fy, gz, -fz * gy);
-      My += fmaf(fz, gx, -fx * gz);
-      Mz += fmaf(fx, gy, -fy * gx);
+    {
+      const float2 q = ffma2(dt2q_2, axy, ffma2(hdt_2, vxy, pxy));
+      const float qz = fmaf(dt2q, az, fmaf(hdt, vz, pz));
+      ang_deriv(p, ffma2(hdt_2, k2A, A), ffma2(hdt_2, k2B, Bq), ffma2(hdt_2, k2C, C),
+                Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
+                k3A, k3B, k3C);
     }
-    // v' = F/m + g is constant over the step: RK4 on (p, v) is exact, so the
-    // stage positions are closed-form; the torque is tau = M - p_stage x F.
-    const float ax = fmaf(Fx, p.inv_mass, p.g[0]), ay = fmaf(Fy, p.inv_mass, p.g[1]),
-                az = fmaf(Fz, p.inv_mass, p.g[2]);
-    float k1[6], k2[6], k3[6], k4[6];
-    {  // stage 1 at p
-      ang_deriv(p, an0, an1, an2, wx, wy, wz, Mx - fmaf(py, Fz, -pz * Fy), My - fmaf(pz, Fx, -px * Fz),
-                Mz - fmaf(px, Fy, -py * Fx), k1[0], k1[1], k1[2], k1[3], k1[4], k1[5]);
-    }
-    {  // stage 2 at p + dt/2 v
-      const float qx = fmaf(hdt, vx, px), qy = fmaf(hdt, vy, py), qz = fmaf(hdt, vz, pz);
-      ang_deriv(p, fmaf(hdt, k1[0], an0), fmaf(hdt, k1[1], an1), fmaf(hdt, k1[2], an2), fmaf(hdt, k1[3], wx),
-                fmaf(hdt, k1[4], wy), fmaf(hdt, k1[5], wz), Mx - fmaf(qy, Fz, -qz * Fy),
-                My - fmaf(qz, Fx, -qx * Fz), Mz - fmaf(qx, Fy, -qy * Fx), k2[0], k2[1], k2[2], k2[3], k2[4],
-                k2[5]);
-    }
-    {  // stage 3 at p + dt/2 v + dt^2/4 a
-      const float qx = fmaf(dt2q, ax, fmaf(hdt, vx, px)), qy = fmaf(dt2q, ay, fmaf(hdt, vy, py)),
-                  qz = fmaf(dt2q, az, fmaf(hdt, vz, pz));
-      ang_deriv(p, fmaf(hdt, k2[0], an0), fmaf(hdt, k2[1], an1), fmaf(hdt, k2[2], an2), fmaf(hdt, k2[3], wx),
-                fmaf(hdt, k2[4], wy), fmaf(hdt, k2[5], wz), Mx - fmaf(qy, Fz, -qz * Fy),
-                My - fmaf(qz, Fx, -qx * Fz), Mz - fmaf(qx, Fy, -qy * Fx), k3[0], k3[1], k3[2], k3[3], k3[4],
-                k3[5]);
-    }
-    // stage 4 at p + dt v + dt^2/2 a  (= p_{j+1})
-    const float nx = fmaf(dt2h, ax, fmaf(dt, vx, px)), ny = fmaf(dt2h, ay, fmaf(dt, vy, py)),
-                nz = fmaf(dt2h, az, fmaf(dt, vz, pz));
-    ang_deriv(p, fmaf(dt, k3[0], an0), fmaf(dt, k3[1], an1), fmaf(dt, k3[2], an2), fmaf(dt, k3[3], wx),
-              fmaf(dt, k3[4], wy), fmaf(dt, k3[5], wz), Mx - fmaf(ny, Fz, -nz * Fy), My - fmaf(nz, Fx, -nx * Fz),
-              Mz - fmaf(nx, Fy, -ny * Fx), k4[0], k4[1], k4[2], k4[3], k4[4], k4[5]);
-    float acc[6];
-#pragma unroll
-    for (int a = 0; a < 6; ++a) acc[a] = fmaf(2.0f, k2[a] + k3[a], k1[a] + k4[a]);
-    an0 = fmaf(dt6, acc[0], an0);
-    an1 = fmaf(dt6, acc[1], an1);
-    an2 = fmaf(dt6, acc[2], an2);
-    wx = fmaf(dt6, acc[3], wx);
-    wy = fmaf(dt6, acc[4], wy);
-    wz = fmaf(dt6, acc[5], wz);
-    px = nx;
-    py = ny;
+    const float2 n = ffma2(dt2h_2, axy, ffma2(dt_2, vxy, pxy));
+    const float nz = fmaf(dt2h, az, fmaf(dt, vz, pz));
+    ang_deriv(p, ffma2(dt_2, k3A, A), ffma2(dt_2, k3B, Bq), ffma2(dt_2, k3C, C), Mx - fmaf(n.y, Fz, -nz * F.y),
+              My - fmaf(nz, F.x, -n.x * Fz), Mz - fmaf(n.x, F.y, -n.y * F.x), k4A, k4B, k4C);
+    A = ffma2(dt6_2, ffma2(two_2, fadd2(k2A, k3A), fadd2(k1A, k4A)), A);
+    Bq = ffma2(dt6_2, ffma2(two_2, fadd2(k2B, k3B), fadd2(k1B, k4B)), Bq);
+    C = ffma2(dt6_2, ffma2(two_2, fadd2(k2C, k3C), fadd2(k1C, k4C)), C);
+    pxy = n;
     pz = nz;
-    vx = fmaf(dt, ax, vx);
-    vy = fmaf(dt, ay, vy);
+    vxy = ffma2(dt_2, axy, vxy);
     vz = fmaf(dt, az, vz);
     // --- divergence of x_{j+1} (L26); NaN fails every <= test ---
-    const float big = fmaxf(fmaxf(fmaxf(fabsf(px), fabsf(py)), fmaxf(fabsf(pz), fabsf(vx))),
-                            fmaxf(fmaxf(fabsf(vy), fabsf(vz)), fmaxf(fabsf(an0), fabsf(an2))));
-    const float big2 = fmaxf(fmaxf(fabsf(wx), fabsf(wy)), fabsf(wz));
-    bad = bad || !(big <= 1e6f) || !(big2 <= 1e6f) || !(fabsf(an1) < kPitchMax);
+    const float big = fmaxf(fmaxf(fmaxf(fabsf(pxy.x), fabsf(pxy.y)), fmaxf(fabsf(pz), fabsf(vxy.x))),
+                            fmaxf(fmaxf(fabsf(vxy.y), fabsf(vz)), fmaxf(fabsf(A.x), fabsf(Bq.x))));
+    const float big2 = fmaxf(fmaxf(fabsf(Bq.y), fabsf(C.x)), fabsf(C.y));
+    bad = bad || !(big <= 1e6f) || !(big2 <= 1e6f) || !(fabsf(A.y) < kPitchMax);
   }
   const float df = p.freq_hz[fi] - p.f_nominal;
   J = fmaf(p.rho * df, df, J);  // P:350, once per rollout (L14)
   return (bad || !(J <= FLT_MAX)) ? kInf : J;
 }
-
 
 // (J, k) lexicographic order: argmin with lowest-index tie-break (L4, L5)
 __device__ __forceinline__ bool jk_less(float ja, int ka, float jb, int kb) {
@@ -615,7 +635,7 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
     const int64_t kl = (int64_t)tile * kBlock + tid;
     const bool valid = kl < p.K_local;
     const int64_t k = p.k_begin + kl;
-    float th[D];
+    Theta<P> th;
     float J = kInf;
     int fi = 0;
     if (valid) {
@@ -683,7 +703,7 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
     const float w = fin ? __expf((mt - J) * p.inv_lambda) : 0.0f;
     if (valid) {
 #pragma unroll
-      for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = w * th[d];
+      for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = w * theta_get(th, d);
     } else {
 #pragma unroll
       for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = 0.0f;
@@ -1145,11 +1165,13 @@ __global__ void __launch_bounds__(128) sbs_debug_samples_kernel(const __grid_con
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  float th[D], zz[D];
+  Theta<P> th;
+  float zz[D];
   const int f = draw_sample<P, true>(p, (uint32_t)(p.robot_offset + r), k0 + i, s, th, zz);
+#pragma unroll
   for (int d = 0; d < D; ++d) {
     z[i * D + d] = zz[d];
-    theta[i * D + d] = th[d];
+    theta[i * D + d] = theta_get(th, d);
   }
   fidx[i] = f;
 }
