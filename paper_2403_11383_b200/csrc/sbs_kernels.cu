@@ -31,8 +31,7 @@ struct RobotSmem {
   float mu[SBS_MAX_D];
   float sig[SBS_MAX_D];
   float x0[12];
-  float feet_cur[12];
-  float feet_next[12];
+  float feet[24];  // [0, 12): feet_cur, [12, 24): feet_next
   float xref[SBS_MAX_HORIZON * 12];  // per step, kernel order (px,py, vx,vy, pz,vz, roll,pitch, yaw,wx, wy,wz)
   uint8_t ctab[SBS_MAX_FREQ][SBS_MAX_HORIZON];  // bits 0-3: stance of leg i at step j; bits 4-7: leg i touched down
   uint32_t phase0;
@@ -63,8 +62,8 @@ __device__ void load_robot(const Params& p, int r, RobotSmem& s) {
   const sbs_input* in = p.in + r;
   for (int a = threadIdx.x; a < 12; a += blockDim.x) {
     s.x0[a] = in->x0[a];
-    s.feet_cur[a] = in->feet_cur[a];
-    s.feet_next[a] = in->feet_next[a];
+    s.feet[a] = in->feet_cur[a];
+    s.feet[12 + a] = in->feet_next[a];
   }
   const float* xr = p.xref + (size_t)r * p.H * 12;
   for (int a = threadIdx.x; a < p.H * 12; a += blockDim.x) {
@@ -231,9 +230,12 @@ __device__ float rollout(const Params& p, const Theta<P>& th, int fi, const Robo
   for (int j = 0; j < p.H; ++j) {
     const uint32_t fl = ct[j];
     const float urz = p.urz[__popc(fl & 0xFu)];
-    const float* Wj = p.W[j];
-    float2 F = f2(0.f, 0.f), effxy = f2(0.f, 0.f);
-    float Fz = 0.f, Mx = 0.f, My = 0.f, Mz = 0.f, pen = 0.f, effz = 0.f;
+    float Wj[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) Wj[q] = p.W[j][q];
+    // accumulators start at -0 (the additive identity), so the first add is not a real op
+    float2 F = f2(-0.f, -0.f), effxy = f2(-0.f, -0.f);
+    float Fz = -0.f, Mx = -0.f, My = -0.f, Mz = -0.f, pen = -0.f, effz = -0.f;
 #pragma unroll
     for (int leg = 0; leg < 4; ++leg) {
       if (fl & (1u << leg)) {
@@ -258,8 +260,8 @@ __device__ float rollout(const Params& p, const Theta<P>& th, int fi, const Robo
         // net force and moment about the origin; feet switch at touchdown (L23)
         F = fadd2(F, c);
         Fz += fzc;
-        const float* ft = (fl & (16u << leg)) ? &s.feet_next[3 * leg] : &s.feet_cur[3 * leg];
-        const float fx = ft[0], fy = ft[1], fzz = ft[2];
+        const int fo = ((fl >> (4 + leg)) & 1u) * 12 + 3 * leg;  // feet_next after touchdown
+        const float fx = s.feet[fo], fy = s.feet[fo + 1], fzz = s.feet[fo + 2];
         Mx += fmaf(fy, fzc, -fzz * c.y);
         My += fmaf(fzz, c.x, -fx * fzc);
         Mz += fmaf(fx, c.y, -fy * c.x);
