@@ -109,7 +109,8 @@ typedef struct sbs_config {
   int32_t robot_offset;   /* global index of robot 0 in the noise counter (robot sharding) */
   int32_t device;         /* CUDA device ordinal */
   int32_t rank, world;    /* sample sharding: rank handles a contiguous slice of the K samples */
-  uint8_t nccl_id[128];   /* ncclUniqueId (from sbs_nccl_unique_id on rank 0) when world > 1 */
+  uint8_t nccl_id[128];   /* ncclUniqueId (sbs_nccl_unique_id on rank 0) when world > 1; all zero:
+                             the caller exchanges the MPPI records (sbs_step_records) */
 } sbs_config;
 
 /* Per-robot input of one iteration (host for sbs_step, device for sbs_step_device). */
@@ -174,6 +175,18 @@ int sbs_step(sbs_ctx* ctx, const sbs_input* in, sbs_output* out);
  * rollout of that robot diverge (status SBS_WARN_ALL_DIVERGED in its output).
  * iter += 1 when the call returns SBS_OK. */
 int sbs_step_device(sbs_ctx* ctx, const sbs_input* d_in, sbs_output* d_out, void* stream);
+
+/* Sample-sharded MPPI with a caller-driven exchange (world > 1 and an all-zero
+ * nccl_id): the same iteration as sbs_step_device, split at its one exchange
+ * point.  sbs_step_records enqueues this rank's rollouts and writes its merged
+ * record per robot to d_rec (device, R x sbs_record_floats(ctx) floats: beta_g,
+ * argmin, sum w, sum w^2, sum w theta relative to beta_g, ...).  The caller
+ * gathers every rank's records in rank order ([world][R][record]) and passes
+ * them to sbs_finish_records, which merges them in rank order and finishes the
+ * iteration (new distribution, d_out); iter += 1.  Both stream-ordered. */
+int sbs_record_floats(const sbs_ctx* ctx);
+int sbs_step_records(sbs_ctx* ctx, const sbs_input* d_in, float* d_rec, void* stream);
+int sbs_finish_records(sbs_ctx* ctx, const float* d_recs, const sbs_input* d_in, sbs_output* d_out, void* stream);
 
 /* Exact checkpoint of the distribution state (means, vars, freq indices,
  * iteration counter, seed).  nbytes: in = capacity, out = size needed. */

@@ -102,6 +102,9 @@ def load_library(path: str = LIB_PATH):
         "sbs_profile": ([ctxp, C.c_int32], C.c_int),
         "sbs_kernel_times": ([ctxp, P(C.c_double), P(C.c_int64)], C.c_int),
         "sbs_launches_per_step": ([ctxp], C.c_int),
+        "sbs_record_floats": ([ctxp], C.c_int),
+        "sbs_step_records": ([ctxp, vp, vp, vp], C.c_int),
+        "sbs_finish_records": ([ctxp, vp, vp, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -254,6 +257,18 @@ class Controller:
     def step_device(self, d_in: int, d_out: int, stream: int = 0):
         return self._check(self.L.sbs_step_device(self.ctx, C.c_void_p(d_in), C.c_void_p(d_out),
                                                   C.c_void_p(stream)))
+
+    # ---- sample sharding with a caller-driven exchange --------------------------
+    def record_floats(self) -> int:
+        return int(self.L.sbs_record_floats(self.ctx))
+
+    def step_records(self, d_in: int, d_rec: int, stream: int = 0):
+        return self._check(self.L.sbs_step_records(self.ctx, C.c_void_p(d_in), C.c_void_p(d_rec),
+                                                   C.c_void_p(stream)))
+
+    def finish_records(self, d_recs: int, d_in: int, d_out: int, stream: int = 0):
+        return self._check(self.L.sbs_finish_records(self.ctx, C.c_void_p(d_recs), C.c_void_p(d_in),
+                                                     C.c_void_p(d_out), C.c_void_p(stream)))
 
     # ---- tests / measurement -------------------------------------------------
     def debug_samples(self, robot: int, k0: int, n: int):

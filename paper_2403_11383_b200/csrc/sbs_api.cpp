@@ -3,8 +3,9 @@
 // Owns the device state of one or more SBS controllers (R robots), derives the
 // constant tables once at creation (Catmull-Rom weights, warm-shift weights,
 // Q0.32 gait increments, inverse inertia), and enqueues one MPC iteration as
-// 2 (MPPI) or 3 (CEM / Naive) kernel launches on one stream.  With world > 1
-// the MPPI partials of the ranks are exchanged by one NCCL all-gather.
+// 1 (MPPI, Naive) or 3 (CEM) kernel launches on one stream.  With world > 1 the
+// MPPI records of the ranks are exchanged by one NCCL all-gather (or by the
+// caller: sbs_step_records / sbs_finish_records).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <math.h>
@@ -103,6 +104,7 @@ struct sbs_ctx {
   int64_t kl[SBS_NKERNELS] = {0, 0, 0, 0};
   // nccl
   nccl_comm_t comm = nullptr;
+  bool external = false;  // world > 1 with an all-zero nccl_id: the caller exchanges the records
 };
 
 namespace {
@@ -233,25 +235,43 @@ cudaError_t timed(sbs_ctx* c, int kernel, cudaStream_t s, F&& launch) {
 }
 
 // enqueue one iteration on stream s with inputs c->P.in and outputs c->P.out
+// sample-sharded MPPI, part 1: rollouts of this rank's slice + its merged record per robot
+int enqueue_records(sbs_ctx* c, cudaStream_t s, float* dst) {
+  Params& P = c->P;
+  P.iter = c->iter;
+  CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, SBS_MPPI, false, s); }));
+  CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_merge(P, dst, s); }));
+  return SBS_OK;
+}
+
+// part 2: merge the `world` ranks' records ([world][R][8 + D], rank order) and finish
+int enqueue_finish(sbs_ctx* c, cudaStream_t s, const float* recs) {
+  Params F = c->P;
+  F.iter = c->iter;
+  F.part = const_cast<float*>(recs);
+  F.n_cta = c->cfg.world;
+  F.part_c_stride = F.R;
+  CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_finalize(F, s); }));
+  return SBS_OK;
+}
+
+// enqueue one iteration on stream s with inputs c->P.in and outputs c->P.out
 int enqueue_step(sbs_ctx* c, cudaStream_t s) {
   Params& P = c->P;
   P.iter = c->iter;
   const int mode = c->cfg.mode;
-  const bool fused = c->cfg.world == 1;
-  CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, mode, fused, s); }));
-  if (mode == SBS_MPPI && !fused) {
-    // rank partial -> all-gather -> merge of the `world` partials in rank order
+  if (c->cfg.world > 1) {  // MPPI: rank record -> all-gather -> merge in rank order
+    if (c->external) return fail(c, SBS_ERR_STATE, "external exchange: use sbs_step_records / sbs_finish_records");
     const size_t n = (size_t)P.R * P.part_stride;
     float* mine = c->d_gather + (size_t)c->cfg.rank * n;
-    CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_merge(P, mine, s); }));
-    int rc = g_nccl.all_gather(mine, c->d_gather, n, kNcclFloat32, c->comm, s);
+    int rc = enqueue_records(c, s, mine);
+    if (rc != SBS_OK) return rc;
+    rc = g_nccl.all_gather(mine, c->d_gather, n, kNcclFloat32, c->comm, s);
     if (rc != 0) return fail(c, SBS_ERR_NCCL, std::string("ncclAllGather: ") + (g_nccl.err ? g_nccl.err(rc) : "?"));
-    Params F = P;
-    F.part = c->d_gather;
-    F.n_cta = c->cfg.world;
-    F.part_c_stride = P.R;  // gathered layout [world][R][stride]
-    CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_finalize(F, s); }));
-  } else if (mode == SBS_CEM) {
+    return enqueue_finish(c, s, c->d_gather);
+  }
+  CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, mode, true, s); }));
+  if (mode == SBS_CEM) {
     CK(timed(c, SBS_KERNEL_SELECT, s, [&] { return sbs::launch_select(P, s); }));
     CK(timed(c, SBS_KERNEL_ELITE, s, [&] { return sbs::launch_elite(P, s); }));
   }
@@ -492,6 +512,11 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   c->ref_set.assign(R, 0);
   // ---- NCCL (sample sharding) ----
   if (cfg->world > 1) {
+    bool zero_id = true;
+    for (int i = 0; i < 128; ++i) zero_id = zero_id && cfg->nccl_id[i] == 0;
+    c->external = zero_id;
+  }
+  if (cfg->world > 1 && !c->external) {
     if (!g_nccl.load()) {
       c->err = "world > 1 but libnccl.so.2 could not be loaded";
       return bail(SBS_ERR_NCCL);
@@ -615,6 +640,29 @@ int sbs_step_device(sbs_ctx* c, const sbs_input* d_in, sbs_output* d_out, void* 
   if (rc != SBS_OK) return rc;
   c->iter += 1;
   return SBS_OK;
+}
+
+int sbs_record_floats(const sbs_ctx* c) { return c ? c->P.part_stride : 0; }
+
+int sbs_step_records(sbs_ctx* c, const sbs_input* d_in, float* d_rec, void* stream) {
+  if (!c || !d_in || !d_rec) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (c->cfg.mode != SBS_MPPI) return fail(c, SBS_ERR_STATE, "records exchange is MPPI only");
+  for (int r = 0; r < c->P.R; ++r)
+    if (!c->ref_set[r]) return fail(c, SBS_ERR_STATE, "reference not set for every robot");
+  CK(cudaSetDevice(c->cfg.device));
+  c->P.in = d_in;
+  return enqueue_records(c, (cudaStream_t)stream, d_rec);
+}
+
+int sbs_finish_records(sbs_ctx* c, const float* d_recs, const sbs_input* d_in, sbs_output* d_out, void* stream) {
+  if (!c || !d_recs || !d_in || !d_out) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (c->cfg.mode != SBS_MPPI) return fail(c, SBS_ERR_STATE, "records exchange is MPPI only");
+  CK(cudaSetDevice(c->cfg.device));
+  c->P.in = d_in;
+  c->P.out = d_out;
+  const int rc = enqueue_finish(c, (cudaStream_t)stream, d_recs);
+  if (rc == SBS_OK) c->iter += 1;
+  return rc;
 }
 
 int sbs_get_state(sbs_ctx* c, void* buf, uint64_t* nbytes) {
@@ -764,7 +812,7 @@ int sbs_kernel_times(sbs_ctx* c, double* total_ms, int64_t* launches) {
 
 int sbs_launches_per_step(const sbs_ctx* c) {
   if (!c) return 0;
-  if (c->cfg.mode == SBS_MPPI) return c->cfg.world > 1 ? 3 : 1;
+  if (c->cfg.mode == SBS_MPPI) return c->cfg.world > 1 ? 2 : 1;
   return c->cfg.mode == SBS_NAIVE ? 1 : 3;
 }
 

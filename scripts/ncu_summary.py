@@ -63,7 +63,7 @@ def full(rep, out, K, H):
             cyc = t * g["sm__cycles_elapsed.avg.per_second"] * (1e9 if u[h.index("sm__cycles_elapsed.avg.per_second")] == "Ghz" else 1e6)
             rate = (2 * g[KEYS[-3]] + g[KEYS[-2]] + g[KEYS[-1]])
             flop = rate * cyc
-            f.write(f"\nDerived: executed FP32 FLOP = {flop:.4e}; per sample-step = {flop/(K*H):.1f}; "
+            f.write(f"\nDerived (scalar FFMA/FMUL/FADD counters only; packed FFMA2/FADD2/FMUL2 are not counted): FP32 FLOP = {flop:.4e}; per sample-step = {flop/(K*H):.1f}; "
                     f"instructions per sample = {g['inst_executed']*32/K:.0f}; "
                     f"FP32 FLOP/cycle/SM = {rate/148:.1f} of 256 ({rate/148/256:.1%}); "
                     f"DRAM bytes per launch = {g['dram__bytes_read.sum'] + g['dram__bytes_write.sum']:.4g}\n\n")

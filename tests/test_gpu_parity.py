@@ -311,3 +311,47 @@ def test_config5_full_size_sampled(B, orc):
         ro = orc.step(cfg, r, inputs[r], dict(st0))
         _check_costs(Jg[r], ro.J)
         _check_outputs(outs[r], ro, cfg)
+
+
+@pytest.mark.parametrize("K,world", [(10000, 2), (4097, 2), (8192, 4)])
+def test_sharded_mppi_records_match_single_gpu(B, orc, K, world):
+    """The world > 1 kernels (rank record + rank-order merge) on one GPU: `world`
+    contexts each roll out their slice and emit a record, the records are
+    concatenated in rank order (what the NCCL all-gather does) and every rank
+    finishes the iteration; all ranks agree with each other and with world = 1."""
+    import ctypes as C
+
+    import torch
+    cfg, inputs = W.config2(K=K)
+    st = W.initial_distribution(cfg)
+    arr = B.make_inputs(inputs)
+    d_in = torch.from_numpy(np.frombuffer(bytes(arr), dtype=np.uint8).copy()).cuda()
+    ranks = [B.Controller(cfg, rank=g, world=world) for g in range(world)]
+    for c in ranks:
+        c.set_reference(0, inputs[0]["xref"])
+    nrec = ranks[0].record_floats()
+    recs = torch.zeros((world, nrec), dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    slices = [c.local_range() for c in ranks]
+    assert slices[0][0] == 0 and sum(kl for _, kl in slices) == K
+    for g, c in enumerate(ranks):
+        c.step_records(d_in.data_ptr(), recs[g].data_ptr(), s)
+    outs = []
+    for c in ranks:
+        d_out = torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+        c.finish_records(recs.data_ptr(), d_in.data_ptr(), d_out.data_ptr(), s)
+        torch.cuda.synchronize()
+        o = B.sbs_output.from_buffer_copy(d_out.cpu().numpy().tobytes())
+        outs.append(B.output_dict(o, 48))
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o["mean"], outs[0]["mean"])
+        assert o["freq_idx"] == outs[0]["freq_idx"]
+    J = np.concatenate([c.debug_costs()[0] for c in ranks])
+    single = _ctrl(B, cfg, inputs, st)
+    _, so = single.step(inputs)
+    np.testing.assert_array_equal(J, single.debug_costs()[0])       # same samples, same costs
+    assert outs[0]["j_min"] == so[0]["j_min"] and outs[0]["n_diverged"] == so[0]["n_diverged"]
+    assert np.max(np.abs(outs[0]["mean"] - so[0]["mean"])) <= 1e-5 * max(np.max(np.abs(so[0]["mean"])), 1.0)
+    ro = orc.step(cfg, 0, inputs[0], dict(st))
+    _check_outputs(outs[0], ro, cfg)
+    assert all(c.iter == 1 for c in ranks)
