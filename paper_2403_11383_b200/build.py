@@ -13,7 +13,7 @@ SOURCES = ["sbs_kernels.cu", "sbs_api.cpp"]
 HEADERS = ["sbs_internal.h", "sbs_noise.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-Wall", "-cudart", "static",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-diag-suppress", "177,550", "-Xcompiler", "-fPIC,-O2,-Wall", "-cudart", "static",
          "--expt-relaxed-constexpr"]
 
 
@@ -31,19 +31,34 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in _inputs())
 
 
+def _units():
+    """(source, extra defines, object suffix): the kernels file once per knot count and once
+    for the common kernels, plus the host runtime -- compiled in parallel."""
+    units = [("sbs_kernels.cu", [f"SBS_TU_P={p}"], f"p{p}") for p in range(2, 9)]
+    units.append(("sbs_kernels.cu", ["SBS_TU_COMMON"], "common"))
+    units.append(("sbs_api.cpp", [], "api"))
+    return units
+
+
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
     """Compile csrc/ into `out` (default: the in-tree libsbs.so)."""
     if out == LIB and not force and not stale():
         return LIB
-    objs = []
-    for src in SOURCES:
-        obj = os.path.join(CSRC, src + (".o" if out == LIB else f".{os.path.basename(out)}.o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
-               os.path.join(CSRC, src), "-o", obj]
+    from concurrent.futures import ThreadPoolExecutor
+    tag = "" if out == LIB else "." + os.path.basename(out)
+
+    def compile_unit(u):
+        src, defs, suffix = u
+        obj = os.path.join(CSRC, f"{src}.{suffix}{tag}.o")
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in (*defines, *defs)], "-I", os.path.join(ROOT, "include"),
+               "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
         subprocess.check_call(cmd)
-        objs.append(obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(9, os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_unit, _units()))
     tmp = out + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, out)

@@ -82,6 +82,7 @@ struct sbs_ctx {
   int* d_status = nullptr;
   int* d_counter = nullptr;
   float* d_epart = nullptr;
+  float* d_sdiag = nullptr;
   sbs_input* d_in = nullptr;
   sbs_output* d_out = nullptr;
   sbs_input* h_in = nullptr;   // pinned
@@ -320,7 +321,7 @@ void sbs_destroy(sbs_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
   for (void* p : {(void*)c->d_mean, (void*)c->d_var, (void*)c->d_fidx, (void*)c->d_xref, (void*)c->d_J,
-                  (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart,
+                  (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart, (void*)c->d_sdiag,
                   (void*)c->d_in, (void*)c->d_out})
     if (p) cudaFree(p);
   if (c->h_in) cudaFreeHost(c->h_in);
@@ -474,6 +475,7 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaMemset(c->d_counter, 0, 2 * R * sizeof(int)));
   P.n_eblk = P.n_elite > 0 ? (int)((P.n_elite + 31) / 32) : 1;  // 32 elites per elite-kernel CTA
   CKC(cudaMalloc(&c->d_epart, (size_t)R * P.n_eblk * sbs::kEPartStride * sizeof(float)));
+  CKC(cudaMalloc(&c->d_sdiag, (size_t)R * 8 * sizeof(float)));
   CKC(cudaMalloc(&c->d_in, R * sizeof(sbs_input)));
   CKC(cudaMalloc(&c->d_out, R * sizeof(sbs_output)));
   CKC(cudaMallocHost(&c->h_in, R * sizeof(sbs_input)));
@@ -509,6 +511,7 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.counter = c->d_counter;
   P.ecounter = c->d_counter + R;
   P.epart = c->d_epart;
+  P.sdiag = c->d_sdiag;
   c->ref_set.assign(R, 0);
   // ---- NCCL (sample sharding) ----
   if (cfg->world > 1) {

@@ -71,6 +71,7 @@ struct Params {
   int* ecounter;              // [R] arrival counters of the elite kernel
   float* epart;               // [R][n_eblk][kEPartStride] CEM elite-moment records
   int n_eblk;                 // elite blocks per robot
+  float* sdiag;               // [R][8] CEM: J_min, k_best, theta1_best, sum J, n finite (select kernel)
 };
 
 // launchers (sbs_kernels.cu); return cudaGetLastError()

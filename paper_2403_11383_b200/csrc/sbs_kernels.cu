@@ -44,7 +44,7 @@ __device__ __forceinline__ int xref_slot(int a) { return a == 2 ? 4 : (a == 3 ? 
 // step a0: mu'[p] = S_mu(min(t_p + dt, T)); std = sqrt(var).
 // Also the contact table of every frequency option (O7, L22, L23) from the
 // Q0.32 phase: one byte per (theta1, step).
-__device__ void load_robot(const Params& p, int r, RobotSmem& s) {
+static __device__ void load_robot(const Params& p, int r, RobotSmem& s, bool rollout_inputs = true) {
   const int D = p.D, P = p.P;
   const float* mean = p.mean + (size_t)r * D;
   const float* var = p.var + (size_t)r * D;
@@ -60,6 +60,8 @@ __device__ void load_robot(const Params& p, int r, RobotSmem& s) {
     s.sig[d] = __fsqrt_rn(var[d]);
   }
   const sbs_input* in = p.in + r;
+  if (threadIdx.x == 0) s.cur_idx = p.fidx[r];
+  if (!rollout_inputs) return;  // sampling only (elite regeneration, debug draws)
   for (int a = threadIdx.x; a < 12; a += blockDim.x) {
     s.x0[a] = in->x0[a];
     s.feet[a] = in->feet_cur[a];
@@ -86,10 +88,7 @@ __device__ void load_robot(const Params& p, int r, RobotSmem& s) {
       s.ctab[f][j] = (uint8_t)(st | (td << 4));
     }
   }
-  if (threadIdx.x == 0) {
-    s.phase0 = ph0;
-    s.cur_idx = p.fidx[r];
-  }
+  if (threadIdx.x == 0) s.phase0 = ph0;
 }
 
 // theta2 of one sample in registers, organised per leg: (x, y) knot pairs for
@@ -213,7 +212,7 @@ __device__ __forceinline__ void ang_deriv(const Params& p, float2 A, float2 B, f
 // Per-leg work sits behind the stance bit: with a fixed gait every lane of a warp
 // shares the contact schedule, so swing legs cost nothing.
 template <int P>
-__device__ float rollout(const Params& p, const Theta<P>& th, int fi, const RobotSmem& s) {
+static __device__ float rollout(const Params& p, const Theta<P>& th, int fi, const RobotSmem& s) {
   float2 pxy = f2(s.x0[0], s.x0[1]), vxy = f2(s.x0[3], s.x0[4]);
   float pz = s.x0[2], vz = s.x0[5];
   float2 A = f2(s.x0[6], s.x0[7]), Bq = f2(s.x0[8], s.x0[9]), C = f2(s.x0[10], s.x0[11]);
@@ -379,7 +378,7 @@ __device__ __forceinline__ void stage_copy(float* dst, const float* src, int n) 
 // ---------------------------------------------------------------------------
 // Output (a7): u0 = delta_0-masked cone projection of knot 0.
 // ---------------------------------------------------------------------------
-__device__ void write_output(const Params& p, int r, int status, const float* mean_new, const float* var_new,
+static __device__ void write_output(const Params& p, int r, int status, const float* mean_new, const float* var_new,
                              int fi, float jmin, float jmean, float omega, float ess, int ndiv) {
   sbs_output* o = p.out + r;
   const int D = p.D;
@@ -419,7 +418,7 @@ struct Best {
   float m;
   int k, f;
 };
-__device__ Best merge_argmin(const Params& p, int r) {
+static __device__ Best merge_argmin(const Params& p, int r) {
   __shared__ float s_m[32];
   __shared__ int s_k[32], s_f[32];
   float m = kInf;
@@ -455,7 +454,7 @@ __device__ Best merge_argmin(const Params& p, int r) {
 // instead of finishing.  blockDim.x = 128; rows split over two column groups.
 // ---------------------------------------------------------------------------
 template <bool EMIT>
-__device__ void mppi_merge_block(const Params& p, int r, float* emit, float* stage, int stage_floats) {
+static __device__ void mppi_merge_block(const Params& p, int r, float* emit, float* stage, int stage_floats) {
   const int tid = threadIdx.x, D = p.D, NR = D + 4, RL = p.part_stride;
   __shared__ float s_row[1][SBS_MAX_D + 4];
   __shared__ float s_sc[128];
@@ -532,7 +531,7 @@ __device__ void mppi_merge_block(const Params& p, int r, float* emit, float* sta
 // Naive UpdateMean (Alg. 3): the best sample theta* becomes the mean,
 // regenerated from the counter RNG; C unchanged.
 template <int P>
-__device__ void naive_finalize_block(const Params& p, int r, const RobotSmem& s) {
+static __device__ void naive_finalize_block(const Params& p, int r, const RobotSmem& s) {
   constexpr int D = 12 * P;
   __shared__ float s_mean[D], s_var[D];
   __shared__ float s_sum[2];
@@ -794,7 +793,7 @@ constexpr int kSelSmemBytes = 200 * 1024;           // dynamic shared memory of 
 constexpr int kSelSmemKeys = kSelSmemBytes / 4 - kSelHistWords;
 
 // smem: [kSelHistWords] per-warp histograms, then the keys when K <= kSelSmemKeys
-__device__ void select_block(const float* J, int64_t K, int64_t K_e, int64_t k_begin, int64_t* elite,
+static __device__ void select_block(const float* J, int64_t K, int64_t K_e, int64_t k_begin, int64_t* elite,
                              uint32_t* smem) {
   __shared__ uint32_t s_prefix, s_want;
   __shared__ uint32_t s_wsum[kSelBlock / 32];
@@ -904,18 +903,20 @@ __device__ void select_block(const float* J, int64_t K, int64_t K_e, int64_t k_b
   }
 }
 
-// Fast path for K <= kSelSmallMax: every thread keeps a contiguous run of at most
-// 16 keys in registers.  Two passes over 16-bit digits (65536 packed 16-bit
-// counters in 128 KB of shared memory) give the exact K_e-th smallest key T and
-// the number of ties at T to take; one block scan of per-thread (lt, eq) counts
-// then places the elites in index order.
-constexpr int kSelSmallMax = 16384;
-constexpr int kSelKPT = kSelSmallMax / kSelBlock;
-constexpr int kSelSmallSmemBytes = 32768 * 4;
+// Fast path for K <= kSelSmallMax, one CTA of kSmallBlock threads: every thread
+// keeps a contiguous run of at most 64 keys in registers; three digit passes
+// (11, 11, 10 bits) with a 2048-bin shared-memory histogram each give
+// the exact K_e-th smallest key T and the number of ties at T to take; one
+// block scan of per-thread (lt, eq) counts then places the elites in index
+// order.  Also merges the rollout records' diagnostics (argmin, sum J, n finite).
+constexpr int kSmallBlock = 256;
+constexpr int kSelKPT = 64;
+constexpr int kSelSmallMax = kSmallBlock * kSelKPT;          // 16384 keys
+constexpr int kSmallBins = 2048;
+constexpr int kSelSmallSmemBytes = kSmallBins * 4;  // 8 KB
 
-// exclusive block scan of v over kSelBlock threads; returns the total in *tot
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_w, uint32_t* tot) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ uint32_t block_excl_scan_small(uint32_t v, uint32_t* s_w, uint32_t* tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   uint32_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -924,83 +925,69 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_w, u
   }
   if (lane == 31) s_w[warp] = x;
   __syncthreads();
-  if (warp == 0) {
-    uint32_t w = s_w[lane];
-    uint32_t wx = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, wx, o);
-      if (lane >= o) wx += y;
-    }
-    s_w[lane] = wx - w;       // exclusive warp offsets
-    if (lane == 31) s_w[32] = wx;
+  uint32_t off = 0, t = 0;
+  for (int w = 0; w < nw; ++w) {
+    const uint32_t c = s_w[w];
+    off += w < warp ? c : 0u;
+    t += c;
   }
+  *tot = t;
   __syncthreads();
-  const uint32_t r = s_w[warp] + x - v;
-  *tot = s_w[32];
-  __syncthreads();
-  return r;
+  return off + x - v;
 }
 
-// 16-bit digit pass: count keys with (key & pmask) == pref by digit (key >> sh) & 0xFFFF,
-// find digit B with rank `want` inside; returns B and the count strictly below it.
-__device__ void digit16_pass(const uint32_t (&key)[kSelKPT], int nk, uint32_t pmask, uint32_t pref, int sh,
-                             uint32_t want, uint32_t* hist, uint32_t* s_w, uint32_t* s_res) {
+// one digit pass over keys with (key & pmask) == pref, digit = (key >> sh) & (nb - 1);
+// returns in s_res the digit holding rank `want` and the count strictly below it
+static __device__ void digit_pass_small(const uint32_t (&key)[kSelKPT], int nk, uint32_t pmask, uint32_t pref, int sh,
+                                 int nb, uint32_t want, uint32_t* hist, uint32_t* s_w, uint32_t* s_res) {
   const int tid = threadIdx.x;
-  for (int i = tid; i < 32768; i += kSelBlock) hist[i] = 0;
+  for (int i = tid; i < kSmallBins; i += blockDim.x) hist[i] = 0;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i)
-    if (i < nk && (key[i] & pmask) == pref) {
-      const uint32_t d = (key[i] >> sh) & 0xFFFFu;
-      atomicAdd(&hist[d >> 1], 1u << ((d & 1u) << 4));
-    }
+    if (i < nk && (key[i] & pmask) == pref) atomicAdd(&hist[(key[i] >> sh) & (uint32_t)(nb - 1)], 1u);
   __syncthreads();
-  // thread t owns digits [64 t, 64 t + 64)
+  // thread t owns the bins [t * per, (t + 1) * per); read in a rotated order (bank spread)
+  const int per = nb / blockDim.x;
   uint32_t loc = 0;
-  for (int w = 0; w < 32; ++w) {
-    const uint32_t h = hist[tid * 32 + ((w + tid) & 31)];  // rotated start: no bank conflicts
-    loc += (h & 0xFFFFu) + (h >> 16);
-  }
+  for (int b = 0; b < per; ++b) loc += hist[tid * per + ((b + tid) & (per - 1))];
   uint32_t tot;
-  const uint32_t base = block_excl_scan(loc, s_w, &tot);
+  const uint32_t base = block_excl_scan_small(loc, s_w, &tot);
   if (base < want && want <= base + loc) {
     uint32_t cum = base;
-    for (int w = 0; w < 32; ++w) {
-      const uint32_t h = hist[tid * 32 + w];
-      const uint32_t c0 = h & 0xFFFFu, c1 = h >> 16;
-      if (cum + c0 >= want) {
-        s_res[0] = (uint32_t)(tid * 64 + 2 * w);
+    for (int b = 0; b < per; ++b) {
+      const uint32_t c = hist[tid * per + b];
+      if (cum + c >= want) {
+        s_res[0] = (uint32_t)(tid * per + b);
         s_res[1] = cum;
         break;
       }
-      cum += c0;
-      if (cum + c1 >= want) {
-        s_res[0] = (uint32_t)(tid * 64 + 2 * w + 1);
-        s_res[1] = cum;
-        break;
-      }
-      cum += c1;
+      cum += c;
     }
   }
   __syncthreads();
 }
 
-__device__ void select_block_small(const float* J, int K, int K_e, int64_t k_begin, int64_t* elite, uint32_t* hist) {
-  __shared__ uint32_t s_w[33];
+static __device__ void select_block_small(const float* J, int K, int K_e, int64_t k_begin, int64_t* elite, uint32_t* hist) {
+  __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_res[2];
   const int tid = threadIdx.x;
-  const int per = (K + kSelBlock - 1) / kSelBlock;
+  const int per = (K + blockDim.x - 1) / blockDim.x;
   const int k0 = tid * per;
   const int nk = max(0, min(per, K - k0));
   uint32_t key[kSelKPT];
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i) key[i] = i < nk ? cost_key(J[k0 + i]) : 0xFFFFFFFFu;
-  digit16_pass(key, nk, 0u, 0u, 16, (uint32_t)K_e, hist, s_w, s_res);
-  const uint32_t hi = s_res[0], below_hi = s_res[1];
-  digit16_pass(key, nk, 0xFFFF0000u, hi << 16, 0, (uint32_t)K_e - below_hi, hist, s_w, s_res);
-  const uint32_t T = (hi << 16) | s_res[0];
-  const uint32_t n_eq = (uint32_t)K_e - below_hi - s_res[1];  // ties at T to take, lowest indices first
+  uint32_t want = (uint32_t)K_e;
+  digit_pass_small(key, nk, 0u, 0u, 21, 2048, want, hist, s_w, s_res);
+  const uint32_t d1 = s_res[0];
+  want -= s_res[1];
+  digit_pass_small(key, nk, 0xFFE00000u, d1 << 21, 10, 2048, want, hist, s_w, s_res);
+  const uint32_t d2 = s_res[0];
+  want -= s_res[1];
+  digit_pass_small(key, nk, 0xFFFFFC00u, (d1 << 21) | (d2 << 10), 0, 1024, want, hist, s_w, s_res);
+  const uint32_t T = (d1 << 21) | (d2 << 10) | s_res[0];
+  const uint32_t n_eq = want - s_res[1];  // ties at T to take, lowest indices first
   uint32_t lt = 0, eq = 0;
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i)
@@ -1009,8 +996,8 @@ __device__ void select_block_small(const float* J, int K, int K_e, int64_t k_beg
       eq += key[i] == T;
     }
   uint32_t t1, t2;
-  const uint32_t lt_before = block_excl_scan(lt, s_w, &t1);
-  uint32_t eq_before = block_excl_scan(eq, s_w, &t2);
+  const uint32_t lt_before = block_excl_scan_small(lt, s_w, &t1);
+  uint32_t eq_before = block_excl_scan_small(eq, s_w, &t2);
   uint32_t pos = lt_before + min(eq_before, n_eq);
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i)
@@ -1020,25 +1007,62 @@ __device__ void select_block_small(const float* J, int K, int K_e, int64_t k_beg
     }
 }
 
+// also merges robot r's rollout records into p.sdiag[r] = (J_min, k_best, theta1_best, sum J, n finite)
+static __device__ void merge_diag(const Params& p, int r) {
+  const Best b = merge_argmin(p, r);
+  if (threadIdx.x < 32) {
+    float sj = 0.f, nf = 0.f;
+    for (int c = threadIdx.x; c < p.n_cta; c += 32) {
+      const float* pc = part_rec(p, r, c);
+      sj += __ldcg(pc + 5);
+      nf += __ldcg(pc + 6);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sj += __shfl_xor_sync(0xffffffffu, sj, o);
+      nf += __shfl_xor_sync(0xffffffffu, nf, o);
+    }
+    if (threadIdx.x == 0) {
+      float* d = p.sdiag + (size_t)r * 8;
+      d[0] = b.m;
+      d[1] = __int_as_float(b.k);
+      d[2] = __int_as_float(b.f);
+      d[3] = sj;
+      d[4] = nf;
+    }
+  }
+}
+
+#if defined(SBS_TU_COMMON)
 __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint32_t sel_smem[];
   const int r = blockIdx.x;
-  if (p.K_local <= kSelSmallMax)
-    select_block_small(p.J + (size_t)r * p.K_local, (int)p.K_local, (int)p.n_elite, p.k_begin,
-                       p.elite + (size_t)r * p.n_elite, sel_smem);
-  else
-    select_block(p.J + (size_t)r * p.K_local, p.K_local, p.n_elite, p.k_begin, p.elite + (size_t)r * p.n_elite,
-                 sel_smem);
+  merge_diag(p, r);
+  select_block(p.J + (size_t)r * p.K_local, p.K_local, p.n_elite, p.k_begin, p.elite + (size_t)r * p.n_elite,
+               sel_smem);
+}
+
+__global__ void __launch_bounds__(kSmallBlock) sbs_select_small_kernel(const __grid_constant__ Params p) {
+  extern __shared__ uint32_t sel_smem[];
+  const int r = blockIdx.x;
+  merge_diag(p, r);
+  select_block_small(p.J + (size_t)r * p.K_local, (int)p.K_local, (int)p.n_elite, p.k_begin,
+                     p.elite + (size_t)r * p.n_elite, sel_smem);
 }
 
 __global__ void __launch_bounds__(kSelBlock) sbs_select_raw_kernel(const float* J, int64_t K, int64_t K_e,
                                                                    int64_t* idx) {
   extern __shared__ uint32_t sel_smem[];
-  if (K <= kSelSmallMax)
-    select_block_small(J, (int)K, (int)K_e, 0, idx, sel_smem);
-  else
-    select_block(J, K, K_e, 0, idx, sel_smem);
+  select_block(J, K, K_e, 0, idx, sel_smem);
 }
+
+__global__ void __launch_bounds__(kSmallBlock) sbs_select_small_raw_kernel(const float* J, int64_t K, int64_t K_e,
+                                                                           int64_t* idx) {
+  extern __shared__ uint32_t sel_smem[];
+  select_block_small(J, (int)K, (int)K_e, 0, idx, sel_smem);
+}
+
+#endif  // SBS_TU_COMMON
 
 // ---------------------------------------------------------------------------
 // sbs_elite_kernel (CEM, Alg. 1 UpdateMean / UpdateCov, L17): grid (n_eblk, R),
@@ -1059,7 +1083,7 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   __shared__ __align__(16) float s_stage[16 * kEPartStride];
   __shared__ float s_diag[2];
   const int r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
-  load_robot(p, r, s);
+  load_robot(p, r, s, false);
   __syncthreads();
   const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
   const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
@@ -1109,23 +1133,12 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
     }
     if (tid < 2 * D + 1) s_tot[tid] = a0;
   }
-  const Best b = merge_argmin(p, r);  // rank-1 sample and diagnostics from the rollout records
-  if (tid < 32) {
-    float sj = 0.f, nf = 0.f;
-    for (int c = tid; c < p.n_cta; c += 32) {
-      const float* pc = part_rec(p, r, c);
-      sj += __ldcg(pc + 5);
-      nf += __ldcg(pc + 6);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sj += __shfl_xor_sync(0xffffffffu, sj, o);
-      nf += __shfl_xor_sync(0xffffffffu, nf, o);
-    }
-    if (tid == 0) {
-      s_diag[0] = sj;
-      s_diag[1] = nf;
-    }
+  // rank-1 sample and diagnostics, merged from the rollout records by the select kernel
+  const float* sd = p.sdiag + (size_t)r * 8;
+  const Best b{sd[0], __float_as_int(sd[1]), __float_as_int(sd[2])};
+  if (tid == 0) {
+    s_diag[0] = sd[3];
+    s_diag[1] = sd[4];
   }
   __syncthreads();
   const float ne = s_tot[D];
@@ -1163,7 +1176,7 @@ __global__ void __launch_bounds__(128) sbs_debug_samples_kernel(const __grid_con
                                                                 int64_t n, float* z, float* theta, int* fidx) {
   constexpr int D = 12 * P;
   __shared__ RobotSmem s;
-  load_robot(p, r, s);
+  load_robot(p, r, s, false);
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1179,8 +1192,20 @@ __global__ void __launch_bounds__(128) sbs_debug_samples_kernel(const __grid_con
 }
 
 // ---------------------------------------------------------------------------
-// launchers
+// launchers.  The build compiles this file once per knot count P (-DSBS_TU_P=P:
+// the rollout / elite / debug kernels for that P) and once with -DSBS_TU_COMMON
+// (dispatch, select and merge kernels), in parallel.
 // ---------------------------------------------------------------------------
+template <int P>
+struct PEntry {
+  static cudaError_t rollout(const Params& p, int mode, bool fused, cudaStream_t s);
+  static int occupancy(int mode);
+  static cudaError_t elite(const Params& p, cudaStream_t s);
+  static cudaError_t debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
+                                   int* fidx, cudaStream_t s);
+};
+
+#if defined(SBS_TU_P)
 template <int P, int EPI, bool FUSED>
 static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
   constexpr int D = 12 * P;
@@ -1196,14 +1221,14 @@ static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
 }
 
 template <int P>
-static cudaError_t launch_rollout_p(const Params& p, int mode, bool fused, cudaStream_t s) {
+cudaError_t PEntry<P>::rollout(const Params& p, int mode, bool fused, cudaStream_t s) {
   if (mode == SBS_MPPI) return fused ? launch_rollout_t<P, EPI_MPPI, true>(p, s) : launch_rollout_t<P, EPI_MPPI, false>(p, s);
   if (mode == SBS_NAIVE) return launch_rollout_t<P, EPI_ARGMIN, true>(p, s);
   return launch_rollout_t<P, EPI_ARGMIN, false>(p, s);  // CEM: select + elite kernels follow
 }
 
 template <int P>
-static int occupancy_t(int mode) {
+int PEntry<P>::occupancy(int mode) {
   constexpr int D = 12 * P;
   const size_t smem = mode == SBS_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : 0;
   const void* f = mode == SBS_MPPI ? (const void*)sbs_rollout_kernel<P, EPI_MPPI, true>
@@ -1214,32 +1239,56 @@ static int occupancy_t(int mode) {
   return n > 0 ? n : 1;
 }
 
-#define SBS_DISPATCH_P(P_, EXPR) \
-  switch (P_) {                  \
-    case 2: { constexpr int PP = 2; EXPR; } \
-    case 3: { constexpr int PP = 3; EXPR; } \
-    case 4: { constexpr int PP = 4; EXPR; } \
-    case 5: { constexpr int PP = 5; EXPR; } \
-    case 6: { constexpr int PP = 6; EXPR; } \
-    case 7: { constexpr int PP = 7; EXPR; } \
-    case 8: { constexpr int PP = 8; EXPR; } \
-    default: return cudaErrorInvalidValue; \
+template <int P>
+cudaError_t PEntry<P>::elite(const Params& p, cudaStream_t s) {
+  dim3 grid(p.n_eblk, p.R);
+  sbs_elite_kernel<P><<<grid, 32 * 3 * P, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int P>
+cudaError_t PEntry<P>::debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
+                                     int* fidx, cudaStream_t s) {
+  const int blocks = (int)((n + 127) / 128);
+  sbs_debug_samples_kernel<P><<<blocks, 128, 0, s>>>(p, robot, k0, n, z, theta, fidx);
+  return cudaGetLastError();
+}
+
+template struct PEntry<SBS_TU_P>;
+#endif  // SBS_TU_P
+
+#if defined(SBS_TU_COMMON)
+#define SBS_DISPATCH_P(P_, CALL)                 \
+  switch (P_) {                                  \
+    case 2: return PEntry<2>::CALL;              \
+    case 3: return PEntry<3>::CALL;              \
+    case 4: return PEntry<4>::CALL;              \
+    case 5: return PEntry<5>::CALL;              \
+    case 6: return PEntry<6>::CALL;              \
+    case 7: return PEntry<7>::CALL;              \
+    case 8: return PEntry<8>::CALL;              \
+    default: break;                              \
   }
 
 cudaError_t launch_rollout(const Params& p, int mode, bool fused, cudaStream_t s) {
-  SBS_DISPATCH_P(p.P, return launch_rollout_p<PP>(p, mode, fused, s));
+  SBS_DISPATCH_P(p.P, rollout(p, mode, fused, s));
+  return cudaErrorInvalidValue;
 }
 
 int rollout_occupancy(int P, int mode) {
-  switch (P) {
-    case 2: return occupancy_t<2>(mode);
-    case 3: return occupancy_t<3>(mode);
-    case 4: return occupancy_t<4>(mode);
-    case 5: return occupancy_t<5>(mode);
-    case 6: return occupancy_t<6>(mode);
-    case 7: return occupancy_t<7>(mode);
-    default: return occupancy_t<8>(mode);
-  }
+  SBS_DISPATCH_P(P, occupancy(mode));
+  return 1;
+}
+
+cudaError_t launch_elite(const Params& p, cudaStream_t s) {
+  SBS_DISPATCH_P(p.P, elite(p, s));
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
+                                 int* fidx, cudaStream_t s) {
+  SBS_DISPATCH_P(p.P, debug_samples(p, robot, k0, n, z, theta, fidx, s));
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_mppi_finalize(const Params& p, cudaStream_t s) {
@@ -1257,6 +1306,9 @@ static size_t select_smem(int64_t K) {
   if (!attr) {
     cudaFuncSetAttribute(sbs_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
     cudaFuncSetAttribute(sbs_select_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
+    cudaFuncSetAttribute(sbs_select_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmallSmemBytes);
+    cudaFuncSetAttribute(sbs_select_small_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSelSmallSmemBytes);
     attr = true;
   }
   if (K <= kSelSmallMax) return (size_t)kSelSmallSmemBytes;
@@ -1264,25 +1316,18 @@ static size_t select_smem(int64_t K) {
 }
 
 cudaError_t launch_select(const Params& p, cudaStream_t s) {
-  sbs_select_kernel<<<p.R, kSelBlock, select_smem(p.K_local), s>>>(p);
+  const size_t smem = select_smem(p.K_local);
+  if (p.K_local <= kSelSmallMax) sbs_select_small_kernel<<<p.R, kSmallBlock, smem, s>>>(p);
+  else sbs_select_kernel<<<p.R, kSelBlock, smem, s>>>(p);
   return cudaGetLastError();
-}
-
-cudaError_t launch_elite(const Params& p, cudaStream_t s) {
-  dim3 grid(p.n_eblk, p.R);
-  SBS_DISPATCH_P(p.P, (sbs_elite_kernel<PP><<<grid, 32 * 3 * PP, 0, s>>>(p)); return cudaGetLastError());
-}
-
-cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
-                                 int* fidx, cudaStream_t s) {
-  const int blocks = (int)((n + 127) / 128);
-  SBS_DISPATCH_P(p.P, (sbs_debug_samples_kernel<PP><<<blocks, 128, 0, s>>>(p, robot, k0, n, z, theta, fidx));
-                 return cudaGetLastError());
 }
 
 cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s) {
-  sbs_select_raw_kernel<<<1, kSelBlock, select_smem(K), s>>>(J, K, K_e, idx);
+  const size_t smem = select_smem(K);
+  if (K <= kSelSmallMax) sbs_select_small_raw_kernel<<<1, kSmallBlock, smem, s>>>(J, K, K_e, idx);
+  else sbs_select_raw_kernel<<<1, kSelBlock, smem, s>>>(J, K, K_e, idx);
   return cudaGetLastError();
 }
+#endif  // SBS_TU_COMMON
 
 }  // namespace sbs
