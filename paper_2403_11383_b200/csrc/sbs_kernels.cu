@@ -903,20 +903,18 @@ static __device__ void select_block(const float* J, int64_t K, int64_t K_e, int6
   }
 }
 
-// Fast path for K <= kSelSmallMax, one CTA of kSmallBlock threads: every thread
-// keeps a contiguous run of at most 64 keys in registers; three digit passes
-// (11, 11, 10 bits) with a 2048-bin shared-memory histogram each give
-// the exact K_e-th smallest key T and the number of ties at T to take; one
-// block scan of per-thread (lt, eq) counts then places the elites in index
-// order.  Also merges the rollout records' diagnostics (argmin, sum J, n finite).
-constexpr int kSmallBlock = 256;
-constexpr int kSelKPT = 64;
-constexpr int kSelSmallMax = kSmallBlock * kSelKPT;          // 16384 keys
-constexpr int kSmallBins = 2048;
-constexpr int kSelSmallSmemBytes = kSmallBins * 4;  // 8 KB
+// Fast path for K <= kSelSmallMax: every thread keeps a contiguous run of at most
+// 16 keys in registers.  Two passes over 16-bit digits (65536 packed 16-bit
+// counters in 128 KB of shared memory) give the exact K_e-th smallest key T and
+// the number of ties at T to take; one block scan of per-thread (lt, eq) counts
+// then places the elites in index order.
+constexpr int kSelSmallMax = 16384;
+constexpr int kSelKPT = kSelSmallMax / kSelBlock;
+constexpr int kSelSmallSmemBytes = 32768 * 4;
 
-__device__ __forceinline__ uint32_t block_excl_scan_small(uint32_t v, uint32_t* s_w, uint32_t* tot) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+// exclusive block scan of v over kSelBlock threads; returns the total in *tot
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_w, uint32_t* tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -925,69 +923,83 @@ __device__ __forceinline__ uint32_t block_excl_scan_small(uint32_t v, uint32_t* 
   }
   if (lane == 31) s_w[warp] = x;
   __syncthreads();
-  uint32_t off = 0, t = 0;
-  for (int w = 0; w < nw; ++w) {
-    const uint32_t c = s_w[w];
-    off += w < warp ? c : 0u;
-    t += c;
+  if (warp == 0) {
+    uint32_t w = s_w[lane];
+    uint32_t wx = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wx, o);
+      if (lane >= o) wx += y;
+    }
+    s_w[lane] = wx - w;       // exclusive warp offsets
+    if (lane == 31) s_w[32] = wx;
   }
-  *tot = t;
   __syncthreads();
-  return off + x - v;
+  const uint32_t r = s_w[warp] + x - v;
+  *tot = s_w[32];
+  __syncthreads();
+  return r;
 }
 
-// one digit pass over keys with (key & pmask) == pref, digit = (key >> sh) & (nb - 1);
-// returns in s_res the digit holding rank `want` and the count strictly below it
-static __device__ void digit_pass_small(const uint32_t (&key)[kSelKPT], int nk, uint32_t pmask, uint32_t pref, int sh,
-                                 int nb, uint32_t want, uint32_t* hist, uint32_t* s_w, uint32_t* s_res) {
+// 16-bit digit pass: count keys with (key & pmask) == pref by digit (key >> sh) & 0xFFFF,
+// find digit B with rank `want` inside; returns B and the count strictly below it.
+static __device__ void digit16_pass(const uint32_t (&key)[kSelKPT], int nk, uint32_t pmask, uint32_t pref, int sh,
+                             uint32_t want, uint32_t* hist, uint32_t* s_w, uint32_t* s_res) {
   const int tid = threadIdx.x;
-  for (int i = tid; i < kSmallBins; i += blockDim.x) hist[i] = 0;
+  for (int i = tid; i < 32768; i += kSelBlock) hist[i] = 0;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i)
-    if (i < nk && (key[i] & pmask) == pref) atomicAdd(&hist[(key[i] >> sh) & (uint32_t)(nb - 1)], 1u);
+    if (i < nk && (key[i] & pmask) == pref) {
+      const uint32_t d = (key[i] >> sh) & 0xFFFFu;
+      atomicAdd(&hist[d >> 1], 1u << ((d & 1u) << 4));
+    }
   __syncthreads();
-  // thread t owns the bins [t * per, (t + 1) * per); read in a rotated order (bank spread)
-  const int per = nb / blockDim.x;
+  // thread t owns digits [64 t, 64 t + 64)
   uint32_t loc = 0;
-  for (int b = 0; b < per; ++b) loc += hist[tid * per + ((b + tid) & (per - 1))];
+  for (int w = 0; w < 32; ++w) {
+    const uint32_t h = hist[tid * 32 + ((w + tid) & 31)];  // rotated start: no bank conflicts
+    loc += (h & 0xFFFFu) + (h >> 16);
+  }
   uint32_t tot;
-  const uint32_t base = block_excl_scan_small(loc, s_w, &tot);
+  const uint32_t base = block_excl_scan(loc, s_w, &tot);
   if (base < want && want <= base + loc) {
     uint32_t cum = base;
-    for (int b = 0; b < per; ++b) {
-      const uint32_t c = hist[tid * per + b];
-      if (cum + c >= want) {
-        s_res[0] = (uint32_t)(tid * per + b);
+    for (int w = 0; w < 32; ++w) {
+      const uint32_t h = hist[tid * 32 + w];
+      const uint32_t c0 = h & 0xFFFFu, c1 = h >> 16;
+      if (cum + c0 >= want) {
+        s_res[0] = (uint32_t)(tid * 64 + 2 * w);
         s_res[1] = cum;
         break;
       }
-      cum += c;
+      cum += c0;
+      if (cum + c1 >= want) {
+        s_res[0] = (uint32_t)(tid * 64 + 2 * w + 1);
+        s_res[1] = cum;
+        break;
+      }
+      cum += c1;
     }
   }
   __syncthreads();
 }
 
 static __device__ void select_block_small(const float* J, int K, int K_e, int64_t k_begin, int64_t* elite, uint32_t* hist) {
-  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_w[33];
   __shared__ uint32_t s_res[2];
   const int tid = threadIdx.x;
-  const int per = (K + blockDim.x - 1) / blockDim.x;
+  const int per = (K + kSelBlock - 1) / kSelBlock;
   const int k0 = tid * per;
   const int nk = max(0, min(per, K - k0));
   uint32_t key[kSelKPT];
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i) key[i] = i < nk ? cost_key(J[k0 + i]) : 0xFFFFFFFFu;
-  uint32_t want = (uint32_t)K_e;
-  digit_pass_small(key, nk, 0u, 0u, 21, 2048, want, hist, s_w, s_res);
-  const uint32_t d1 = s_res[0];
-  want -= s_res[1];
-  digit_pass_small(key, nk, 0xFFE00000u, d1 << 21, 10, 2048, want, hist, s_w, s_res);
-  const uint32_t d2 = s_res[0];
-  want -= s_res[1];
-  digit_pass_small(key, nk, 0xFFFFFC00u, (d1 << 21) | (d2 << 10), 0, 1024, want, hist, s_w, s_res);
-  const uint32_t T = (d1 << 21) | (d2 << 10) | s_res[0];
-  const uint32_t n_eq = want - s_res[1];  // ties at T to take, lowest indices first
+  digit16_pass(key, nk, 0u, 0u, 16, (uint32_t)K_e, hist, s_w, s_res);
+  const uint32_t hi = s_res[0], below_hi = s_res[1];
+  digit16_pass(key, nk, 0xFFFF0000u, hi << 16, 0, (uint32_t)K_e - below_hi, hist, s_w, s_res);
+  const uint32_t T = (hi << 16) | s_res[0];
+  const uint32_t n_eq = (uint32_t)K_e - below_hi - s_res[1];  // ties at T to take, lowest indices first
   uint32_t lt = 0, eq = 0;
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i)
@@ -996,8 +1008,8 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
       eq += key[i] == T;
     }
   uint32_t t1, t2;
-  const uint32_t lt_before = block_excl_scan_small(lt, s_w, &t1);
-  uint32_t eq_before = block_excl_scan_small(eq, s_w, &t2);
+  const uint32_t lt_before = block_excl_scan(lt, s_w, &t1);
+  uint32_t eq_before = block_excl_scan(eq, s_w, &t2);
   uint32_t pos = lt_before + min(eq_before, n_eq);
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i)
@@ -1042,7 +1054,7 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_cons
                sel_smem);
 }
 
-__global__ void __launch_bounds__(kSmallBlock) sbs_select_small_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kSelBlock) sbs_select_small_kernel(const __grid_constant__ Params p) {
   extern __shared__ uint32_t sel_smem[];
   const int r = blockIdx.x;
   merge_diag(p, r);
@@ -1056,7 +1068,7 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_raw_kernel(const float* 
   select_block(J, K, K_e, 0, idx, sel_smem);
 }
 
-__global__ void __launch_bounds__(kSmallBlock) sbs_select_small_raw_kernel(const float* J, int64_t K, int64_t K_e,
+__global__ void __launch_bounds__(kSelBlock) sbs_select_small_raw_kernel(const float* J, int64_t K, int64_t K_e,
                                                                            int64_t* idx) {
   extern __shared__ uint32_t sel_smem[];
   select_block_small(J, (int)K, (int)K_e, 0, idx, sel_smem);
@@ -1317,14 +1329,14 @@ static size_t select_smem(int64_t K) {
 
 cudaError_t launch_select(const Params& p, cudaStream_t s) {
   const size_t smem = select_smem(p.K_local);
-  if (p.K_local <= kSelSmallMax) sbs_select_small_kernel<<<p.R, kSmallBlock, smem, s>>>(p);
+  if (p.K_local <= kSelSmallMax) sbs_select_small_kernel<<<p.R, kSelBlock, smem, s>>>(p);
   else sbs_select_kernel<<<p.R, kSelBlock, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s) {
   const size_t smem = select_smem(K);
-  if (K <= kSelSmallMax) sbs_select_small_raw_kernel<<<1, kSmallBlock, smem, s>>>(J, K, K_e, idx);
+  if (K <= kSelSmallMax) sbs_select_small_raw_kernel<<<1, kSelBlock, smem, s>>>(J, K, K_e, idx);
   else sbs_select_raw_kernel<<<1, kSelBlock, smem, s>>>(J, K, K_e, idx);
   return cudaGetLastError();
 }
