@@ -85,10 +85,16 @@ struct sbs_ctx {
   float* d_sdiag = nullptr;
   sbs_input* d_in = nullptr;
   sbs_output* d_out = nullptr;
-  sbs_input* h_in = nullptr;   // pinned
+  // host path staging: one pinned block [iter | R inputs | R x H x 12 reference], one H2D per step
+  char* h_blk = nullptr;
+  char* d_blk = nullptr;
+  size_t blk_in_off = 0, blk_ref_off = 0, blk_bytes = 0;
+  sbs_input* h_in = nullptr;   // = h_blk + blk_in_off
+  float* h_xref = nullptr;     // = h_blk + blk_ref_off
   sbs_output* h_out = nullptr; // pinned
-  float* h_xref = nullptr;     // pinned [R][H][12] staging of sbs_set_reference
-  std::vector<cudaEvent_t> ref_ev;
+  cudaEvent_t blk_ev = nullptr;  // last H2D of h_blk (the host rewrites it only after this completed)
+  bool ref_dirty = false;
+  cudaGraphExec_t graph = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<char> ref_set;
   uint32_t iter = 0;
@@ -320,14 +326,16 @@ void sbs_destroy(sbs_ctx* c) {
   cudaSetDevice(c->cfg.device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
-  for (void* p : {(void*)c->d_mean, (void*)c->d_var, (void*)c->d_fidx, (void*)c->d_xref, (void*)c->d_J,
+  for (void* p : {(void*)c->d_mean, (void*)c->d_var, (void*)c->d_fidx, (void*)c->d_J,
                   (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart, (void*)c->d_sdiag,
-                  (void*)c->d_in, (void*)c->d_out})
+                  (void*)c->d_out})
     if (p) cudaFree(p);
   if (c->h_in) cudaFreeHost(c->h_in);
   if (c->h_out) cudaFreeHost(c->h_out);
-  if (c->h_xref) cudaFreeHost(c->h_xref);
-  for (auto e : c->ref_ev) cudaEventDestroy(e);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->h_blk) cudaFreeHost(c->h_blk);
+  if (c->d_blk) cudaFree(c->d_blk);
+  if (c->blk_ev) cudaEventDestroy(c->blk_ev);
   for (auto& pd : c->pending) {
     cudaEventDestroy(pd.a);
     cudaEventDestroy(pd.b);
@@ -363,6 +371,7 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaSetDevice(cfg->device));
   CKC(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, cfg->device));
   CKC(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CKC(sbs::prepare_kernels(cfg->knots));
   CKC(cudaEventCreate(&c->ev0));
   CKC(cudaEventCreate(&c->ev1));
 
@@ -462,8 +471,19 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaMalloc(&c->d_mean, RD * sizeof(float)));
   CKC(cudaMalloc(&c->d_var, RD * sizeof(float)));
   CKC(cudaMalloc(&c->d_fidx, R * sizeof(int)));
-  CKC(cudaMalloc(&c->d_xref, (size_t)R * H * 12 * sizeof(float)));
-  CKC(cudaMemset(c->d_xref, 0, (size_t)R * H * 12 * sizeof(float)));
+  c->blk_in_off = 16;
+  c->blk_ref_off = c->blk_in_off + (size_t)R * sizeof(sbs_input);
+  c->blk_bytes = c->blk_ref_off + (size_t)R * H * 12 * sizeof(float);
+  CKC(cudaMalloc(&c->d_blk, c->blk_bytes));
+  CKC(cudaMemset(c->d_blk, 0, c->blk_bytes));
+  CKC(cudaMallocHost(&c->h_blk, c->blk_bytes));
+  memset(c->h_blk, 0, c->blk_bytes);
+  c->h_in = reinterpret_cast<sbs_input*>(c->h_blk + c->blk_in_off);
+  c->h_xref = reinterpret_cast<float*>(c->h_blk + c->blk_ref_off);
+  c->d_in = reinterpret_cast<sbs_input*>(c->d_blk + c->blk_in_off);
+  c->d_xref = reinterpret_cast<float*>(c->d_blk + c->blk_ref_off);
+  CKC(cudaEventCreateWithFlags(&c->blk_ev, cudaEventDisableTiming));
+  CKC(cudaEventRecord(c->blk_ev, c->stream));
   CKC(cudaMalloc(&c->d_J, (size_t)R * P.K_local * sizeof(float)));
   CKC(cudaMalloc(&c->d_part, (size_t)R * P.n_cta * P.part_stride * sizeof(float)));
   if (cfg->world > 1)
@@ -476,16 +496,8 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.n_eblk = P.n_elite > 0 ? (int)((P.n_elite + 31) / 32) : 1;  // 32 elites per elite-kernel CTA
   CKC(cudaMalloc(&c->d_epart, (size_t)R * P.n_eblk * sbs::kEPartStride * sizeof(float)));
   CKC(cudaMalloc(&c->d_sdiag, (size_t)R * 8 * sizeof(float)));
-  CKC(cudaMalloc(&c->d_in, R * sizeof(sbs_input)));
   CKC(cudaMalloc(&c->d_out, R * sizeof(sbs_output)));
-  CKC(cudaMallocHost(&c->h_in, R * sizeof(sbs_input)));
   CKC(cudaMallocHost(&c->h_out, R * sizeof(sbs_output)));
-  CKC(cudaMallocHost(&c->h_xref, (size_t)R * H * 12 * sizeof(float)));
-  c->ref_ev.assign(R, nullptr);
-  for (int r = 0; r < R; ++r) {
-    CKC(cudaEventCreateWithFlags(&c->ref_ev[r], cudaEventDisableTiming));
-    CKC(cudaEventRecord(c->ref_ev[r], c->stream));
-  }
   // initial distribution: mean (0, 0, m|g_z|/4) per leg and knot, var = sigma^2, freq_idx 0
   {
     std::vector<float> m(RD), v(RD);
@@ -544,13 +556,11 @@ int sbs_set_reference(sbs_ctx* c, int32_t robot, const float* x_ref) {
   const int n = c->P.H * 12;
   if (!finite_all(x_ref, n)) return fail(c, SBS_ERR_NONFINITE, "reference not finite");
   CK(cudaSetDevice(c->cfg.device));
-  // stage in this robot's pinned slot (the caller's buffer is free on return) and
-  // copy asynchronously; the slot is reused only after its previous copy completed
-  CK(cudaEventSynchronize(c->ref_ev[robot]));
-  float* slot = c->h_xref + (size_t)robot * n;
-  memcpy(slot, x_ref, n * sizeof(float));
-  CK(cudaMemcpyAsync(c->d_xref + (size_t)robot * n, slot, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
-  CK(cudaEventRecord(c->ref_ev[robot], c->stream));
+  // staged in pinned memory (the caller's buffer is free on return); uploaded with
+  // the next step's inputs.  The block is rewritten only after its last upload.
+  CK(cudaEventSynchronize(c->blk_ev));
+  memcpy(c->h_xref + (size_t)robot * n, x_ref, n * sizeof(float));
+  c->ref_dirty = true;
   c->ref_set[robot] = 1;
   return SBS_OK;
 }
@@ -558,8 +568,16 @@ int sbs_set_reference(sbs_ctx* c, int32_t robot, const float* x_ref) {
 int sbs_set_reference_device(sbs_ctx* c, const float* d_x_ref, void* stream) {
   if (!c || !d_x_ref) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
   CK(cudaSetDevice(c->cfg.device));
+  if (c->ref_dirty) {  // host-staged references of earlier calls are superseded
+    CK(cudaEventSynchronize(c->blk_ev));
+    c->ref_dirty = false;
+  }
   CK(cudaMemcpyAsync(c->d_xref, d_x_ref, (size_t)c->P.R * c->P.H * 12 * sizeof(float), cudaMemcpyDeviceToDevice,
                      (cudaStream_t)stream));
+  // keep the pinned copy in sync for later host-path steps
+  CK(cudaMemcpyAsync(c->h_xref, d_x_ref, (size_t)c->P.R * c->P.H * 12 * sizeof(float), cudaMemcpyDeviceToHost,
+                     (cudaStream_t)stream));
+  CK(cudaEventRecord(c->blk_ev, (cudaStream_t)stream));
   std::fill(c->ref_set.begin(), c->ref_set.end(), 1);
   return SBS_OK;
 }
@@ -599,6 +617,23 @@ int sbs_set_iter(sbs_ctx* c, uint32_t iter) {
   return SBS_OK;
 }
 
+namespace {
+// one host-path iteration on c->stream: upload [iter | inputs | reference] in one
+// copy, the kernels, the outputs back (captured once into a CUDA graph when possible)
+int enqueue_host_step(sbs_ctx* c, cudaStream_t s) {
+  CK(cudaMemcpyAsync(c->d_blk, c->h_blk, c->blk_bytes, cudaMemcpyHostToDevice, s));
+  Params saved = c->P;
+  c->P.in = c->d_in;
+  c->P.out = c->d_out;
+  c->P.iter_dev = reinterpret_cast<const uint32_t*>(c->d_blk);
+  int rc = enqueue_step(c, s);
+  c->P = saved;
+  if (rc != SBS_OK) return rc;
+  CK(cudaMemcpyAsync(c->h_out, c->d_out, c->P.R * sizeof(sbs_output), cudaMemcpyDeviceToHost, s));
+  return SBS_OK;
+}
+}  // namespace
+
 int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
   if (!c || !in || !out) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
   const int R = c->P.R;
@@ -608,17 +643,37 @@ int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
       return fail(c, SBS_ERR_NONFINITE, "non-finite x0 / feet");
     if (!(fabsf(in[r].x0[7]) < 1.5697963267948966f)) return fail(c, SBS_ERR_SINGULAR, "|pitch(x0)| >= pi/2 - 1e-3");
   }
+  if (c->external) return fail(c, SBS_ERR_STATE, "external exchange: use sbs_step_records / sbs_finish_records");
   CK(cudaSetDevice(c->cfg.device));
-  memcpy(c->h_in, in, R * sizeof(sbs_input));
   cudaStream_t s = c->stream;
-  CK(cudaMemcpyAsync(c->d_in, c->h_in, R * sizeof(sbs_input), cudaMemcpyHostToDevice, s));
-  c->P.in = c->d_in;
-  c->P.out = c->d_out;
-  CK(cudaEventRecord(c->ev0, s));
-  int rc = enqueue_step(c, s);
-  if (rc != SBS_OK) return rc;
+  CK(cudaEventSynchronize(c->blk_ev));
+  memcpy(c->h_blk, &c->iter, sizeof(uint32_t));
+  memcpy(c->h_in, in, R * sizeof(sbs_input));
+  c->ref_dirty = false;  // the whole block (with the reference) goes up with this step
+  const bool use_graph = !c->profile && c->cfg.world == 1;
+  CK(cudaEventRecord(c->ev0, s));  // events stay outside the graph (host-synchronisable)
+  if (use_graph) {
+    if (!c->graph) {
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      const int rc = enqueue_host_step(c, s);
+      const cudaError_t e = cudaStreamEndCapture(s, &g);  // always leave capture mode
+      if (rc != SBS_OK) {
+        if (e == cudaSuccess) cudaGraphDestroy(g);
+        return rc;
+      }
+      CK(e);
+      const cudaError_t ei = cudaGraphInstantiate(&c->graph, g, 0);
+      cudaGraphDestroy(g);
+      CK(ei);
+    }
+    CK(cudaGraphLaunch(c->graph, s));
+  } else {
+    const int rc = enqueue_host_step(c, s);
+    if (rc != SBS_OK) return rc;
+  }
   CK(cudaEventRecord(c->ev1, s));
-  CK(cudaMemcpyAsync(c->h_out, c->d_out, R * sizeof(sbs_output), cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(c->blk_ev, s));
   CK(cudaStreamSynchronize(s));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, c->ev0, c->ev1);
@@ -637,6 +692,12 @@ int sbs_step_device(sbs_ctx* c, const sbs_input* d_in, sbs_output* d_out, void* 
   for (int r = 0; r < c->P.R; ++r)
     if (!c->ref_set[r]) return fail(c, SBS_ERR_STATE, "reference not set for every robot");
   CK(cudaSetDevice(c->cfg.device));
+  if (c->ref_dirty) {  // references staged by sbs_set_reference go up first, in stream order
+    CK(cudaMemcpyAsync(c->d_xref, c->h_xref, (size_t)c->P.R * c->P.H * 12 * sizeof(float),
+                       cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    CK(cudaEventRecord(c->blk_ev, (cudaStream_t)stream));
+    c->ref_dirty = false;
+  }
   c->P.in = d_in;
   c->P.out = d_out;
   int rc = enqueue_step(c, (cudaStream_t)stream);
@@ -653,6 +714,12 @@ int sbs_step_records(sbs_ctx* c, const sbs_input* d_in, float* d_rec, void* stre
   for (int r = 0; r < c->P.R; ++r)
     if (!c->ref_set[r]) return fail(c, SBS_ERR_STATE, "reference not set for every robot");
   CK(cudaSetDevice(c->cfg.device));
+  if (c->ref_dirty) {
+    CK(cudaMemcpyAsync(c->d_xref, c->h_xref, (size_t)c->P.R * c->P.H * 12 * sizeof(float),
+                       cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    CK(cudaEventRecord(c->blk_ev, (cudaStream_t)stream));
+    c->ref_dirty = false;
+  }
   c->P.in = d_in;
   return enqueue_records(c, (cudaStream_t)stream, d_rec);
 }
@@ -764,6 +831,7 @@ int sbs_debug_select(const float* J, int64_t K, int64_t K_e, int64_t* idx, int32
   if (!J || !idx || K < 1 || K_e < 1 || K_e > K || K > 0x7fffffffLL)
     return fail(nullptr, SBS_ERR_INVALID_ARG, "bad argument");
   CK(cudaSetDevice(device));
+  CK(sbs::prepare_kernels(0));
   float* dJ;
   int64_t* di;
   CK(cudaMalloc(&dJ, K * sizeof(float)));

@@ -48,6 +48,7 @@ struct Params {
   uint32_t seed_lo, seed_hi;
   uint32_t rk[10][2];         // Philox round keys (seed_lo + r 0x9E3779B9, seed_hi + r 0xBB67AE85)
   uint32_t iter;
+  const uint32_t* iter_dev;   // non-null: read the iteration counter from device memory (graph replay)
   int robot_offset;
   // --- sizes / sharding ---
   int R;
@@ -85,6 +86,8 @@ cudaError_t launch_elite(const Params& p, cudaStream_t s);
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                  int* fidx, cudaStream_t s);
 cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s);
-int rollout_occupancy(int P, int mode);  // resident CTAs per SM of the rollout kernel
+int rollout_occupancy(int P, int mode);
+// kernel attributes (dynamic shared memory limits), once per process and P, never inside a capture
+cudaError_t prepare_kernels(int P);  // resident CTAs per SM of the rollout kernel
 
 }  // namespace sbs

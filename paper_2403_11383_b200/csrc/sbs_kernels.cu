@@ -35,8 +35,13 @@ struct RobotSmem {
   float xref[SBS_MAX_HORIZON * 12];  // per step, kernel order (px,py, vx,vy, pz,vz, roll,pitch, yaw,wx, wy,wz)
   uint8_t ctab[SBS_MAX_FREQ][SBS_MAX_HORIZON];  // bits 0-3: stance of leg i at step j; bits 4-7: leg i touched down
   uint32_t phase0;
+  uint32_t iter;  // iteration counter of this step (noise counter word 2)
   int cur_idx;
 };
+
+// iteration counter: kernel parameter, or device memory when the step runs as a
+// captured CUDA graph (the host writes it with the inputs every step)
+__device__ __forceinline__ uint32_t step_iter(const Params& p) { return p.iter_dev ? *p.iter_dev : p.iter; }
 
 // state-vector index in the kernel's pair order for each index of x = (p, v, Phi, w)
 __device__ __forceinline__ int xref_slot(int a) { return a == 2 ? 4 : (a == 3 ? 2 : (a == 4 ? 3 : a)); }
@@ -60,7 +65,10 @@ static __device__ void load_robot(const Params& p, int r, RobotSmem& s, bool rol
     s.sig[d] = __fsqrt_rn(var[d]);
   }
   const sbs_input* in = p.in + r;
-  if (threadIdx.x == 0) s.cur_idx = p.fidx[r];
+  if (threadIdx.x == 0) {
+    s.cur_idx = p.fidx[r];
+    s.iter = step_iter(p);
+  }
   if (!rollout_inputs) return;  // sampling only (elite regeneration, debug draws)
   for (int a = threadIdx.x; a < 12; a += blockDim.x) {
     s.x0[a] = in->x0[a];
@@ -126,7 +134,7 @@ __device__ __forceinline__ int draw_sample(const Params& p, uint32_t robot_g, in
   const uint32_t kk = (uint32_t)k;
 #pragma unroll
   for (int q = 0; q < D / 4; ++q) {
-    const U4 w = philox4x32_10_rk((uint32_t)q, kk, p.iter, robot_g, p.rk);
+    const U4 w = philox4x32_10_rk((uint32_t)q, kk, s.iter, robot_g, p.rk);
     float z[4];
     box_muller(w.x, w.y, z[0], z[1]);
     box_muller(w.z, w.w, z[2], z[3]);
@@ -138,7 +146,7 @@ __device__ __forceinline__ int draw_sample(const Params& p, uint32_t robot_g, in
   }
   int idx = s.cur_idx;
   if (p.gait_adapt) {
-    const U4 w = philox4x32_10_rk(0x80000000u, kk, p.iter, robot_g, p.rk);
+    const U4 w = philox4x32_10_rk(0x80000000u, kk, s.iter, robot_g, p.rk);
     idx = (int)__umulhi(w.x, (uint32_t)p.n_freq);  // (w * n) >> 32
   }
   return idx;
@@ -153,7 +161,7 @@ __device__ __forceinline__ void sample_block(const Params& p, uint32_t robot_g, 
     for (int i = 0; i < 4; ++i) th4[i] = s.mu[4 * q + i];
     return;
   }
-  const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k, p.iter, robot_g, p.rk);
+  const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k, s.iter, robot_g, p.rk);
   float z[4];
   box_muller(w.x, w.y, z[0], z[1]);
   box_muller(w.z, w.w, z[2], z[3]);
@@ -402,7 +410,7 @@ static __device__ void write_output(const Params& p, int r, int status, const fl
     o->freq_idx = fi;
     o->freq_hz = p.freq_hz[fi];
     o->status = status;
-    o->iter = p.iter;
+    o->iter = step_iter(p);
     o->j_min = jmin;
     o->j_mean = jmean;
     o->omega = omega;
@@ -1215,6 +1223,7 @@ struct PEntry {
   static cudaError_t elite(const Params& p, cudaStream_t s);
   static cudaError_t debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                    int* fidx, cudaStream_t s);
+  static cudaError_t prepare();  // function attributes, set once outside any stream capture
 };
 
 #if defined(SBS_TU_P)
@@ -1222,11 +1231,6 @@ template <int P, int EPI, bool FUSED>
 static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
   constexpr int D = 12 * P;
   const size_t smem = EPI == EPI_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
-  }
   dim3 grid(p.n_cta, p.R);
   sbs_rollout_kernel<P, EPI, FUSED><<<grid, kBlock, smem, s>>>(p);
   return cudaGetLastError();
@@ -1264,6 +1268,19 @@ cudaError_t PEntry<P>::debug_samples(const Params& p, int robot, int64_t k0, int
   const int blocks = (int)((n + 127) / 128);
   sbs_debug_samples_kernel<P><<<blocks, 128, 0, s>>>(p, robot, k0, n, z, theta, fidx);
   return cudaGetLastError();
+}
+
+template <int P>
+cudaError_t PEntry<P>::prepare() {
+  const int big = 96 * 1024;
+  cudaError_t e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  return e;
 }
 
 template struct PEntry<SBS_TU_P>;
@@ -1314,17 +1331,22 @@ cudaError_t launch_mppi_merge(const Params& p, float* dst, cudaStream_t s) {
 }
 
 static size_t select_smem(int64_t K) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sbs_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
-    cudaFuncSetAttribute(sbs_select_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
-    cudaFuncSetAttribute(sbs_select_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmallSmemBytes);
-    cudaFuncSetAttribute(sbs_select_small_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSelSmallSmemBytes);
-    attr = true;
-  }
   if (K <= kSelSmallMax) return (size_t)kSelSmallSmemBytes;
   return (size_t)(kSelHistWords + (K <= kSelSmemKeys ? K : 0)) * 4;
+}
+
+cudaError_t prepare_kernels(int P) {
+  cudaError_t e = cudaFuncSetAttribute(sbs_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_select_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_select_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmallSmemBytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_select_small_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSelSmallSmemBytes);
+  if (e != cudaSuccess || P == 0) return e;
+  SBS_DISPATCH_P(P, prepare());
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_select(const Params& p, cudaStream_t s) {
