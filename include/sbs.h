@@ -110,7 +110,8 @@ typedef struct sbs_config {
   int32_t device;         /* CUDA device ordinal */
   int32_t rank, world;    /* sample sharding: rank handles a contiguous slice of the K samples */
   uint8_t nccl_id[128];   /* ncclUniqueId (sbs_nccl_unique_id on rank 0) when world > 1; all zero:
-                             the caller exchanges the MPPI records (sbs_step_records) */
+                             the caller exchanges the rank records (sbs_step_records).  CEM with
+                             world > 1 needs n_elite <= n_samples / world. */
 } sbs_config;
 
 /* Per-robot input of one iteration (host for sbs_step, device for sbs_step_device). */
@@ -176,14 +177,24 @@ int sbs_step(sbs_ctx* ctx, const sbs_input* in, sbs_output* out);
  * iter += 1 when the call returns SBS_OK. */
 int sbs_step_device(sbs_ctx* ctx, const sbs_input* d_in, sbs_output* d_out, void* stream);
 
-/* Sample-sharded MPPI with a caller-driven exchange (world > 1 and an all-zero
- * nccl_id): the same iteration as sbs_step_device, split at its one exchange
- * point.  sbs_step_records enqueues this rank's rollouts and writes its merged
- * record per robot to d_rec (device, R x sbs_record_floats(ctx) floats: beta_g,
- * argmin, sum w, sum w^2, sum w theta relative to beta_g, ...).  The caller
- * gathers every rank's records in rank order ([world][R][record]) and passes
- * them to sbs_finish_records, which merges them in rank order and finishes the
- * iteration (new distribution, d_out); iter += 1.  Both stream-ordered. */
+/* Sample sharding with a caller-driven exchange (world > 1 and an
+ * all-zero nccl_id): the same iteration as sbs_step_device, split at its one
+ * exchange point.  sbs_step_records enqueues this rank's rollouts and writes
+ * its record per robot to d_rec (device, R x sbs_record_floats(ctx) floats):
+ *   MPPI  [beta_g, k_argmin, theta1, sum w, sum w^2, sum J, n finite, 0 | sum w theta[D]]
+ *         (weights relative to this rank's beta_g)
+ *   Naive [J_min, k_argmin, theta1, 0, 0, sum J, n finite, 0]
+ *   CEM   [same 8-float header | J of the rank's K_e smallest (J, k), index order |
+ *          their global k as int32 bits], padded to a multiple of 4 floats
+ * The caller gathers every rank's records in rank order ([world][R][record])
+ * and passes them to sbs_finish_records, which merges them in rank order
+ * (MPPI: rescaled sums; Naive: argmin; CEM: exact K_e-smallest selection over
+ * the world x K_e candidates, whose rank-order concatenation is in global
+ * index order, then elite moments regenerated from the counter RNG) and
+ * finishes the iteration (new distribution, d_out); iter += 1.  Both
+ * stream-ordered.  With a nonzero nccl_id, sbs_step / sbs_step_device do the
+ * same with one ncclAllGather in between.  Noise, costs, elites and (MPPI
+ * aside, whose sums regroup) the new distribution are independent of world. */
 int sbs_record_floats(const sbs_ctx* ctx);
 int sbs_step_records(sbs_ctx* ctx, const sbs_input* d_in, float* d_rec, void* stream);
 int sbs_finish_records(sbs_ctx* ctx, const float* d_recs, const sbs_input* d_in, sbs_output* d_out, void* stream);

@@ -76,7 +76,9 @@ struct sbs_ctx {
   float* d_xref = nullptr;
   float* d_J = nullptr;
   float* d_part = nullptr;
-  float* d_gather = nullptr;  // [world][R][part_stride] (world > 1)
+  float* d_gather = nullptr;  // [world][R][ex_stride] (world > 1)
+  float* d_eJ = nullptr;      // [R][K_e] elite costs
+  float* d_cand = nullptr;    // [R][world][K_e] CEM world > 1 candidates
   int64_t* d_elite = nullptr;
   int64_t* d_best = nullptr;
   int* d_status = nullptr;
@@ -208,8 +210,9 @@ int validate(const sbs_config* c, std::string& why) {
   if (c->n_robots < 1) return bad("n_robots must be >= 1");
   if (c->robot_offset < 0) return bad("robot_offset must be >= 0");
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad("bad rank / world");
-  if (c->world > 1 && c->mode != SBS_MPPI) return bad("sample sharding (world > 1) is implemented for MPPI only");
   if (c->world > 1 && c->n_samples < c->world) return bad("n_samples < world");
+  if (c->world > 1 && c->mode == SBS_CEM && c->n_samples / c->world < c->n_elite)
+    return bad("CEM with world > 1 needs n_elite <= n_samples / world (every rank offers K_e candidates)");
   return SBS_OK;
 }
 
@@ -241,24 +244,37 @@ cudaError_t timed(sbs_ctx* c, int kernel, cudaStream_t s, F&& launch) {
   return e;
 }
 
-// enqueue one iteration on stream s with inputs c->P.in and outputs c->P.out
-// sample-sharded MPPI, part 1: rollouts of this rank's slice + its merged record per robot
+// sample sharding (world > 1), part 1: rollouts of this rank's slice and its
+// record per robot at dst[R][ex_stride]:
+//   MPPI  [beta_g, k, f, S, S2, sum J, n finite, 0 | V[D]]   (weights relative to beta_g)
+//   Naive [J_min, k, f, 0, 0, sum J, n finite, 0]
+//   CEM   [J_min, k, f, 0, 0, sum J, n finite, 0 | J[K_e] | k[K_e]]  (local K_e smallest, index order)
 int enqueue_records(sbs_ctx* c, cudaStream_t s, float* dst) {
   Params& P = c->P;
   P.iter = c->iter;
-  CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, SBS_MPPI, false, s); }));
-  CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_merge(P, dst, s); }));
+  const int mode = c->cfg.mode;
+  CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, mode, false, s); }));
+  if (mode == SBS_MPPI) CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_merge(P, dst, s); }));
+  else if (mode == SBS_NAIVE) CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_argmin_emit(P, dst, s); }));
+  else CK(timed(c, SBS_KERNEL_SELECT, s, [&] { return sbs::launch_select_emit(P, dst, s); }));
   return SBS_OK;
 }
 
-// part 2: merge the `world` ranks' records ([world][R][8 + D], rank order) and finish
+// part 2: merge the `world` ranks' records ([world][R][ex_stride], rank order) and finish
 int enqueue_finish(sbs_ctx* c, cudaStream_t s, const float* recs) {
   Params F = c->P;
   F.iter = c->iter;
   F.part = const_cast<float*>(recs);
   F.n_cta = c->cfg.world;
   F.part_c_stride = F.R;
-  CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_finalize(F, s); }));
+  F.part_stride = F.ex_stride;
+  const int mode = c->cfg.mode;
+  if (mode == SBS_MPPI) CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_finalize(F, s); }));
+  else if (mode == SBS_NAIVE) CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_naive_finalize(F, s); }));
+  else {
+    CK(timed(c, SBS_KERNEL_SELECT, s, [&] { return sbs::launch_select_merge(F, s); }));
+    CK(timed(c, SBS_KERNEL_ELITE, s, [&] { return sbs::launch_elite(F, s); }));
+  }
   return SBS_OK;
 }
 
@@ -267,9 +283,9 @@ int enqueue_step(sbs_ctx* c, cudaStream_t s) {
   Params& P = c->P;
   P.iter = c->iter;
   const int mode = c->cfg.mode;
-  if (c->cfg.world > 1) {  // MPPI: rank record -> all-gather -> merge in rank order
+  if (c->cfg.world > 1) {  // rank record -> all-gather -> merge in rank order
     if (c->external) return fail(c, SBS_ERR_STATE, "external exchange: use sbs_step_records / sbs_finish_records");
-    const size_t n = (size_t)P.R * P.part_stride;
+    const size_t n = (size_t)P.R * P.ex_stride;
     float* mine = c->d_gather + (size_t)c->cfg.rank * n;
     int rc = enqueue_records(c, s, mine);
     if (rc != SBS_OK) return rc;
@@ -327,7 +343,7 @@ void sbs_destroy(sbs_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
   for (void* p : {(void*)c->d_mean, (void*)c->d_var, (void*)c->d_fidx, (void*)c->d_J,
-                  (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart, (void*)c->d_sdiag,
+                  (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart, (void*)c->d_sdiag, (void*)c->d_eJ, (void*)c->d_cand,
                   (void*)c->d_out})
     if (p) cudaFree(p);
   if (c->h_in) cudaFreeHost(c->h_in);
@@ -466,6 +482,10 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   }
   P.part_c_stride = 1;
   P.part_stride = sbs::kPartHdr + D;
+  // rank record of the world > 1 exchange (16-byte multiple)
+  if (cfg->mode == SBS_MPPI) P.ex_stride = P.part_stride;
+  else if (cfg->mode == SBS_NAIVE) P.ex_stride = sbs::kPartHdr;
+  else P.ex_stride = (int)((sbs::kPartHdr + 2 * cfg->n_elite + 3) / 4 * 4);
   // ---- device buffers ----
   const size_t RD = (size_t)R * D;
   CKC(cudaMalloc(&c->d_mean, RD * sizeof(float)));
@@ -487,8 +507,13 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaMalloc(&c->d_J, (size_t)R * P.K_local * sizeof(float)));
   CKC(cudaMalloc(&c->d_part, (size_t)R * P.n_cta * P.part_stride * sizeof(float)));
   if (cfg->world > 1)
-    CKC(cudaMalloc(&c->d_gather, (size_t)cfg->world * R * P.part_stride * sizeof(float)));
-  if (P.n_elite > 0) CKC(cudaMalloc(&c->d_elite, (size_t)R * P.n_elite * sizeof(int64_t)));
+    CKC(cudaMalloc(&c->d_gather, (size_t)cfg->world * R * P.ex_stride * sizeof(float)));
+  if (P.n_elite > 0) {
+    CKC(cudaMalloc(&c->d_elite, (size_t)R * P.n_elite * sizeof(int64_t)));
+    CKC(cudaMalloc(&c->d_eJ, (size_t)R * P.n_elite * sizeof(float)));
+  }
+  if (cfg->mode == SBS_CEM && cfg->world > 1)
+    CKC(cudaMalloc(&c->d_cand, (size_t)R * cfg->world * P.n_elite * sizeof(float)));
   CKC(cudaMalloc(&c->d_best, R * sizeof(int64_t)));
   CKC(cudaMalloc(&c->d_status, R * sizeof(int)));
   CKC(cudaMalloc(&c->d_counter, 2 * R * sizeof(int)));
@@ -524,6 +549,8 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.ecounter = c->d_counter + R;
   P.epart = c->d_epart;
   P.sdiag = c->d_sdiag;
+  P.elite_J = c->d_eJ;
+  P.cand = c->d_cand;
   c->ref_set.assign(R, 0);
   // ---- NCCL (sample sharding) ----
   if (cfg->world > 1) {
@@ -706,11 +733,11 @@ int sbs_step_device(sbs_ctx* c, const sbs_input* d_in, sbs_output* d_out, void* 
   return SBS_OK;
 }
 
-int sbs_record_floats(const sbs_ctx* c) { return c ? c->P.part_stride : 0; }
+int sbs_record_floats(const sbs_ctx* c) { return c ? c->P.ex_stride : 0; }
 
 int sbs_step_records(sbs_ctx* c, const sbs_input* d_in, float* d_rec, void* stream) {
   if (!c || !d_in || !d_rec) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
-  if (c->cfg.mode != SBS_MPPI) return fail(c, SBS_ERR_STATE, "records exchange is MPPI only");
+  if (c->cfg.world < 2) return fail(c, SBS_ERR_STATE, "records exchange needs world > 1");
   for (int r = 0; r < c->P.R; ++r)
     if (!c->ref_set[r]) return fail(c, SBS_ERR_STATE, "reference not set for every robot");
   CK(cudaSetDevice(c->cfg.device));
@@ -726,7 +753,7 @@ int sbs_step_records(sbs_ctx* c, const sbs_input* d_in, float* d_rec, void* stre
 
 int sbs_finish_records(sbs_ctx* c, const float* d_recs, const sbs_input* d_in, sbs_output* d_out, void* stream) {
   if (!c || !d_recs || !d_in || !d_out) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
-  if (c->cfg.mode != SBS_MPPI) return fail(c, SBS_ERR_STATE, "records exchange is MPPI only");
+  if (c->cfg.world < 2) return fail(c, SBS_ERR_STATE, "records exchange needs world > 1");
   CK(cudaSetDevice(c->cfg.device));
   c->P.in = d_in;
   c->P.out = d_out;
@@ -883,8 +910,8 @@ int sbs_kernel_times(sbs_ctx* c, double* total_ms, int64_t* launches) {
 
 int sbs_launches_per_step(const sbs_ctx* c) {
   if (!c) return 0;
-  if (c->cfg.mode == SBS_MPPI) return c->cfg.world > 1 ? 2 : 1;
-  return c->cfg.mode == SBS_NAIVE ? 1 : 3;
+  if (c->cfg.world > 1) return c->cfg.mode == SBS_CEM ? 4 : 2;  // + one ncclAllGather
+  return c->cfg.mode == SBS_CEM ? 3 : 1;
 }
 
 }  // extern "C"

@@ -73,15 +73,24 @@ struct Params {
   float* epart;               // [R][n_eblk][kEPartStride] CEM elite-moment records
   int n_eblk;                 // elite blocks per robot
   float* sdiag;               // [R][8] CEM: J_min, k_best, theta1_best, sum J, n finite (select kernel)
+  float* elite_J;             // [R][n_elite] costs of the elites (select kernel)
+  float* cand;                // [R][world * n_elite] CEM world > 1: gathered candidate costs
+  int ex_stride;              // floats per robot in a rank record (world > 1 exchange)
 };
 
 // launchers (sbs_kernels.cu); return cudaGetLastError()
-// mode: SBS_MPPI (fused: merge + finish in the last CTA), SBS_NAIVE (always fused), SBS_CEM (records only)
+// mode: SBS_MPPI / SBS_NAIVE (fused: merge + finish in the last CTA; else records only), SBS_CEM (records only)
 cudaError_t launch_rollout(const Params& p, int mode, bool fused, cudaStream_t s);
 cudaError_t launch_mppi_finalize(const Params& p, cudaStream_t s);
 // merge this rank's CTA partials into one record per robot at dst[R][part_stride]
 cudaError_t launch_mppi_merge(const Params& p, float* dst, cudaStream_t s);
 cudaError_t launch_select(const Params& p, cudaStream_t s);
+// world > 1 CEM: rank record [8 | K_e J | K_e k] per robot at emit[R][ex_stride]; merge of the gathered records
+cudaError_t launch_select_emit(const Params& p, float* emit, cudaStream_t s);
+cudaError_t launch_select_merge(const Params& p, cudaStream_t s);
+// world > 1 Naive: rank argmin record per robot at emit[R][ex_stride]; merge of the gathered records + finish
+cudaError_t launch_argmin_emit(const Params& p, float* emit, cudaStream_t s);
+cudaError_t launch_naive_finalize(const Params& p, cudaStream_t s);
 cudaError_t launch_elite(const Params& p, cudaStream_t s);
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                  int* fidx, cudaStream_t s);

@@ -802,7 +802,7 @@ constexpr int kSelSmemKeys = kSelSmemBytes / 4 - kSelHistWords;
 
 // smem: [kSelHistWords] per-warp histograms, then the keys when K <= kSelSmemKeys
 static __device__ void select_block(const float* J, int64_t K, int64_t K_e, int64_t k_begin, int64_t* elite,
-                             uint32_t* smem) {
+                             float* eJ, uint32_t* smem) {
   __shared__ uint32_t s_prefix, s_want;
   __shared__ uint32_t s_wsum[kSelBlock / 32];
   uint32_t* whist = smem;
@@ -903,7 +903,11 @@ static __device__ void select_block(const float* J, int64_t K, int64_t K_e, int6
     const uint32_t eq_sel_chunk0 = eq_base < n_eq ? eq_base : n_eq;
     const uint32_t eq_sel_before_me = (eq_before < n_eq ? eq_before : n_eq) - eq_sel_chunk0;
     const bool sel = lt || (eq && eq_before < n_eq);
-    if (sel) elite[sel_base + lt_before + eq_sel_before_me] = k_begin + k;
+    if (sel) {
+      const uint32_t pos = sel_base + lt_before + eq_sel_before_me;
+      elite[pos] = k_begin + k;
+      if (eJ) eJ[pos] = J[k];
+    }
     const uint32_t eq_end = eq_base + eq_tot;
     sel_base += lt_tot + ((eq_end < n_eq ? eq_end : n_eq) - eq_sel_chunk0);
     eq_base = eq_end;
@@ -993,7 +997,8 @@ static __device__ void digit16_pass(const uint32_t (&key)[kSelKPT], int nk, uint
   __syncthreads();
 }
 
-static __device__ void select_block_small(const float* J, int K, int K_e, int64_t k_begin, int64_t* elite, uint32_t* hist) {
+static __device__ void select_block_small(const float* J, int K, int K_e, int64_t k_begin, int64_t* elite, float* eJ,
+                                          uint32_t* hist) {
   __shared__ uint32_t s_w[33];
   __shared__ uint32_t s_res[2];
   const int tid = threadIdx.x;
@@ -1023,12 +1028,17 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
   for (int i = 0; i < kSelKPT; ++i)
     if (i < nk) {
       const bool take = key[i] < T || (key[i] == T && eq_before++ < n_eq);
-      if (take) elite[pos++] = k_begin + k0 + i;
+      if (take) {
+        if (eJ) eJ[pos] = J[k0 + i];
+        elite[pos++] = k_begin + k0 + i;
+      }
     }
 }
 
-// also merges robot r's rollout records into p.sdiag[r] = (J_min, k_best, theta1_best, sum J, n finite)
-static __device__ void merge_diag(const Params& p, int r) {
+// merges robot r's records (the rollout's CTA records, or the gathered rank
+// records) into d: sdiag layout (J_min, k_best, theta1_best, sum J, n finite),
+// or, with part_layout, a rank record header [m, k, f, 0, 0, sum J, n finite, 0]
+static __device__ void merge_diag(const Params& p, int r, float* d, bool part_layout) {
   const Best b = merge_argmin(p, r);
   if (threadIdx.x < 32) {
     float sj = 0.f, nf = 0.f;
@@ -1043,43 +1053,87 @@ static __device__ void merge_diag(const Params& p, int r) {
       nf += __shfl_xor_sync(0xffffffffu, nf, o);
     }
     if (threadIdx.x == 0) {
-      float* d = p.sdiag + (size_t)r * 8;
       d[0] = b.m;
       d[1] = __int_as_float(b.k);
       d[2] = __int_as_float(b.f);
-      d[3] = sj;
-      d[4] = nf;
+      if (part_layout) {
+        d[3] = 0.f;
+        d[4] = 0.f;
+        d[5] = sj;
+        d[6] = nf;
+        d[7] = 0.f;
+      } else {
+        d[3] = sj;
+        d[4] = nf;
+      }
     }
   }
 }
 
+// Select kernels, one CTA per robot.
+//   SEL_LOCAL (world = 1): rollout records -> p.sdiag; K_e smallest of J -> p.elite, p.elite_J.
+//   SEL_EMIT  (world > 1, before the all-gather): this rank's record [8 header | K_e J | K_e k]
+//             (the local K_e smallest, index order) -> emit[r].
+//   SEL_MERGE (after the all-gather; p.part = [world][R] gathered records): rank-order
+//             header merge -> p.sdiag; the K_e smallest of the world*K_e candidates,
+//             concatenated in rank order (= global index order, so position order is
+//             the (J, k) tie order) -> p.elite (global k, index order), p.elite_J.
+enum { SEL_LOCAL = 0, SEL_EMIT = 1, SEL_MERGE = 2 };
+
 #if defined(SBS_TU_COMMON)
-__global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_constant__ Params p) {
+template <int MODE, bool SMALL>
+__global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_constant__ Params p, float* emit) {
   extern __shared__ uint32_t sel_smem[];
-  const int r = blockIdx.x;
-  merge_diag(p, r);
-  select_block(p.J + (size_t)r * p.K_local, p.K_local, p.n_elite, p.k_begin, p.elite + (size_t)r * p.n_elite,
-               sel_smem);
+  const int r = blockIdx.x, tid = threadIdx.x;
+  const int64_t Ke = p.n_elite;
+  float* hdr = MODE == SEL_EMIT ? emit + (size_t)r * p.ex_stride : p.sdiag + (size_t)r * 8;
+  merge_diag(p, r, hdr, MODE == SEL_EMIT);
+  const float* J = p.J + (size_t)r * p.K_local;
+  int64_t K = p.K_local, kb = p.k_begin;
+  if (MODE == SEL_MERGE) {
+    float* cand = p.cand + (size_t)r * p.n_cta * Ke;
+    for (int64_t i = tid; i < (int64_t)p.n_cta * Ke; i += blockDim.x)
+      cand[i] = __ldcg(part_rec(p, r, (int)(i / Ke)) + kPartHdr + i % Ke);
+    __syncthreads();
+    J = cand;
+    K = (int64_t)p.n_cta * Ke;
+    kb = 0;
+  }
+  int64_t* el = p.elite + (size_t)r * Ke;
+  float* eJ = p.elite_J + (size_t)r * Ke;
+  if (SMALL) select_block_small(J, (int)K, (int)Ke, kb, el, eJ, sel_smem);
+  else select_block(J, K, Ke, kb, el, eJ, sel_smem);
+  __syncthreads();
+  if (MODE == SEL_EMIT) {
+    float* o = emit + (size_t)r * p.ex_stride + kPartHdr;
+    for (int64_t e = tid; e < Ke; e += blockDim.x) {
+      o[e] = eJ[e];
+      o[Ke + e] = __int_as_float((int)el[e]);
+    }
+  }
+  if (MODE == SEL_MERGE) {
+    for (int64_t e = tid; e < Ke; e += blockDim.x) {
+      const int64_t pos = el[e];
+      el[e] = (int64_t)__float_as_int(__ldcg(part_rec(p, r, (int)(pos / Ke)) + kPartHdr + Ke + pos % Ke));
+    }
+  }
 }
 
-__global__ void __launch_bounds__(kSelBlock) sbs_select_small_kernel(const __grid_constant__ Params p) {
-  extern __shared__ uint32_t sel_smem[];
-  const int r = blockIdx.x;
-  merge_diag(p, r);
-  select_block_small(p.J + (size_t)r * p.K_local, (int)p.K_local, (int)p.n_elite, p.k_begin,
-                     p.elite + (size_t)r * p.n_elite, sel_smem);
+// Naive with world > 1, before the all-gather: this rank's argmin record per robot
+__global__ void __launch_bounds__(128) sbs_argmin_emit_kernel(const __grid_constant__ Params p, float* emit) {
+  merge_diag(p, blockIdx.x, emit + (size_t)blockIdx.x * p.ex_stride, true);
 }
 
 __global__ void __launch_bounds__(kSelBlock) sbs_select_raw_kernel(const float* J, int64_t K, int64_t K_e,
                                                                    int64_t* idx) {
   extern __shared__ uint32_t sel_smem[];
-  select_block(J, K, K_e, 0, idx, sel_smem);
+  select_block(J, K, K_e, 0, idx, nullptr, sel_smem);
 }
 
 __global__ void __launch_bounds__(kSelBlock) sbs_select_small_raw_kernel(const float* J, int64_t K, int64_t K_e,
                                                                            int64_t* idx) {
   extern __shared__ uint32_t sel_smem[];
-  select_block_small(J, (int)K, (int)K_e, 0, idx, sel_smem);
+  select_block_small(J, (int)K, (int)K_e, 0, idx, nullptr, sel_smem);
 }
 
 #endif  // SBS_TU_COMMON
@@ -1107,12 +1161,11 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   __syncthreads();
   const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
   const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
-  const float* Jr = p.J + (size_t)r * p.K_local;
   float dev[4] = {0.f, 0.f, 0.f, 0.f};
   float n = 0.f;
   if (e < p.n_elite) {
     const int64_t k = p.elite[(size_t)r * p.n_elite + e];
-    if (Jr[k - p.k_begin] < kInf) {  // diverged samples never enter the moments (L17)
+    if (p.elite_J[(size_t)r * p.n_elite + e] < kInf) {  // diverged samples never enter the moments (L17)
       float th4[4];
       sample_block(p, robot_g, k, q, s, th4);
 #pragma unroll
@@ -1188,6 +1241,15 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
                s_diag[1] > 0.f ? s_diag[0] / s_diag[1] : kInf, ne, ne, (int)((float)p.K_global - s_diag[1]));
 }
 
+// Naive with world > 1, after the all-gather (p.part = [world][R] rank records)
+template <int P>
+__global__ void __launch_bounds__(128) sbs_naive_finalize_kernel(const __grid_constant__ Params p) {
+  __shared__ RobotSmem s;
+  load_robot(p, blockIdx.x, s, false);
+  __syncthreads();
+  naive_finalize_block<P>(p, blockIdx.x, s);
+}
+
 // ---------------------------------------------------------------------------
 // debug: z, theta, theta1 of samples k0..k0+n-1 of one robot (same draw code)
 // ---------------------------------------------------------------------------
@@ -1221,6 +1283,7 @@ struct PEntry {
   static cudaError_t rollout(const Params& p, int mode, bool fused, cudaStream_t s);
   static int occupancy(int mode);
   static cudaError_t elite(const Params& p, cudaStream_t s);
+  static cudaError_t naive_finalize(const Params& p, cudaStream_t s);
   static cudaError_t debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                    int* fidx, cudaStream_t s);
   static cudaError_t prepare();  // function attributes, set once outside any stream capture
@@ -1239,8 +1302,8 @@ static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
 template <int P>
 cudaError_t PEntry<P>::rollout(const Params& p, int mode, bool fused, cudaStream_t s) {
   if (mode == SBS_MPPI) return fused ? launch_rollout_t<P, EPI_MPPI, true>(p, s) : launch_rollout_t<P, EPI_MPPI, false>(p, s);
-  if (mode == SBS_NAIVE) return launch_rollout_t<P, EPI_ARGMIN, true>(p, s);
-  return launch_rollout_t<P, EPI_ARGMIN, false>(p, s);  // CEM: select + elite kernels follow
+  if (mode == SBS_NAIVE && fused) return launch_rollout_t<P, EPI_ARGMIN, true>(p, s);
+  return launch_rollout_t<P, EPI_ARGMIN, false>(p, s);  // CEM, or sharded Naive: records only
 }
 
 template <int P>
@@ -1259,6 +1322,12 @@ template <int P>
 cudaError_t PEntry<P>::elite(const Params& p, cudaStream_t s) {
   dim3 grid(p.n_eblk, p.R);
   sbs_elite_kernel<P><<<grid, 32 * 3 * P, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int P>
+cudaError_t PEntry<P>::naive_finalize(const Params& p, cudaStream_t s) {
+  sbs_naive_finalize_kernel<P><<<p.R, 128, 0, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -1314,6 +1383,16 @@ cudaError_t launch_elite(const Params& p, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_naive_finalize(const Params& p, cudaStream_t s) {
+  SBS_DISPATCH_P(p.P, naive_finalize(p, s));
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_argmin_emit(const Params& p, float* emit, cudaStream_t s) {
+  sbs_argmin_emit_kernel<<<p.R, 128, 0, s>>>(p, emit);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                  int* fidx, cudaStream_t s) {
   SBS_DISPATCH_P(p.P, debug_samples(p, robot, k0, n, z, theta, fidx, s));
@@ -1335,25 +1414,42 @@ static size_t select_smem(int64_t K) {
   return (size_t)(kSelHistWords + (K <= kSelSmemKeys ? K : 0)) * 4;
 }
 
+template <int MODE, bool SMALL>
+static cudaError_t set_select_attr() {
+  return cudaFuncSetAttribute(sbs_select_kernel<MODE, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              SMALL ? kSelSmallSmemBytes : kSelSmemBytes);
+}
+
 cudaError_t prepare_kernels(int P) {
-  cudaError_t e = cudaFuncSetAttribute(sbs_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(sbs_select_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(sbs_select_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmallSmemBytes);
+  cudaError_t e = cudaFuncSetAttribute(sbs_select_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSelSmemBytes);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_select_small_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSelSmallSmemBytes);
+  if (e == cudaSuccess) e = set_select_attr<SEL_LOCAL, true>();
+  if (e == cudaSuccess) e = set_select_attr<SEL_LOCAL, false>();
+  if (e == cudaSuccess) e = set_select_attr<SEL_EMIT, true>();
+  if (e == cudaSuccess) e = set_select_attr<SEL_EMIT, false>();
+  if (e == cudaSuccess) e = set_select_attr<SEL_MERGE, true>();
+  if (e == cudaSuccess) e = set_select_attr<SEL_MERGE, false>();
   if (e != cudaSuccess || P == 0) return e;
   SBS_DISPATCH_P(P, prepare());
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_select(const Params& p, cudaStream_t s) {
-  const size_t smem = select_smem(p.K_local);
-  if (p.K_local <= kSelSmallMax) sbs_select_small_kernel<<<p.R, kSelBlock, smem, s>>>(p);
-  else sbs_select_kernel<<<p.R, kSelBlock, smem, s>>>(p);
+template <int MODE>
+static cudaError_t launch_select_t(const Params& p, int64_t K, float* emit, cudaStream_t s) {
+  const size_t smem = select_smem(K);
+  if (K <= kSelSmallMax) sbs_select_kernel<MODE, true><<<p.R, kSelBlock, smem, s>>>(p, emit);
+  else sbs_select_kernel<MODE, false><<<p.R, kSelBlock, smem, s>>>(p, emit);
   return cudaGetLastError();
+}
+
+cudaError_t launch_select(const Params& p, cudaStream_t s) { return launch_select_t<SEL_LOCAL>(p, p.K_local, nullptr, s); }
+cudaError_t launch_select_emit(const Params& p, float* emit, cudaStream_t s) {
+  return launch_select_t<SEL_EMIT>(p, p.K_local, emit, s);
+}
+cudaError_t launch_select_merge(const Params& p, cudaStream_t s) {
+  return launch_select_t<SEL_MERGE>(p, (int64_t)p.n_cta * p.n_elite, nullptr, s);
 }
 
 cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s) {

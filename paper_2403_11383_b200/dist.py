@@ -2,7 +2,7 @@
 
 The library shards the K samples of every robot by global sample index
 (`shard_range`, the same formula as sbs_create in csrc/sbs_api.cpp) and combines
-the ranks' MPPI records with one NCCL all-gather inside sbs_step; this module only
+the ranks' records (MPPI, Naive or CEM) with one NCCL all-gather inside sbs_step; this module only
 bootstraps the NCCL communicator (rank 0's ncclUniqueId broadcast over the
 torch.distributed store) -- no method arithmetic here.
 """

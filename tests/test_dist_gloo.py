@@ -5,8 +5,11 @@ sample indices (the counter RNG makes the noise independent of the sharding),
 reduces it to one MPPI record (beta_r, sum w, sum w^2, sum w theta relative to
 beta_r) and the ranks' records are all-gathered and merged in rank order.  Here
 the per-rank work is done by the CPU oracle and the exchange by gloo; the merged
-result must equal the single-process oracle iteration.  Also covered: the NCCL
-unique-id bootstrap through torch.distributed.
+result must equal the single-process oracle iteration.  CEM / Naive: every rank
+offers its K_e smallest (J, k) (Naive: K_e = 1), the offers are all-gathered in
+rank order (= global index order) and the K_e smallest of the world * K_e
+candidates are the global elite set.  Also covered: the NCCL unique-id
+bootstrap through torch.distributed.
 """
 import math
 import os
@@ -106,3 +109,49 @@ def test_shard_range_matches_library_formula():
             assert all(slices[i][0] + slices[i][1] == slices[i + 1][0] for i in range(world - 1))
             assert slices[-1][0] + slices[-1][1] == K
             assert max(s[1] for s in slices) - min(s[1] for s in slices) <= 1
+
+
+def _cem_worker(rank, world, port, cfg, inp, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import Oracle
+    orc = Oracle()
+    K, D = cfg["n_samples"], 12 * cfg["knots"]
+    ke = 1 if cfg["mode"] == "naive" else cfg["n_elite"]
+    st = W.initial_distribution(cfg)
+    mu_s = orc.warm_shift(cfg, st["mean"])
+    k0, kl = shard_range(K, rank, world)
+    J = np.zeros(kl)
+    for i in range(kl):
+        th, _, f = orc.sample(cfg, mu_s, st["var"], 0, 0, 0, k0 + i)
+        J[i] = orc.rollout(cfg, inp["x0"], inp["phase"], inp["feet_cur"], inp["feet_next"], inp["xref"], th, f)
+    loc = np.sort(orc.cem_select(J, ke))                          # local K_e smallest, index order
+    offer = torch.tensor(np.concatenate([J[loc], (k0 + loc).astype(np.float64)]), dtype=torch.float64)
+    offers = [torch.zeros_like(offer) for _ in range(world)]
+    dist.all_gather(offers, offer)
+    cand_J = np.concatenate([o.numpy()[:ke] for o in offers])     # rank order = global index order
+    cand_k = np.concatenate([o.numpy()[ke:] for o in offers]).astype(np.int64)
+    assert np.all(np.diff(cand_k) > 0)
+    elite = cand_k[orc.cem_select(cand_J, ke)]                    # (J, position) order = (J, k) order
+    out_q.put((rank, elite))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode,K,ke", [("cem", 400, 50), ("cem", 301, 150), ("naive", 300, 1)])
+def test_two_rank_cem_elites_equal_single_process(orc, mode, K, ke):
+    cfg, inputs = W.config3(mode, K=K)
+    cfg = dict(cfg, n_elite=ke)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cem_worker, args=(r, 2, port, cfg, inputs[0], q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ro = orc.step(cfg, 0, inputs[0], W.initial_distribution(cfg))
+    for _, elite in res:
+        np.testing.assert_array_equal(elite, ro.elite[:ke])       # same set, same rank order

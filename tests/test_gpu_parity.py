@@ -355,3 +355,63 @@ def test_sharded_mppi_records_match_single_gpu(B, orc, K, world):
     ro = orc.step(cfg, 0, inputs[0], dict(st))
     _check_outputs(outs[0], ro, cfg)
     assert all(c.iter == 1 for c in ranks)
+
+
+@pytest.mark.parametrize("mode,K,world,ke", [("cem", 10000, 2, 1000), ("cem", 10000, 4, 2500), ("cem", 4099, 3, 37),
+                                             ("cem", 40000, 2, 3000), ("naive", 10000, 2, 1), ("naive", 5003, 4, 1)])
+def test_sharded_cem_naive_records_match_single_gpu(B, orc, mode, K, world, ke):
+    """Sample-sharded CEM / Naive on one GPU through the caller-driven
+    exchange: every rank offers its K_e smallest (J, k) (CEM) or its argmin
+    (Naive); after the rank-order merge every rank holds the same elite set and
+    distribution, bitwise equal to world = 1 (same costs, same exact selection,
+    same regenerated elites and moment order), and within tolerance of the oracle."""
+    import ctypes as C
+
+    import torch
+    cfg, inputs = W.config3(mode, K=K)
+    cfg = dict(cfg, n_elite=ke)
+    st = W.initial_distribution(cfg)
+    arr = B.make_inputs(inputs)
+    d_in = torch.from_numpy(np.frombuffer(bytes(arr), dtype=np.uint8).copy()).cuda()
+    ranks = [B.Controller(cfg, rank=g, world=world) for g in range(world)]
+    for c in ranks:
+        c.set_reference(0, inputs[0]["xref"])
+    nrec = ranks[0].record_floats()
+    assert nrec % 4 == 0 and nrec >= 8 + (2 * ke if mode == "cem" else 0)
+    recs = torch.zeros((world, nrec), dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    for g, c in enumerate(ranks):
+        c.step_records(d_in.data_ptr(), recs[g].data_ptr(), s)
+    outs, elites = [], []
+    for c in ranks:
+        d_out = torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+        c.finish_records(recs.data_ptr(), d_in.data_ptr(), d_out.data_ptr(), s)
+        torch.cuda.synchronize()
+        o = B.sbs_output.from_buffer_copy(d_out.cpu().numpy().tobytes())
+        outs.append(B.output_dict(o, 48))
+        elites.append(c.debug_elites(0))
+    single = _ctrl(B, cfg, inputs, st)
+    _, so = single.step(inputs)
+    J = np.concatenate([c.debug_costs()[0] for c in ranks])
+    np.testing.assert_array_equal(J, single.debug_costs()[0])
+    e1 = single.debug_elites(0)
+    for o, e in zip(outs, elites):
+        np.testing.assert_array_equal(e, e1)                       # same global elite set, index order
+        np.testing.assert_array_equal(o["mean"], so[0]["mean"])    # bitwise: same elites, same order
+        np.testing.assert_array_equal(o["var"], so[0]["var"])
+        np.testing.assert_array_equal(o["u0"], so[0]["u0"])
+        assert o["freq_idx"] == so[0]["freq_idx"] and o["j_min"] == so[0]["j_min"]
+        assert o["n_diverged"] == so[0]["n_diverged"]
+        assert abs(o["j_mean"] - so[0]["j_mean"]) <= 1e-5 * abs(so[0]["j_mean"])  # rank-grouped sum
+    # the elite set is the exact K_e smallest (J, k) of the concatenated costs
+    order = np.lexsort((np.arange(K), np.where(np.isfinite(J), J, np.inf)))
+    np.testing.assert_array_equal(np.sort(order[:ke]), e1)
+    ro = orc.step(cfg, 0, inputs[0], dict(st))
+    _check_outputs(outs[0], ro, cfg)
+    assert all(c.iter == 1 for c in ranks)
+
+
+def test_sharded_cem_rejects_too_few_samples_per_rank(B):
+    cfg, _ = W.config3("cem", K=1000)
+    with pytest.raises(Exception):
+        B.Controller(dict(cfg, n_elite=600), rank=0, world=2)
