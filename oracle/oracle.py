@@ -66,6 +66,28 @@ class OrcOutput(C.Structure):
                 ("status", C.c_int32), ("freq_hz", C.c_double), ("diag", OrcDiag)]
 
 
+class OrcLoopConfig(C.Structure):
+    _fields_ = [("hip", C.c_double * 12), ("h_nom", C.c_double), ("fall_angle", C.c_double),
+                ("fall_height", C.c_double)]
+
+
+def make_loop_config(lc: dict) -> OrcLoopConfig:
+    o = OrcLoopConfig()
+    o.hip[:] = [float(v) for v in np.asarray(lc["hip"], dtype=np.float64).reshape(12)]
+    o.h_nom, o.fall_angle, o.fall_height = float(lc["h_nom"]), float(lc["fall_angle"]), float(lc["fall_height"])
+    return o
+
+
+@dataclass
+class AdvanceResult:
+    fallen: int
+    x0: np.ndarray
+    phase: int
+    feet_cur: np.ndarray
+    feet_next: np.ndarray
+    xref: np.ndarray
+
+
 def _dp(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
@@ -163,6 +185,13 @@ class Oracle:
         L.orc_step.argtypes = [cfgp, C.c_uint32, dp, C.c_uint32, dp, dp, dp,
                                C.POINTER(OrcState), C.POINTER(OrcOutput), dp, i32p, dp,
                                C.POINTER(C.c_float), C.POINTER(C.c_int64)]
+        L.orc_foothold.argtypes = [dp, dp, dp, C.c_double, C.c_double, C.c_double, dp]
+        L.orc_plant_dynamics.argtypes = [cfgp, dp, dp, i32p, dp, dp, dp]
+        L.orc_plant_step.argtypes = [cfgp, dp, dp, i32p, dp, dp, C.c_double, dp]
+        L.orc_reference.argtypes = [cfgp, C.c_double, dp, dp, C.c_double, dp]
+        L.orc_advance.argtypes = [cfgp, C.POINTER(OrcLoopConfig), dp, C.c_uint32, dp, dp, dp, i32p, C.c_int32,
+                                  dp, C.c_double, dp, dp, u32p, dp, dp, dp]
+        L.orc_advance.restype = C.c_int
 
     # ---- noise -----------------------------------------------------------
     def philox(self, ctr, key):
@@ -331,3 +360,47 @@ class Oracle:
                           contact0=np.array(out.contact0), j_min=dg.j_min, j_mean=dg.j_mean,
                           omega=dg.omega, ess=dg.ess, n_diverged=dg.n_diverged, argmin=dg.argmin,
                           J=J, fidx=fidx, theta=theta, z=z, elite=elite)
+
+    # ---- closed loop (L36-L40) -------------------------------
+    def foothold(self, p_hip, v_c, v_d, p_cz, t_st, g):
+        out = np.zeros(3)
+        self.lib.orc_foothold(_dp(_f64(p_hip, 3)), _dp(_f64(v_c, 3)), _dp(_f64(v_d, 3)), float(p_cz),
+                              float(t_st), float(g), _dp(out))
+        return out
+
+    def plant_dynamics(self, cfg, x, gamma, stance, feet, wrench):
+        xd = np.zeros(12)
+        st = np.asarray(stance, dtype=np.int32)
+        self.lib.orc_plant_dynamics(C.byref(make_config(cfg)), _dp(_f64(x, 12)), _dp(_f64(gamma, 12)),
+                                    st.ctypes.data_as(C.POINTER(C.c_int32)), _dp(_f64(feet, 12)),
+                                    _dp(_f64(wrench, 6)), _dp(xd))
+        return xd
+
+    def plant_step(self, cfg, x, gamma, stance, feet, wrench, h):
+        xn = np.zeros(12)
+        st = np.asarray(stance, dtype=np.int32)
+        self.lib.orc_plant_step(C.byref(make_config(cfg)), _dp(_f64(x, 12)), _dp(_f64(gamma, 12)),
+                                st.ctypes.data_as(C.POINTER(C.c_int32)), _dp(_f64(feet, 12)),
+                                _dp(_f64(wrench, 6)), float(h), _dp(xn))
+        return xn
+
+    def reference(self, cfg, h_nom, x, v_d, yaw_rate):
+        xr = np.zeros((cfg["horizon"], 12))
+        self.lib.orc_reference(C.byref(make_config(cfg)), float(h_nom), _dp(_f64(x, 12)), _dp(_f64(v_d, 3)),
+                               float(yaw_rate), _dp(xr))
+        return xr
+
+    def advance(self, cfg, lc, inp, u0, contact0, freq_idx, v_d, yaw_rate=0.0, wrench=None):
+        """One closed-loop advance of one robot: plant, fall flag, phase, footholds, reference."""
+        x = np.zeros(12)
+        ph = C.c_uint32(0)
+        fc, fn = np.zeros(12), np.zeros(12)
+        xr = np.zeros((cfg["horizon"], 12))
+        ct = np.asarray(contact0, dtype=np.int32)
+        w = np.zeros(6) if wrench is None else _f64(wrench, 6)
+        fallen = self.lib.orc_advance(
+            C.byref(make_config(cfg)), C.byref(make_loop_config(lc)), _dp(_f64(inp["x0"], 12)),
+            int(inp["phase"]) & 0xFFFFFFFF, _dp(_f64(inp["feet_cur"], 12)), _dp(_f64(inp["feet_next"], 12)),
+            _dp(_f64(u0, 12)), ct.ctypes.data_as(C.POINTER(C.c_int32)), int(freq_idx), _dp(_f64(v_d, 3)),
+            float(yaw_rate), _dp(w), _dp(x), C.byref(ph), _dp(fc), _dp(fn), _dp(xr))
+        return AdvanceResult(fallen=int(fallen), x0=x, phase=int(ph.value), feet_cur=fc, feet_next=fn, xref=xr)

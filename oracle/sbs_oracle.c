@@ -632,3 +632,119 @@ int orc_step(const orc_config* c, uint32_t robot, const double x0[12], uint32_t 
   free(theta); free(J); free(fidx);
   return out->status = rc;
 }
+
+/* ======================================================================
+ * the closed loop around one iteration (readings L36-L40).
+ * The MPC output drives an SRBD plant for one control period; the gait
+ * phase advances at the chosen step frequency; the foothold reference
+ * generator (Eq. 3) places the next footholds; the state
+ * reference is rebuilt from the command (L13).  Order as in P:212 / P:313:
+ * apply u0 -> plant -> leg framework -> next MPC iteration.
+ * ==================================================================== */
+
+/* Eq. 3: p_f = p_hip + T_st/2 v_d + sqrt(p_cz / g) (v_c - v_d),
+ * horizontal components, z snapped to the flat terrain (L38). */
+void orc_foothold(const double p_hip[3], const double v_c[3], const double v_d[3], double p_cz,
+                  double t_st, double g, double p_f[3]) {
+  const double k = sqrt(fmax(p_cz, 0.0) / g);
+  for (int a = 0; a < 2; ++a) p_f[a] = p_hip[a] + 0.5 * t_st * v_d[a] + k * (v_c[a] - v_d[a]);
+  p_f[2] = 0.0;
+}
+
+/* Eq. 1 with an external wrench at the CoM (L36): force F_e and torque tau_e,
+ * both world frame ("wrenches ... applied to the robot CoM"):
+ * v_dot += F_e / m,  omega_dot += I^-1 R^T tau_e. */
+void orc_plant_dynamics(const orc_config* c, const double x[12], const double gamma[12],
+                        const int32_t stance[4], const double feet[12], const double wrench[6],
+                        double xd[12]) {
+  orc_dynamics(c, x, gamma, stance, feet, xd);
+  const double phi = x[6], th = x[7], psi = x[8];
+  const double cr = cos(phi), sr = sin(phi), cp = cos(th), sp = sin(th), cy = cos(psi), sy = sin(psi);
+  const double Rz[9] = {cy, -sy, 0, sy, cy, 0, 0, 0, 1};
+  const double Ry[9] = {cp, 0, sp, 0, 1, 0, -sp, 0, cp};
+  const double Rx[9] = {1, 0, 0, 0, cr, -sr, 0, sr, cr};
+  double Rzy[9], R[9], tb[3], Iinv[9], wd[3];
+  mat3_mul(Rz, Ry, Rzy);
+  mat3_mul(Rzy, Rx, R);
+  mat3T_vec(R, &wrench[3], tb);
+  mat3_inv(c->inertia, Iinv);
+  mat3_vec(Iinv, tb, wd);
+  for (int a = 0; a < 3; ++a) {
+    xd[3 + a] += wrench[a] / c->mass;
+    xd[9 + a] += wd[a];
+  }
+}
+
+/* one control period of the plant: classic RK4, u and wrench held (L36) */
+void orc_plant_step(const orc_config* c, const double x[12], const double gamma[12],
+                    const int32_t stance[4], const double feet[12], const double wrench[6], double h,
+                    double xn[12]) {
+  double k1[12], k2[12], k3[12], k4[12], t[12];
+  orc_plant_dynamics(c, x, gamma, stance, feet, wrench, k1);
+  for (int a = 0; a < 12; ++a) t[a] = x[a] + 0.5 * h * k1[a];
+  orc_plant_dynamics(c, t, gamma, stance, feet, wrench, k2);
+  for (int a = 0; a < 12; ++a) t[a] = x[a] + 0.5 * h * k2[a];
+  orc_plant_dynamics(c, t, gamma, stance, feet, wrench, k3);
+  for (int a = 0; a < 12; ++a) t[a] = x[a] + h * k3[a];
+  orc_plant_dynamics(c, t, gamma, stance, feet, wrench, k4);
+  for (int a = 0; a < 12; ++a) xn[a] = x[a] + h / 6.0 * (k1[a] + 2.0 * k2[a] + 2.0 * k3[a] + k4[a]);
+}
+
+/* L13: x^r_j = (p_xy + v_d j dt, h_nom | v_d | 0, 0, psi + yaw_rate j dt | 0, 0, yaw_rate) */
+void orc_reference(const orc_config* c, double h_nom, const double x[12], const double v_d[3],
+                   double yaw_rate, double* xref) {
+  for (int j = 0; j < c->horizon; ++j) {
+    double* r = &xref[12 * j];
+    const double t = (double)j * c->dt;
+    r[0] = x[0] + v_d[0] * t;
+    r[1] = x[1] + v_d[1] * t;
+    r[2] = h_nom;
+    r[3] = v_d[0];
+    r[4] = v_d[1];
+    r[5] = v_d[2];
+    r[6] = 0.0;
+    r[7] = 0.0;
+    r[8] = x[8] + yaw_rate * t;
+    r[9] = 0.0;
+    r[10] = 0.0;
+    r[11] = yaw_rate;
+  }
+}
+
+/* the whole advance of one robot (L36-L40); returns the fall flag (L40) */
+int orc_advance(const orc_config* c, const orc_loop_config* lc, const double x0[12], uint32_t phase0,
+                const double feet_cur[12], const double feet_next[12], const double u0[12],
+                const int32_t contact0[4], int32_t freq_idx, const double v_d[3], double yaw_rate,
+                const double wrench[6], double x_out[12], uint32_t* phase_out, double feet_cur_out[12],
+                double feet_next_out[12], double* xref_out) {
+  /* 1. plant: u0 held over dt on the stance legs, lever arms on feet_cur (L36) */
+  orc_plant_step(c, x0, u0, contact0, feet_cur, wrench, c->dt, x_out);
+  /* 2. fall criterion (L40) */
+  int fallen = 0;
+  for (int a = 0; a < 12; ++a) fallen |= !isfinite(x_out[a]);
+  fallen |= fabs(x_out[6]) > lc->fall_angle || fabs(x_out[7]) > lc->fall_angle || x_out[2] < lc->fall_height;
+  /* 3. gait phase at the chosen step frequency (L37) */
+  const double f = c->freq_hz[freq_idx];
+  *phase_out = phase0 + orc_phase_inc(f, c->dt);
+  /* 4. touchdown: a leg that was in swing and is now in stance lands on its planned foothold (L38) */
+  const uint64_t thr = orc_stance_threshold(c->duty_factor);
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t off = (uint32_t)(uint64_t)llround(c->phase_offset[i] * 4294967296.0);
+    const int st_new = ((uint64_t)(uint32_t)(*phase_out + off) < thr);
+    const int land = !contact0[i] && st_new;
+    for (int a = 0; a < 3; ++a) feet_cur_out[3 * i + a] = land ? feet_next[3 * i + a] : feet_cur[3 * i + a];
+  }
+  /* 5. next footholds, Eq. 3 with T_st = D_f / f_s at the new state */
+  const double t_st = c->duty_factor / f;
+  const double g = fabs(c->gravity[2]);
+  const double cy = cos(x_out[8]), sy = sin(x_out[8]);
+  const double v_c[3] = {x_out[3], x_out[4], 0.0};
+  for (int i = 0; i < 4; ++i) {
+    const double* hp = &lc->hip[3 * i];
+    const double p_hip[3] = {x_out[0] + cy * hp[0] - sy * hp[1], x_out[1] + sy * hp[0] + cy * hp[1], 0.0};
+    orc_foothold(p_hip, v_c, v_d, x_out[2], t_st, g, &feet_next_out[3 * i]);
+  }
+  /* 6. reference rebuilt from the command at the new state (L13) */
+  if (xref_out) orc_reference(c, lc->h_nom, x_out, v_d, yaw_rate, xref_out);
+  return fallen;
+}

@@ -124,4 +124,26 @@ int orc_step(const orc_config* c, uint32_t robot, const double x0[12], uint32_t 
              double* J_out /*[K] or NULL*/, int32_t* fidx_out /*[K] or NULL*/,
              double* theta_out /*[K][D] or NULL*/, float* z_out /*[K][D] or NULL*/,
              int64_t* elite_out /*[K_e] or NULL*/);
+/* ---- closed loop around the iteration (L36-L40) ---- */
+typedef struct orc_loop_config {
+  double hip[12];               /* body-frame hip offsets FL, FR, RL, RR (L29); z ignored */
+  double h_nom;                 /* nominal CoM height of the rebuilt reference (L13) */
+  double fall_angle, fall_height; /* fallen iff |roll| or |pitch| > fall_angle or p_z < fall_height (L40) */
+} orc_loop_config;
+
+void orc_foothold(const double p_hip[3], const double v_c[3], const double v_d[3], double p_cz,
+                  double t_st, double g, double p_f[3]);                  /* Eq. 3 */
+void orc_plant_dynamics(const orc_config* c, const double x[12], const double gamma[12],
+                        const int32_t stance[4], const double feet[12], const double wrench[6],
+                        double xd[12]);
+void orc_plant_step(const orc_config* c, const double x[12], const double gamma[12],
+                    const int32_t stance[4], const double feet[12], const double wrench[6], double h,
+                    double xn[12]);
+void orc_reference(const orc_config* c, double h_nom, const double x[12], const double v_d[3],
+                   double yaw_rate, double* xref /*[H][12]*/);
+int orc_advance(const orc_config* c, const orc_loop_config* lc, const double x0[12], uint32_t phase0,
+                const double feet_cur[12], const double feet_next[12], const double u0[12],
+                const int32_t contact0[4], int32_t freq_idx, const double v_d[3], double yaw_rate,
+                const double wrench[6], double x_out[12], uint32_t* phase_out, double feet_cur_out[12],
+                double feet_next_out[12], double* xref_out /*[H][12] or NULL*/);
 #endif

@@ -103,6 +103,12 @@ def robot_input(cfg: dict, robot: int, cmd=(0.0, 0.0, 0.0), phase=0, push=None, 
                 xref=f32(xref))
 
 
+def loop_config() -> dict:
+    """Closed-loop constants (L38, L40): hip offsets (L29), nominal
+    height (L13), fall criterion |roll|, |pitch| > 0.8 rad or p_z < 0.12 m."""
+    return dict(hip=f32(HIPS.reshape(12)), h_nom=f32(H_NOM), fall_angle=f32(0.8), fall_height=f32(0.12))
+
+
 def q32(frac: float) -> int:
     return int(round(frac * 2 ** 32)) & 0xFFFFFFFF
 
