@@ -199,6 +199,64 @@ int sbs_record_floats(const sbs_ctx* ctx);
 int sbs_step_records(sbs_ctx* ctx, const sbs_input* d_in, float* d_rec, void* stream);
 int sbs_finish_records(sbs_ctx* ctx, const float* d_recs, const sbs_input* d_in, sbs_output* d_out, void* stream);
 
+/* ---- closed loop around the iteration (DESIGN L36-L40) -------
+ * The MPC output drives a plant for one control period and the next
+ * iteration's inputs are built on the device, so a whole closed-loop episode
+ * (for every robot of the context) runs without host round trips:
+ *   plant (L36): x <- one RK4 step (dt) of Eq. 1 with u0 on the
+ *     stance legs (contact0, lever arms on feet_cur) plus an external wrench
+ *     (world-frame force and torque at the CoM): v_dot += F/m,
+ *     omega_dot += I^-1 R^T tau;
+ *   fall (L40): |roll| or |pitch| > fall_angle or p_z < fall_height (or a
+ *     non-finite state) sets fallen[r]; a fallen robot's inputs are frozen;
+ *   gait (L37): phase += Q0.32 increment of the chosen step frequency;
+ *     freq_idx <- the chosen theta1 (output freq_idx);
+ *   footholds (L38, Eq. 3): a leg that was in swing and is in
+ *     stance at the new phase lands on its planned foothold (feet_cur <-
+ *     feet_next); every leg's next foothold is Eq. 3 at the new state with
+ *     p_hip = p_c + Rz(yaw) hip_i (z = 0) and T_st = D_f / f_s;
+ *   reference (L13): the context's x^r is rebuilt from the command at the
+ *     new state: p^r_j = p_xy + v_d j dt, h_nom; v^r = v_d;
+ *     yaw^r_j = yaw + yaw_rate j dt; omega^r = (0, 0, yaw_rate).
+ * A later host-path sbs_step uploads the host-staged reference again (call
+ * sbs_set_reference first). */
+typedef struct sbs_loop_config {
+  float hip[12];          /* body-frame hip offsets FL, FR, RL, RR (z ignored) */
+  float h_nom;            /* nominal CoM height of the rebuilt reference (L13) */
+  float fall_angle;       /* rad (L40) */
+  float fall_height;      /* m (L40) */
+} sbs_loop_config;
+
+typedef struct sbs_command {  /* per robot, device */
+  float v[3];             /* desired CoM velocity v_c^d, world frame (Eq. 3) */
+  float yaw_rate;         /* desired yaw rate (L13) */
+} sbs_command;
+
+#define SBS_TRACE_FLOATS 16   /* per robot per iteration: x after the plant step [12], freq_hz,
+                                 j_min, fallen, status */
+
+/* One advance of every robot after a step: d_in [R] is updated in place from
+ * d_out [R] (the outputs of the step that consumed d_in).  d_cmd [R];
+ * d_wrench [R][6] (F, tau) or NULL (no disturbance); d_fallen [R] (in/out,
+ * sticky).  Stream-ordered; does not change iter. */
+int sbs_advance(sbs_ctx* ctx, sbs_input* d_in, const sbs_output* d_out, const sbs_command* d_cmd,
+                const float* d_wrench, int32_t* d_fallen, const sbs_loop_config* lc, void* stream);
+
+/* n_iter closed-loop iterations on the device: each is sbs_step_device(d_in,
+ * d_out) then sbs_advance with wrench row i of d_wrench [n_iter][R][6] (or
+ * NULL) and, if d_trace [n_iter][R][SBS_TRACE_FLOATS] is not NULL, trace row
+ * i.  One iteration is captured once as a CUDA graph (the iteration counter
+ * lives in device memory) and replayed n_iter times.  world = 1 only.
+ * iter += n_iter.  Stream-ordered. */
+int sbs_run_loop(sbs_ctx* ctx, int32_t n_iter, sbs_input* d_in, sbs_output* d_out, const sbs_command* d_cmd,
+                 const float* d_wrench, int32_t* d_fallen, float* d_trace, const sbs_loop_config* lc,
+                 void* stream);
+
+/* The context's current reference of one robot (host out [H][12]): the last
+ * sbs_set_reference / sbs_set_reference_device, or the rebuild of the last
+ * sbs_advance / sbs_run_loop.  Synchronises the context's stream. */
+int sbs_get_reference(sbs_ctx* ctx, int32_t robot, float* x_ref);
+
 /* Exact checkpoint of the distribution state (means, vars, freq indices,
  * iteration counter, seed).  nbytes: in = capacity, out = size needed. */
 int sbs_get_state(sbs_ctx* ctx, void* buf, uint64_t* nbytes);
@@ -226,7 +284,8 @@ int sbs_local_range(const sbs_ctx* ctx, int64_t* k_begin, int64_t* K_local);
 #define SBS_KERNEL_REDUCE 1
 #define SBS_KERNEL_SELECT 2
 #define SBS_KERNEL_ELITE 3
-#define SBS_NKERNELS 4
+#define SBS_KERNEL_ADVANCE 4
+#define SBS_NKERNELS 5
 int sbs_profile(sbs_ctx* ctx, int32_t enable);
 int sbs_kernel_times(sbs_ctx* ctx, double* total_ms /*[SBS_NKERNELS]*/, int64_t* launches /*[SBS_NKERNELS]*/);
 /* Number of kernel launches one sbs_step issues (for the bench's gpu_launches). */

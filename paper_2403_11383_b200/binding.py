@@ -22,7 +22,7 @@ SBS_MAX_HORIZON = 64
 MODES = {"mppi": 0, "cem": 1, "naive": 2}
 STATUS = {0: "SBS_OK", 1: "SBS_WARN_ALL_DIVERGED", -1: "SBS_ERR_INVALID_ARG", -2: "SBS_ERR_SINGULAR",
           -3: "SBS_ERR_NONFINITE", -4: "SBS_ERR_STATE", -5: "SBS_ERR_CUDA", -6: "SBS_ERR_NCCL", -7: "SBS_ERR_OOM"}
-KERNELS = ["rollout", "reduce", "select", "elite"]
+KERNELS = ["rollout", "reduce", "select", "elite", "advance"]
 
 
 class sbs_config(C.Structure):
@@ -52,6 +52,25 @@ class sbs_output(C.Structure):
                 ("freq_hz", C.c_float), ("status", C.c_int32), ("iter", C.c_uint32), ("j_min", C.c_float),
                 ("j_mean", C.c_float), ("omega", C.c_float), ("ess", C.c_float), ("n_diverged", C.c_int32),
                 ("device_us", C.c_float), ("mean", C.c_float * SBS_MAX_D), ("var", C.c_float * SBS_MAX_D)]
+
+
+class sbs_loop_config(C.Structure):
+    _fields_ = [("hip", C.c_float * 12), ("h_nom", C.c_float), ("fall_angle", C.c_float),
+                ("fall_height", C.c_float)]
+
+
+class sbs_command(C.Structure):
+    _fields_ = [("v", C.c_float * 3), ("yaw_rate", C.c_float)]
+
+
+SBS_TRACE_FLOATS = 16
+
+
+def make_loop_config(lc: dict) -> sbs_loop_config:
+    o = sbs_loop_config()
+    o.hip[:] = [float(v) for v in np.asarray(lc["hip"], dtype=np.float64).reshape(12)]
+    o.h_nom, o.fall_angle, o.fall_height = float(lc["h_nom"]), float(lc["fall_angle"]), float(lc["fall_height"])
+    return o
 
 
 class SBSError(RuntimeError):
@@ -105,6 +124,9 @@ def load_library(path: str = LIB_PATH):
         "sbs_record_floats": ([ctxp], C.c_int),
         "sbs_step_records": ([ctxp, vp, vp, vp], C.c_int),
         "sbs_finish_records": ([ctxp, vp, vp, vp, vp], C.c_int),
+        "sbs_get_reference": ([ctxp, C.c_int32, P(C.c_float)], C.c_int),
+        "sbs_advance": ([ctxp, vp, vp, vp, vp, vp, P(sbs_loop_config), vp], C.c_int),
+        "sbs_run_loop": ([ctxp, C.c_int32, vp, vp, vp, vp, vp, vp, P(sbs_loop_config), vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -300,10 +322,31 @@ class Controller:
         return self._check(self.L.sbs_profile(self.ctx, 1 if enable else 0))
 
     def kernel_times(self):
-        ms = (C.c_double * 4)()
-        n = (C.c_int64 * 4)()
+        nk = len(KERNELS)
+        ms = (C.c_double * nk)()
+        n = (C.c_int64 * nk)()
         self._check(self.L.sbs_kernel_times(self.ctx, ms, n))
-        return {KERNELS[i]: (ms[i], n[i]) for i in range(4)}
+        return {KERNELS[i]: (ms[i], n[i]) for i in range(nk)}
+
+    def get_reference(self, robot: int = 0):
+        x = np.zeros((self.H, 12), dtype=np.float32)
+        self._check(self.L.sbs_get_reference(self.ctx, robot, _fp(x)))
+        return x
+
+    # ---- closed loop: device pointers (ints), 0 for NULL ----
+    def advance(self, d_in: int, d_out: int, d_cmd: int, d_wrench: int, d_fallen: int, lc: dict, stream: int = 0):
+        lcs = make_loop_config(lc)
+        return self._check(self.L.sbs_advance(self.ctx, C.c_void_p(d_in), C.c_void_p(d_out), C.c_void_p(d_cmd or None),
+                                              C.c_void_p(d_wrench or None), C.c_void_p(d_fallen or None),
+                                              C.byref(lcs), C.c_void_p(stream)))
+
+    def run_loop(self, n_iter: int, d_in: int, d_out: int, d_cmd: int, d_wrench: int, d_fallen: int, d_trace: int,
+                 lc: dict, stream: int = 0):
+        lcs = make_loop_config(lc)
+        return self._check(self.L.sbs_run_loop(self.ctx, int(n_iter), C.c_void_p(d_in), C.c_void_p(d_out),
+                                               C.c_void_p(d_cmd or None), C.c_void_p(d_wrench or None),
+                                               C.c_void_p(d_fallen or None), C.c_void_p(d_trace or None),
+                                               C.byref(lcs), C.c_void_p(stream)))
 
     def launches_per_step(self) -> int:
         return int(self.L.sbs_launches_per_step(self.ctx))

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsbs.so")
-SOURCES = ["sbs_kernels.cu", "sbs_api.cpp"]
+SOURCES = ["sbs_kernels.cu", "sbs_loop.cu", "sbs_api.cpp"]
 HEADERS = ["sbs_internal.h", "sbs_noise.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -36,6 +36,7 @@ def _units():
     for the common kernels, plus the host runtime -- compiled in parallel."""
     units = [("sbs_kernels.cu", [f"SBS_TU_P={p}"], f"p{p}") for p in range(2, 9)]
     units.append(("sbs_kernels.cu", ["SBS_TU_COMMON"], "common"))
+    units.append(("sbs_loop.cu", [], "loop"))
     units.append(("sbs_api.cpp", [], "api"))
     return units
 
@@ -57,7 +58,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         subprocess.check_call(cmd)
         return obj
 
-    with ThreadPoolExecutor(max_workers=min(9, os.cpu_count() or 4)) as ex:
+    with ThreadPoolExecutor(max_workers=min(10, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_unit, _units()))
     tmp = out + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"])

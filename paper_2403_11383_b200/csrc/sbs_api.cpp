@@ -97,6 +97,12 @@ struct sbs_ctx {
   cudaEvent_t blk_ev = nullptr;  // last H2D of h_blk (the host rewrites it only after this completed)
   bool ref_dirty = false;
   cudaGraphExec_t graph = nullptr;
+  // closed loop (sbs_run_loop): device words {iteration counter, counter at call start, arrival counter},
+  // pinned staging of the start value, and one captured iteration keyed by its arguments
+  uint32_t* d_loopw = nullptr;
+  uint32_t* h_loopw = nullptr;
+  cudaGraphExec_t loop_graph = nullptr;
+  std::vector<char> loop_key;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<char> ref_set;
   uint32_t iter = 0;
@@ -109,8 +115,8 @@ struct sbs_ctx {
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> free_events;
-  double kt[SBS_NKERNELS] = {0, 0, 0, 0};
-  int64_t kl[SBS_NKERNELS] = {0, 0, 0, 0};
+  double kt[SBS_NKERNELS] = {};
+  int64_t kl[SBS_NKERNELS] = {};
   // nccl
   nccl_comm_t comm = nullptr;
   bool external = false;  // world > 1 with an all-zero nccl_id: the caller exchanges the records
@@ -346,9 +352,11 @@ void sbs_destroy(sbs_ctx* c) {
                   (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart, (void*)c->d_sdiag, (void*)c->d_eJ, (void*)c->d_cand,
                   (void*)c->d_out})
     if (p) cudaFree(p);
-  if (c->h_in) cudaFreeHost(c->h_in);
-  if (c->h_out) cudaFreeHost(c->h_out);
+  if (c->h_out) cudaFreeHost(c->h_out);  // (h_in and h_xref point into h_blk)
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->loop_graph) cudaGraphExecDestroy(c->loop_graph);
+  if (c->d_loopw) cudaFree(c->d_loopw);
+  if (c->h_loopw) cudaFreeHost(c->h_loopw);
   if (c->h_blk) cudaFreeHost(c->h_blk);
   if (c->d_blk) cudaFree(c->d_blk);
   if (c->blk_ev) cudaEventDestroy(c->blk_ev);
@@ -361,6 +369,7 @@ void sbs_destroy(sbs_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
+  (void)cudaGetLastError();  // teardown errors (e.g. a context that failed half-way) must not leak into later launches
 }
 
 int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
@@ -418,6 +427,7 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.fz_min = cfg->fz_min;
   P.fz_max = cfg->fz_max;
   P.dt = cfg->dt;
+  P.duty = cfg->duty_factor;
   for (int a = 0; a < 12; ++a) {
     P.Q[a] = cfg->Q[a];
     P.Rw[a] = cfg->R[a];
@@ -760,6 +770,141 @@ int sbs_finish_records(sbs_ctx* c, const float* d_recs, const sbs_input* d_in, s
   const int rc = enqueue_finish(c, (cudaStream_t)stream, d_recs);
   if (rc == SBS_OK) c->iter += 1;
   return rc;
+}
+
+namespace {
+sbs::LoopArgs loop_args(const sbs_loop_config* lc, const sbs_command* d_cmd, const float* d_wrench,
+                        int32_t* d_fallen, float* d_trace) {
+  sbs::LoopArgs a;
+  memset(&a, 0, sizeof a);  // padding too: the struct is part of the loop graph's key
+  for (int k = 0; k < 12; ++k) a.hip[k] = lc->hip[k];
+  a.h_nom = lc->h_nom;
+  a.fall_angle = lc->fall_angle;
+  a.fall_height = lc->fall_height;
+  a.cmd = d_cmd;
+  a.wrench = d_wrench;
+  a.fallen = d_fallen;
+  a.trace = d_trace;
+  return a;
+}
+
+int check_loop_config(sbs_ctx* c, const sbs_loop_config* lc) {
+  if (!lc) return fail(c, SBS_ERR_INVALID_ARG, "NULL loop config");
+  if (!finite_all(lc->hip, 12) || !std::isfinite(lc->h_nom) || !(lc->fall_angle > 0) || !std::isfinite(lc->fall_height))
+    return fail(c, SBS_ERR_INVALID_ARG, "bad loop config");
+  return SBS_OK;
+}
+
+int upload_dirty_reference(sbs_ctx* c, cudaStream_t s) {
+  if (c->ref_dirty) {  // references staged by sbs_set_reference go up first, in stream order
+    CK(cudaMemcpyAsync(c->d_xref, c->h_xref, (size_t)c->P.R * c->P.H * 12 * sizeof(float), cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(c->blk_ev, s));
+    c->ref_dirty = false;
+  }
+  return SBS_OK;
+}
+}  // namespace
+
+int sbs_advance(sbs_ctx* c, sbs_input* d_in, const sbs_output* d_out, const sbs_command* d_cmd, const float* d_wrench,
+                int32_t* d_fallen, const sbs_loop_config* lc, void* stream) {
+  if (!c || !d_in || !d_out) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  int rc = check_loop_config(c, lc);
+  if (rc != SBS_OK) return rc;
+  CK(cudaSetDevice(c->cfg.device));
+  cudaStream_t s = (cudaStream_t)stream;
+  rc = upload_dirty_reference(c, s);  // keep the stream order of staged references before the rebuild
+  if (rc != SBS_OK) return rc;
+  const sbs::LoopArgs a = loop_args(lc, d_cmd, d_wrench, d_fallen, nullptr);
+  CK(timed(c, SBS_KERNEL_ADVANCE, s, [&] { return sbs::launch_advance(c->P, a, d_in, d_out, s); }));
+  std::fill(c->ref_set.begin(), c->ref_set.end(), 1);
+  return SBS_OK;
+}
+
+int sbs_run_loop(sbs_ctx* c, int32_t n_iter, sbs_input* d_in, sbs_output* d_out, const sbs_command* d_cmd,
+                 const float* d_wrench, int32_t* d_fallen, float* d_trace, const sbs_loop_config* lc, void* stream) {
+  if (!c || !d_in || !d_out || n_iter < 0) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument or n_iter < 0");
+  if (c->cfg.world != 1) return fail(c, SBS_ERR_STATE, "sbs_run_loop needs world = 1 (shard robots across contexts)");
+  int rc = check_loop_config(c, lc);
+  if (rc != SBS_OK) return rc;
+  for (int r = 0; r < c->P.R; ++r)
+    if (!c->ref_set[r]) return fail(c, SBS_ERR_STATE, "reference not set for every robot");
+  if (n_iter == 0) return SBS_OK;
+  CK(cudaSetDevice(c->cfg.device));
+  cudaStream_t s = (cudaStream_t)stream;
+  rc = upload_dirty_reference(c, s);
+  if (rc != SBS_OK) return rc;
+  if (!c->d_loopw) {
+    CK(cudaMalloc(&c->d_loopw, 4 * sizeof(uint32_t)));
+    CK(cudaMemset(c->d_loopw, 0, 4 * sizeof(uint32_t)));
+    CK(cudaMallocHost(&c->h_loopw, 2 * sizeof(uint32_t)));
+  }
+  // device iteration counter := iter (the step kernels read it; the advance kernel moves it)
+  CK(cudaEventSynchronize(c->blk_ev));  // h_loopw's previous upload has completed
+  c->h_loopw[0] = c->iter;
+  c->h_loopw[1] = c->iter;
+  CK(cudaMemcpyAsync(c->d_loopw, c->h_loopw, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(c->blk_ev, s));
+  sbs::LoopArgs a = loop_args(lc, d_cmd, d_wrench, d_fallen, d_trace);
+  a.loop = c->d_loopw;
+  a.counter = reinterpret_cast<int*>(c->d_loopw + 2);
+  auto enqueue_iter = [&](cudaStream_t st) -> int {
+    Params saved = c->P;
+    c->P.in = d_in;
+    c->P.out = d_out;
+    c->P.iter_dev = c->d_loopw;
+    int r2 = enqueue_step(c, st);
+    c->P = saved;
+    if (r2 != SBS_OK) return r2;
+    CK(timed(c, SBS_KERNEL_ADVANCE, st, [&] { return sbs::launch_advance(c->P, a, d_in, d_out, st); }));
+    return SBS_OK;
+  };
+  if (c->profile) {  // per-kernel events: no graph
+    for (int i = 0; i < n_iter; ++i) {
+      rc = enqueue_iter(s);
+      if (rc != SBS_OK) return rc;
+    }
+  } else {
+    std::vector<char> key(sizeof(a) + sizeof(d_in) + sizeof(d_out));
+    memcpy(key.data(), &a, sizeof(a));
+    memcpy(key.data() + sizeof(a), &d_in, sizeof(d_in));
+    memcpy(key.data() + sizeof(a) + sizeof(d_in), &d_out, sizeof(d_out));
+    if (!c->loop_graph || key != c->loop_key) {
+      if (c->loop_graph) {
+        CK(cudaGraphExecDestroy(c->loop_graph));
+        c->loop_graph = nullptr;
+      }
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      rc = enqueue_iter(c->stream);
+      const cudaError_t e = cudaStreamEndCapture(c->stream, &g);  // always leave capture mode
+      if (rc != SBS_OK) {
+        if (e == cudaSuccess) cudaGraphDestroy(g);
+        return rc;
+      }
+      CK(e);
+      const cudaError_t ei = cudaGraphInstantiate(&c->loop_graph, g, 0);
+      cudaGraphDestroy(g);
+      CK(ei);
+      c->loop_key = key;
+    }
+    for (int i = 0; i < n_iter; ++i) CK(cudaGraphLaunch(c->loop_graph, s));
+  }
+  c->iter += (uint32_t)n_iter;
+  return SBS_OK;
+}
+
+int sbs_get_reference(sbs_ctx* c, int32_t robot, float* x_ref) {
+  if (!c || !x_ref) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (robot < 0 || robot >= c->P.R) return fail(c, SBS_ERR_INVALID_ARG, "robot out of range");
+  const int n = c->P.H * 12;
+  if (c->ref_dirty) {  // staged on the host, not uploaded yet
+    memcpy(x_ref, c->h_xref + (size_t)robot * n, n * sizeof(float));
+    return SBS_OK;
+  }
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaDeviceSynchronize());  // the reference may be rebuilt on any caller stream
+  CK(cudaMemcpy(x_ref, c->d_xref + (size_t)robot * n, n * sizeof(float), cudaMemcpyDeviceToHost));
+  return SBS_OK;
 }
 
 int sbs_get_state(sbs_ctx* c, void* buf, uint64_t* nbytes) {

@@ -25,6 +25,7 @@ struct Params {
   int diag_inertia;
   float mu, fz_min, fz_max;
   float dt;
+  float duty;                 // duty factor D_f (closed-loop T_st = D_f / f_s)
   // --- cost ---
   float Q[12], Rw[12];
   float rho, f_nominal, w_fc, inv_lambda;
@@ -77,6 +78,19 @@ struct Params {
   float* cand;                // [R][world * n_elite] CEM world > 1: gathered candidate costs
   int ex_stride;              // floats per robot in a rank record (world > 1 exchange)
 };
+
+// closed loop (sbs_loop.cu)
+struct LoopArgs {
+  float hip[12];
+  float h_nom, fall_angle, fall_height;
+  const sbs_command* cmd;     // [R] or null (zero command)
+  const float* wrench;        // [n_iter][R][6] or null
+  int32_t* fallen;            // [R] or null
+  float* trace;               // [n_iter][R][SBS_TRACE_FLOATS] or null
+  uint32_t* loop;             // null, or device words {iteration counter (Params::iter_dev), counter at call start}
+  int* counter;               // arrival counter (re-armed to 0) of the advance kernel
+};
+cudaError_t launch_advance(const Params& p, const LoopArgs& a, sbs_input* in, const sbs_output* out, cudaStream_t s);
 
 // launchers (sbs_kernels.cu); return cudaGetLastError()
 // mode: SBS_MPPI / SBS_NAIVE (fused: merge + finish in the last CTA; else records only), SBS_CEM (records only)

@@ -1,2 +1,2 @@
-python scripts/profile_step.py --workload c3cem --steps 8 > gpurun_out/plain_c3.log 2>&1 && \
-ncu --set full --warp-sampling-interval 0 --clock-control none --import-source on -k regex:"sbs_cem" -s 5 -c 1 -o gpurun_out/prof_cem python scripts/profile_step.py --workload c3cem --steps 8 > gpurun_out/ncu_cem.log 2>&1; echo ncu rc=$?
+timeout 900 python -m pytest tests/test_gpu_loop.py tests/test_gpu_parity.py -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?; tail -5 gpurun_out/pytest_gpu.log
+grep -E "^E " gpurun_out/pytest_gpu.log | head -20
