@@ -225,6 +225,8 @@ typedef struct sbs_loop_config {
   float h_nom;            /* nominal CoM height of the rebuilt reference (L13) */
   float fall_angle;       /* rad (L40) */
   float fall_height;      /* m (L40) */
+  int32_t n_inner;        /* sbs_run_loop: SBS iterations per control step, 1..64 (Alg. 1 "multiple
+                             times"; L34): all on the same x0, warm shift on the first only */
 } sbs_loop_config;
 
 typedef struct sbs_command {  /* per robot, device */
@@ -242,12 +244,13 @@ typedef struct sbs_command {  /* per robot, device */
 int sbs_advance(sbs_ctx* ctx, sbs_input* d_in, const sbs_output* d_out, const sbs_command* d_cmd,
                 const float* d_wrench, int32_t* d_fallen, const sbs_loop_config* lc, void* stream);
 
-/* n_iter closed-loop iterations on the device: each is sbs_step_device(d_in,
- * d_out) then sbs_advance with wrench row i of d_wrench [n_iter][R][6] (or
+/* n_iter closed-loop control steps on the device: each is lc->n_inner x
+ * sbs_step_device(d_in, d_out) (the first with the warm shift, the others
+ * refining the same distribution at the same x0) then sbs_advance with wrench row i of d_wrench [n_iter][R][6] (or
  * NULL) and, if d_trace [n_iter][R][SBS_TRACE_FLOATS] is not NULL, trace row
  * i.  One iteration is captured once as a CUDA graph (the iteration counter
  * lives in device memory) and replayed n_iter times.  world = 1 only.
- * iter += n_iter.  Stream-ordered. */
+ * iter += n_iter * n_inner.  Stream-ordered. */
 int sbs_run_loop(sbs_ctx* ctx, int32_t n_iter, sbs_input* d_in, sbs_output* d_out, const sbs_command* d_cmd,
                  const float* d_wrench, int32_t* d_fallen, float* d_trace, const sbs_loop_config* lc,
                  void* stream);

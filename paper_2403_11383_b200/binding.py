@@ -56,7 +56,7 @@ class sbs_output(C.Structure):
 
 class sbs_loop_config(C.Structure):
     _fields_ = [("hip", C.c_float * 12), ("h_nom", C.c_float), ("fall_angle", C.c_float),
-                ("fall_height", C.c_float)]
+                ("fall_height", C.c_float), ("n_inner", C.c_int32)]
 
 
 class sbs_command(C.Structure):
@@ -70,6 +70,7 @@ def make_loop_config(lc: dict) -> sbs_loop_config:
     o = sbs_loop_config()
     o.hip[:] = [float(v) for v in np.asarray(lc["hip"], dtype=np.float64).reshape(12)]
     o.h_nom, o.fall_angle, o.fall_height = float(lc["h_nom"]), float(lc["fall_angle"]), float(lc["fall_height"])
+    o.n_inner = int(lc.get("n_inner", 1))
     return o
 
 

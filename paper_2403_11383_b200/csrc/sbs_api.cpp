@@ -781,6 +781,7 @@ sbs::LoopArgs loop_args(const sbs_loop_config* lc, const sbs_command* d_cmd, con
   a.h_nom = lc->h_nom;
   a.fall_angle = lc->fall_angle;
   a.fall_height = lc->fall_height;
+  a.n_inner = lc->n_inner;
   a.cmd = d_cmd;
   a.wrench = d_wrench;
   a.fallen = d_fallen;
@@ -790,7 +791,8 @@ sbs::LoopArgs loop_args(const sbs_loop_config* lc, const sbs_command* d_cmd, con
 
 int check_loop_config(sbs_ctx* c, const sbs_loop_config* lc) {
   if (!lc) return fail(c, SBS_ERR_INVALID_ARG, "NULL loop config");
-  if (!finite_all(lc->hip, 12) || !std::isfinite(lc->h_nom) || !(lc->fall_angle > 0) || !std::isfinite(lc->fall_height))
+  if (!finite_all(lc->hip, 12) || !std::isfinite(lc->h_nom) || !(lc->fall_angle > 0) || !std::isfinite(lc->fall_height) ||
+      lc->n_inner < 1 || lc->n_inner > 64)
     return fail(c, SBS_ERR_INVALID_ARG, "bad loop config");
   return SBS_OK;
 }
@@ -848,13 +850,17 @@ int sbs_run_loop(sbs_ctx* c, int32_t n_iter, sbs_input* d_in, sbs_output* d_out,
   a.loop = c->d_loopw;
   a.counter = reinterpret_cast<int*>(c->d_loopw + 2);
   auto enqueue_iter = [&](cudaStream_t st) -> int {
-    Params saved = c->P;
-    c->P.in = d_in;
-    c->P.out = d_out;
-    c->P.iter_dev = c->d_loopw;
-    int r2 = enqueue_step(c, st);
-    c->P = saved;
-    if (r2 != SBS_OK) return r2;
+    for (int k = 0; k < lc->n_inner; ++k) {  // n_inner SBS iterations on the same x0 (warm shift on the first only)
+      Params saved = c->P;
+      c->P.in = d_in;
+      c->P.out = d_out;
+      c->P.iter_dev = c->d_loopw;
+      c->P.iter_add = (uint32_t)k;
+      if (k > 0) c->P.warm_shift = 0;
+      int r2 = enqueue_step(c, st);
+      c->P = saved;
+      if (r2 != SBS_OK) return r2;
+    }
     CK(timed(c, SBS_KERNEL_ADVANCE, st, [&] { return sbs::launch_advance(c->P, a, d_in, d_out, st); }));
     return SBS_OK;
   };
@@ -889,7 +895,7 @@ int sbs_run_loop(sbs_ctx* c, int32_t n_iter, sbs_input* d_in, sbs_output* d_out,
     }
     for (int i = 0; i < n_iter; ++i) CK(cudaGraphLaunch(c->loop_graph, s));
   }
-  c->iter += (uint32_t)n_iter;
+  c->iter += (uint32_t)n_iter * (uint32_t)lc->n_inner;
   return SBS_OK;
 }
 

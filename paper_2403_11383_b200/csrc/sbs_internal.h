@@ -49,7 +49,8 @@ struct Params {
   uint32_t seed_lo, seed_hi;
   uint32_t rk[10][2];         // Philox round keys (seed_lo + r 0x9E3779B9, seed_hi + r 0xBB67AE85)
   uint32_t iter;
-  const uint32_t* iter_dev;   // non-null: read the iteration counter from device memory (graph replay)
+  const uint32_t* iter_dev;   // non-null: read the iteration counter from device memory (graph replay) ...
+  uint32_t iter_add;          // ... plus this offset (inner iterations of a closed-loop control step)
   int robot_offset;
   // --- sizes / sharding ---
   int R;
@@ -88,6 +89,7 @@ struct LoopArgs {
   int32_t* fallen;            // [R] or null
   float* trace;               // [n_iter][R][SBS_TRACE_FLOATS] or null
   uint32_t* loop;             // null, or device words {iteration counter (Params::iter_dev), counter at call start}
+  int n_inner;                // SBS iterations per control step (the advance moves the counter by n_inner)
   int* counter;               // arrival counter (re-armed to 0) of the advance kernel
 };
 cudaError_t launch_advance(const Params& p, const LoopArgs& a, sbs_input* in, const sbs_output* out, cudaStream_t s);

@@ -41,7 +41,7 @@ struct RobotSmem {
 
 // iteration counter: kernel parameter, or device memory when the step runs as a
 // captured CUDA graph (the host writes it with the inputs every step)
-__device__ __forceinline__ uint32_t step_iter(const Params& p) { return p.iter_dev ? *p.iter_dev : p.iter; }
+__device__ __forceinline__ uint32_t step_iter(const Params& p) { return p.iter_dev ? *p.iter_dev + p.iter_add : p.iter; }
 
 // state-vector index in the kernel's pair order for each index of x = (p, v, Phi, w)
 __device__ __forceinline__ int xref_slot(int a) { return a == 2 ? 4 : (a == 3 ? 2 : (a == 4 ? 3 : a)); }

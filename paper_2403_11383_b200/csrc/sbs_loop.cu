@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(128) sbs_advance_kernel(const __grid_constant_
                                                           sbs_input* in, const sbs_output* out) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < p.R) {
-    const uint32_t it = a.loop ? __ldcg(a.loop) - __ldcg(a.loop + 1) : 0u;  // iteration within this call
+    const uint32_t it = a.loop ? (__ldcg(a.loop) - __ldcg(a.loop + 1)) / (uint32_t)a.n_inner : 0u;  // control step
     sbs_input s = in[r];
     const sbs_output& o = out[r];
     const bool was_fallen = a.fallen && a.fallen[r];
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(128) sbs_advance_kernel(const __grid_constant_
       s_last = atomicAdd(a.counter, 1) == (int)gridDim.x - 1;
       if (s_last) {
         *a.counter = 0;
-        a.loop[0] += 1u;
+        a.loop[0] += (uint32_t)a.n_inner;
       }
     }
   }

@@ -221,3 +221,44 @@ def test_closed_loop_iterations_match_oracle_along_the_gpu_trajectory(B, orc):
             np.testing.assert_array_equal(gnext[r]["feet_cur"], ra.feet_cur.astype(np.float32))
             assert _close(c.get_reference(r), ra.xref)
     assert c.iter == n and int(fallen.sum()) == 0
+
+
+def test_inner_iterations_match_oracle(B, orc):
+    """n_inner = 3 SBS iterations per control step (Alg. 1 "multiple times"; L34):
+    the first with the warm shift, the others refining the same distribution at the same
+    x0 with fresh noise (iteration counter + 1 each), then one advance."""
+    import torch
+    R, inner = 2, 3
+    cfg = W.base_config(n_samples=300, mode="mppi", n_robots=R)
+    inputs = [W.robot_input(cfg, r, cmd=(0.2, 0.1, 0), phase=W.q32(0.3 * r)) for r in range(R)]
+    lc = dict(W.loop_config(), n_inner=inner)
+    cmd_np = np.tile(np.array([0.2, 0.1, 0.0, 0.0], dtype=np.float32), (R, 1))
+    c = B.Controller(cfg)
+    for r, inp in enumerate(inputs):
+        c.set_reference(r, inp["xref"])
+    d_in = _dev_bytes(B.make_inputs(inputs))
+    d_out = torch.zeros(R * C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+    cmd = torch.from_numpy(cmd_np).cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    for step in range(3):
+        gin = _inputs_of(B, d_in, R)
+        states = []
+        for r in range(R):
+            m, v, f = c.get_distribution(r)
+            states.append(dict(mean=m.astype(np.float64), var=v.astype(np.float64), freq_idx=f, iter=c.iter))
+            gin[r]["xref"] = c.get_reference(r).astype(np.float64)
+        c.run_loop(1, d_in.data_ptr(), d_out.data_ptr(), cmd.data_ptr(), 0, 0, 0, lc, s)
+        torch.cuda.synchronize()
+        assert c.iter == inner * (step + 1)
+        outs = _outputs_of(B, d_out, R, 48)
+        gnext = _inputs_of(B, d_in, R)
+        for r in range(R):
+            st = states[r]
+            for k in range(inner):
+                ro = orc.step(cfg if k == 0 else dict(cfg, warm_shift=0), r, gin[r], st, keep=False)
+            o = outs[r]
+            assert np.max(np.abs(o["mean"] - ro.mean)) <= 1e-4 * max(np.max(np.abs(ro.mean)), 1.0)
+            assert np.max(np.abs(o["u0"] - ro.u0)) <= 1e-4 * max(np.max(np.abs(ro.u0)), 1.0)
+            ra = orc.advance(cfg, lc, gin[r], o["u0"], o["contact0"], o["freq_idx"], cmd_np[r, :3], 0.0)
+            assert gnext[r]["phase"] == ra.phase
+            assert _close(gnext[r]["x0"], ra.x0)
