@@ -112,6 +112,11 @@ typedef struct sbs_config {
   uint8_t nccl_id[128];   /* ncclUniqueId (sbs_nccl_unique_id on rank 0) when world > 1; all zero:
                              the caller exchanges the rank records (sbs_step_records).  CEM with
                              world > 1 needs n_elite <= n_samples / world. */
+  /* multiple Gaussians ("we sample from multiple Gaussian distributions"; L41): sample k
+     draws theta2 = mu' + sigma_scale[k mod n_sigma_groups] * sigma * z (elite-preserved sample 0
+     excepted).  n_sigma_groups 0 or 1: one Gaussian (sigma_scale ignored); at most 8; scales >= 0. */
+  int32_t n_sigma_groups;
+  float sigma_scale[8];
 } sbs_config;
 
 /* Per-robot input of one iteration (host for sbs_step, device for sbs_step_device). */

@@ -48,6 +48,7 @@ class OrcConfig(C.Structure):
         ("n_samples", C.c_int64), ("n_elite", C.c_int64), ("lambda_", C.c_double),
         ("sigma", C.c_double * 3), ("sigma_min_frac", C.c_double),
         ("warm_shift", C.c_int32), ("_pad", C.c_int32), ("seed", C.c_uint64),
+        ("n_sigma_groups", C.c_int32), ("_pad2", C.c_int32), ("sigma_scale", C.c_double * 8),
     ]
 
 
@@ -125,6 +126,9 @@ def make_config(cfg: dict) -> OrcConfig:
     c.sigma_min_frac = cfg["sigma_min_frac"]
     c.warm_shift = int(cfg["warm_shift"])
     c.seed = cfg["seed"]
+    sc = list(cfg.get("sigma_scale", [1.0]))
+    c.n_sigma_groups = len(sc)
+    c.sigma_scale[:len(sc)] = [float(v) for v in sc]
     return c
 
 

@@ -183,7 +183,9 @@ void orc_sample(const orc_config* c, const double* mu_shift, const double* var,
     orc_philox4x32_10(ctr, key, w);
     orc_normal4(w, &z[4 * q]);
   }
-  for (int64_t d = 0; d < D; ++d) theta[d] = mu_shift[d] + sqrt(var[d]) * (double)z[d];
+  /* L41: interleaved groups of samples with std scaled by sigma_scale[g] */
+  const double sc = c->n_sigma_groups > 1 ? c->sigma_scale[k % c->n_sigma_groups] : 1.0;
+  for (int64_t d = 0; d < D; ++d) theta[d] = mu_shift[d] + sc * sqrt(var[d]) * (double)z[d];
   if (c->gait_adapt) {
     uint32_t ctr[4] = {0x80000000u, (uint32_t)k, iter, robot}, w[4];
     orc_philox4x32_10(ctr, key, w);

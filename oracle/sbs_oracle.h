@@ -50,6 +50,9 @@ typedef struct orc_config {
   double sigma[3], sigma_min_frac;
   int32_t warm_shift, _pad;
   uint64_t seed;
+  /* multiple Gaussians: sample k draws with std sigma_scale[k mod n_sigma_groups] * sigma */
+  int32_t n_sigma_groups, _pad2;
+  double sigma_scale[8];
 } orc_config;
 
 typedef struct orc_diag {

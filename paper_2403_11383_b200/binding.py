@@ -39,6 +39,7 @@ class sbs_config(C.Structure):
         ("warm_shift", C.c_int32), ("seed", C.c_uint64),
         ("n_robots", C.c_int32), ("robot_offset", C.c_int32), ("device", C.c_int32),
         ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_uint8 * 128),
+        ("n_sigma_groups", C.c_int32), ("sigma_scale", C.c_float * 8),
     ]
 
 
@@ -175,6 +176,9 @@ def make_config(cfg: dict, device: int = 0, rank: int = 0, world: int = 1, nccl_
     c.device, c.rank, c.world = device, rank, world
     if nccl_id is not None:
         c.nccl_id[:] = list(nccl_id)
+    sc = list(cfg.get("sigma_scale", [1.0]))
+    c.n_sigma_groups = len(sc)
+    c.sigma_scale[:len(sc)] = [float(v) for v in sc]
     return c
 
 

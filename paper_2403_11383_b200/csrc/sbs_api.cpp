@@ -213,6 +213,9 @@ int validate(const sbs_config* c, std::string& why) {
   for (int a = 0; a < 3; ++a)
     if (!(c->sigma[a] > 0)) return bad("sigma must be > 0");
   if (!(c->sigma_min_frac >= 0)) return bad("sigma_min_frac must be >= 0");
+  if (c->n_sigma_groups < 0 || c->n_sigma_groups > 8) return bad("n_sigma_groups must be in [0, 8]");
+  for (int g = 0; g < c->n_sigma_groups; ++g)
+    if (!(c->sigma_scale[g] >= 0) || !std::isfinite(c->sigma_scale[g])) return bad("sigma_scale must be finite, >= 0");
   if (c->n_robots < 1) return bad("n_robots must be >= 1");
   if (c->robot_offset < 0) return bad("robot_offset must be >= 0");
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad("bad rank / world");
@@ -472,6 +475,8 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
     const double s = (double)cfg->sigma_min_frac * (double)cfg->sigma[a];
     P.var_floor[a] = (float)(s * s);
   }
+  P.n_sig_groups = cfg->n_sigma_groups > 1 ? cfg->n_sigma_groups : 1;
+  for (int g = 0; g < 8; ++g) P.sig_scale[g] = g < cfg->n_sigma_groups ? cfg->sigma_scale[g] : 1.0f;
   P.seed_lo = (uint32_t)(cfg->seed & 0xFFFFFFFFull);
   P.seed_hi = (uint32_t)(cfg->seed >> 32);
   for (int r = 0; r < 10; ++r) {

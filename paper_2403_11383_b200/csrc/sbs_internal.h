@@ -45,6 +45,8 @@ struct Params {
   int mode;
   int64_t n_elite;
   float var_floor[3];
+  int n_sig_groups;           // multiple Gaussians (L41): sample k uses sig_scale[k mod n_sig_groups]
+  float sig_scale[8];
   // --- noise ---
   uint32_t seed_lo, seed_hi;
   uint32_t rk[10][2];         // Philox round keys (seed_lo + r 0x9E3779B9, seed_hi + r 0xBB67AE85)

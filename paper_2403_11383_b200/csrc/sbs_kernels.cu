@@ -132,6 +132,8 @@ __device__ __forceinline__ int draw_sample(const Params& p, uint32_t robot_g, in
     return s.cur_idx;
   }
   const uint32_t kk = (uint32_t)k;
+  const bool grp = p.n_sig_groups > 1;  // uniform per launch
+  const float sc = grp ? p.sig_scale[(int)(k % p.n_sig_groups)] : 1.0f;
 #pragma unroll
   for (int q = 0; q < D / 4; ++q) {
     const U4 w = philox4x32_10_rk((uint32_t)q, kk, s.iter, robot_g, p.rk);
@@ -140,7 +142,8 @@ __device__ __forceinline__ int draw_sample(const Params& p, uint32_t robot_g, in
     box_muller(w.z, w.w, z[2], z[3]);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      theta_set(th, 4 * q + i, __fmaf_rn(s.sig[4 * q + i], z[i], s.mu[4 * q + i]));
+      const float sg = grp ? __fmul_rn(s.sig[4 * q + i], sc) : s.sig[4 * q + i];
+      theta_set(th, 4 * q + i, __fmaf_rn(sg, z[i], s.mu[4 * q + i]));
       if (WITH_Z) z_out[4 * q + i] = z[i];
     }
   }
@@ -165,8 +168,11 @@ __device__ __forceinline__ void sample_block(const Params& p, uint32_t robot_g, 
   float z[4];
   box_muller(w.x, w.y, z[0], z[1]);
   box_muller(w.z, w.w, z[2], z[3]);
+  const bool grp = p.n_sig_groups > 1;
+  const float sc = grp ? p.sig_scale[(int)(k % p.n_sig_groups)] : 1.0f;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) th4[i] = __fmaf_rn(s.sig[4 * q + i], z[i], s.mu[4 * q + i]);
+  for (int i = 0; i < 4; ++i)
+    th4[i] = __fmaf_rn(grp ? __fmul_rn(s.sig[4 * q + i], sc) : s.sig[4 * q + i], z[i], s.mu[4 * q + i]);
 }
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }

@@ -40,7 +40,7 @@ def base_config(**kw) -> dict:
         mode="mppi", n_samples=10000, n_elite=1, **{"lambda": 1.0},
         sigma=[8.0, 8.0, 15.0], sigma_min_frac=0.1,
         elite_preserve=1, warm_shift=1, seed=SEED,
-        n_robots=1,
+        n_robots=1, sigma_scale=[1.0],
     )
     cfg.update(kw)
     return round_config(cfg)

@@ -159,6 +159,22 @@ def test_knot_and_horizon_variants(B, orc, P, H):
     _run_pair(B, orc, cfg, inputs)
 
 
+@pytest.mark.parametrize("mode,scales", [("naive", [0.5, 1.0, 2.0]), ("mppi", [1.0, 0.25]), ("cem", [2.0, 1.0, 0.0])])
+def test_multiple_gaussians(B, orc, mode, scales):
+    """Naive's multiple Gaussian distributions (L41): sample k uses sigma_scale[k mod G]."""
+    cfg = W.base_config(n_samples=900, mode=mode, n_elite=90 if mode == "cem" else 1, gait_adapt=1,
+                        sigma_scale=scales)
+    inputs = [W.robot_input(cfg, 0, cmd=(0.2, 0.1, 0.0), phase=W.q32(0.4))]
+    st = W.initial_distribution(cfg)
+    c = _ctrl(B, cfg, inputs, st)
+    z, th, f = c.debug_samples(0, 0, 900)
+    r = orc.step(cfg, 0, inputs[0], dict(st))
+    np.testing.assert_array_equal(z.view(np.uint32), r.z.view(np.uint32))
+    mu_s = orc.warm_shift(cfg, st["mean"])
+    assert np.all(np.abs(th - r.theta) <= 1e-6 * (np.abs(r.theta) + np.abs(mu_s)[None, :] + 1.0))
+    _run_pair(B, orc, cfg, inputs, n_steps=2)
+
+
 def test_full_inertia_and_no_warm_shift(B, orc):
     cfg = W.base_config(n_samples=500, inertia=[0.135, 0.01, -0.02, 0.01, 0.54, 0.03, -0.02, 0.03, 0.58],
                         warm_shift=0, elite_preserve=0, duty_factor=1.0)

@@ -118,3 +118,43 @@ def test_theta1_uniform_chi2(orc):
         counts[idx] += 1
     chi2 = ((counts - 2000) ** 2 / 2000).sum()
     assert stats.chi2.sf(chi2, 2) > 1e-3, counts
+
+
+# ---------------------------------------------------------------------------
+# multiple Gaussians (DESIGN L41)
+# ---------------------------------------------------------------------------
+def test_multiple_gaussians_group_structure(orc):
+    """Sample k draws with std sigma_scale[k mod G]: the same z as the one-Gaussian draw,
+    a zero scale reproduces mu' exactly, a scale s multiplies theta - mu' by s."""
+    from paper_2403_11383_b200 import workloads as W
+    base = W.base_config(n_samples=64)
+    st = W.initial_distribution(base)
+    mu_s = orc.warm_shift(base, st["mean"])
+    for k in range(1, 40):
+        th1, z1, _ = orc.sample(base, mu_s, st["var"], 0, 3, 0, k)
+        th, z, _ = orc.sample(dict(base, sigma_scale=[1.0, 0.0, 2.0]), mu_s, st["var"], 0, 3, 0, k)
+        np.testing.assert_array_equal(z, z1)
+        g = k % 3
+        if g == 0:
+            np.testing.assert_array_equal(th, th1)
+        elif g == 1:
+            np.testing.assert_array_equal(th, mu_s)
+        else:
+            np.testing.assert_allclose(th - mu_s, 2.0 * (th1 - mu_s), rtol=1e-15, atol=1e-12)
+    # elite preservation is unaffected
+    th0, _, _ = orc.sample(dict(base, sigma_scale=[3.0, 0.5]), mu_s, st["var"], 0, 3, 0, 0)
+    np.testing.assert_array_equal(th0, mu_s)
+
+
+def test_multiple_gaussians_group_variances(orc):
+    from paper_2403_11383_b200 import workloads as W
+    cfg = W.base_config(n_samples=64, sigma_scale=[0.5, 1.0, 2.0], elite_preserve=0)
+    st = W.initial_distribution(cfg)
+    mu_s = orc.warm_shift(cfg, st["mean"])
+    dev = {0: [], 1: [], 2: []}
+    for k in range(3000):
+        th, _, _ = orc.sample(cfg, mu_s, st["var"], 0, 0, 0, k)
+        dev[k % 3].append((th - mu_s) / np.sqrt(st["var"]))
+    for g, s in enumerate([0.5, 1.0, 2.0]):
+        v = np.var(np.array(dev[g]))                 # 1000 x 48 standardised deviations
+        assert abs(v / s ** 2 - 1.0) < 0.05
