@@ -49,6 +49,7 @@ class OrcConfig(C.Structure):
         ("sigma", C.c_double * 3), ("sigma_min_frac", C.c_double),
         ("warm_shift", C.c_int32), ("_pad", C.c_int32), ("seed", C.c_uint64),
         ("n_sigma_groups", C.c_int32), ("_pad2", C.c_int32), ("sigma_scale", C.c_double * 8),
+        ("full_cov", C.c_int32), ("_pad3", C.c_int32),
     ]
 
 
@@ -59,7 +60,7 @@ class OrcDiag(C.Structure):
 
 class OrcState(C.Structure):
     _fields_ = [("mean", C.c_double * MAX_D), ("var", C.c_double * MAX_D),
-                ("freq_idx", C.c_int32), ("iter", C.c_uint32)]
+                ("freq_idx", C.c_int32), ("iter", C.c_uint32), ("chol", C.c_double * (MAX_D * MAX_D))]
 
 
 class OrcOutput(C.Structure):
@@ -129,6 +130,7 @@ def make_config(cfg: dict) -> OrcConfig:
     sc = list(cfg.get("sigma_scale", [1.0]))
     c.n_sigma_groups = len(sc)
     c.sigma_scale[:len(sc)] = [float(v) for v in sc]
+    c.full_cov = int(cfg.get("full_cov", 0))
     return c
 
 
@@ -189,6 +191,11 @@ class Oracle:
         L.orc_step.argtypes = [cfgp, C.c_uint32, dp, C.c_uint32, dp, dp, dp,
                                C.POINTER(OrcState), C.POINTER(OrcOutput), dp, i32p, dp,
                                C.POINTER(C.c_float), C.POINTER(C.c_int64)]
+        L.orc_cholesky.argtypes = [C.c_int32, dp, dp]
+        L.orc_sample_full.argtypes = [cfgp, dp, dp, C.c_int32, C.c_uint32, C.c_uint32, C.c_int64,
+                                      dp, C.POINTER(C.c_float), i32p]
+        L.orc_cem_update_full.argtypes = [C.c_int64, C.c_int32, dp, dp, C.c_int64, dp, dp, dp, dp,
+                                          C.POINTER(C.c_int64), C.POINTER(OrcDiag)]
         L.orc_foothold.argtypes = [dp, dp, dp, C.c_double, C.c_double, C.c_double, dp]
         L.orc_plant_dynamics.argtypes = [cfgp, dp, dp, i32p, dp, dp, dp]
         L.orc_plant_step.argtypes = [cfgp, dp, dp, i32p, dp, dp, C.c_double, dp]
@@ -340,6 +347,8 @@ class Oracle:
         st.var[:D] = list(np.asarray(state["var"], dtype=np.float64))
         st.freq_idx = int(state["freq_idx"])
         st.iter = int(state["iter"])
+        if cfg.get("full_cov", 0):
+            st.chol[:D * D] = [float(v) for v in np.asarray(state["chol"], dtype=np.float64).reshape(D * D)]
         out = OrcOutput()
         J = np.zeros(K) if keep else None
         fidx = np.zeros(K, dtype=np.int32) if keep else None
@@ -358,6 +367,8 @@ class Oracle:
         state["var"] = np.array(st.var[:D])
         state["freq_idx"] = st.freq_idx
         state["iter"] = st.iter
+        if cfg.get("full_cov", 0):
+            state["chol"] = np.array(st.chol[:D * D]).reshape(D, D)
         dg = out.diag
         return StepResult(status=rc, mean=state["mean"].copy(), var=state["var"].copy(),
                           freq_idx=out.freq_idx, freq_hz=out.freq_hz, u0=np.array(out.u0),
@@ -408,3 +419,34 @@ class Oracle:
             _dp(_f64(u0, 12)), ct.ctypes.data_as(C.POINTER(C.c_int32)), int(freq_idx), _dp(_f64(v_d, 3)),
             float(yaw_rate), _dp(w), _dp(x), C.byref(ph), _dp(fc), _dp(fn), _dp(xr))
         return AdvanceResult(fallen=int(fallen), x0=x, phase=int(ph.value), feet_cur=fc, feet_next=fn, xref=xr)
+
+    # ---- full covariance (f3; L42) ---------------------------------------
+    def cholesky(self, Cm):
+        Cm = _f64(Cm)
+        D = int(round(np.sqrt(Cm.size)))
+        Lm = np.zeros((D, D))
+        rc = self.lib.orc_cholesky(D, _dp(Cm), _dp(Lm))
+        return rc, Lm
+
+    def sample_full(self, cfg, mu_shift, Lm, cur_idx, it, robot, k):
+        D = 12 * cfg["knots"]
+        th = np.zeros(D)
+        z = np.zeros(D, dtype=np.float32)
+        idx = C.c_int32(0)
+        self.lib.orc_sample_full(C.byref(make_config(cfg)), _dp(_f64(mu_shift, D)), _dp(_f64(Lm, D * D)),
+                                 int(cur_idx), int(it) & 0xFFFFFFFF, int(robot), int(k), _dp(th),
+                                 z.ctypes.data_as(C.POINTER(C.c_float)), C.byref(idx))
+        return th, z, idx.value
+
+    def cem_update_full(self, J, theta, K_e, var_floor):
+        J = _f64(J)
+        th = _f64(theta)
+        K = J.size
+        D = th.size // K
+        mu = np.zeros(D)
+        Cn, Ln = np.zeros((D, D)), np.zeros((D, D))
+        e = np.zeros(int(K_e), dtype=np.int64)
+        dg = OrcDiag()
+        rc = self.lib.orc_cem_update_full(K, D, _dp(J), _dp(th), int(K_e), _dp(_f64(var_floor, D)), _dp(mu),
+                                          _dp(Cn), _dp(Ln), e.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(dg))
+        return rc, mu, Cn, Ln, e, dg

@@ -551,6 +551,62 @@ int orc_cem_update(int64_t K, int32_t D, const double* J, const double* theta,
 }
 
 /* ======================================================================
+ * f3 (L42): CEM with a full covariance C = L L^T (Alg. 1 UpdateCov).
+ * Sampling theta2 = mu' + L z (z the same normative noise); the elite
+ * covariance (1/n) sum (theta - mu_new)(theta - mu_new)^T plus the diagonal
+ * floor diag((sigma_min_frac sigma_axis)^2) (keeps C positive definite for any
+ * K_e); L = Cholesky factor (Cholesky-Banachiewicz, textbook order).
+ * ==================================================================== */
+int orc_cholesky(int32_t D, const double* C, double* L) {
+  for (int32_t i = 0; i < D; ++i)
+    for (int32_t j = 0; j < D; ++j) L[i * D + j] = 0.0;
+  for (int32_t i = 0; i < D; ++i) {
+    for (int32_t j = 0; j <= i; ++j) {
+      double s = C[i * D + j];
+      for (int32_t k = 0; k < j; ++k) s -= L[i * D + k] * L[j * D + k];
+      if (i == j) {
+        if (!(s > 0.0)) return -1;
+        L[i * D + i] = sqrt(s);
+      } else {
+        L[i * D + j] = s / L[j * D + j];
+      }
+    }
+  }
+  return 0;
+}
+
+void orc_sample_full(const orc_config* c, const double* mu_shift, const double* L, int32_t cur_idx,
+                     uint32_t iter, uint32_t robot, int64_t k, double* theta, float* z, int32_t* idx) {
+  const int64_t D = orc_D(c);
+  double dummy_var[ORC_MAX_D] = {0};
+  orc_sample(c, mu_shift, dummy_var, cur_idx, iter, robot, k, theta, z, idx); /* z, theta1; theta2 = mu' */
+  if (c->elite_preserve && k == 0) return;
+  for (int64_t i = 0; i < D; ++i) {
+    double s = 0.0;
+    for (int64_t j = 0; j <= i; ++j) s += L[i * D + j] * (double)z[j];
+    theta[i] = mu_shift[i] + s;
+  }
+}
+
+int orc_cem_update_full(int64_t K, int32_t D, const double* J, const double* theta, int64_t K_e,
+                        const double* var_floor, double* mu_new, double* C_new, double* L_new,
+                        int64_t* elite, orc_diag* dg) {
+  double var_dummy[ORC_MAX_D];
+  int rc = orc_cem_update(K, D, J, theta, K_e, var_floor, 0, mu_new, var_dummy, elite, dg);
+  if (rc != ORC_OK) return rc;
+  int64_t n_fin = K - dg->n_diverged;
+  int64_t ne = K_e < n_fin ? K_e : n_fin;
+  for (int32_t i = 0; i < D; ++i)
+    for (int32_t j = 0; j < D; ++j) {
+      double s = 0.0;
+      for (int64_t e = 0; e < ne; ++e)
+        s += (theta[elite[e] * D + i] - mu_new[i]) * (theta[elite[e] * D + j] - mu_new[j]);
+      C_new[i * D + j] = s / (double)ne + (i == j ? var_floor[i] : 0.0);
+    }
+  return orc_cholesky(D, C_new, L_new) == 0 ? ORC_OK : ORC_ERR_INVALID_ARG;
+}
+
+/* ======================================================================
  * Alg. 5: one iteration of the SBS predictive controller.
  *   sample K thetas  ->  J_k = Rollout(theta_k, x0)  ->  update  ->  output
  * Output: u0 = mask(delta_0) proj(mean_new at t = 0).
@@ -575,7 +631,8 @@ int orc_step(const orc_config* c, uint32_t robot, const double x0[12], uint32_t 
   int32_t* fidx = (int32_t*)malloc(sizeof(int32_t) * (size_t)K);
   float z[ORC_MAX_D];
   for (int64_t k = 0; k < K; ++k) {
-    orc_sample(c, mu_shift, st->var, st->freq_idx, st->iter, robot, k, &theta[k * D], z, &fidx[k]);
+    if (c->full_cov) orc_sample_full(c, mu_shift, st->chol, st->freq_idx, st->iter, robot, k, &theta[k * D], z, &fidx[k]);
+    else orc_sample(c, mu_shift, st->var, st->freq_idx, st->iter, robot, k, &theta[k * D], z, &fidx[k]);
     if (z_out) memcpy(&z_out[k * D], z, sizeof(float) * (size_t)D);
     J[k] = orc_rollout(c, x0, phase0, feet_cur, feet_next, xref, &theta[k * D], fidx[k], NULL);
   }
@@ -595,7 +652,19 @@ int orc_step(const orc_config* c, uint32_t robot, const double x0[12], uint32_t 
       floor_[d] = s * s;
     }
     int64_t* elite = (int64_t*)malloc(sizeof(int64_t) * (size_t)Ke);
-    rc = orc_cem_update(K, (int32_t)D, J, theta, Ke, floor_, c->mode == ORC_CEM, mu_new, var_new, elite, &out->diag);
+    if (c->full_cov && c->mode == ORC_CEM) {
+      double* Cn = (double*)malloc(sizeof(double) * (size_t)(D * D));
+      double* Ln = (double*)malloc(sizeof(double) * (size_t)(D * D));
+      rc = orc_cem_update_full(K, (int32_t)D, J, theta, Ke, floor_, mu_new, Cn, Ln, elite, &out->diag);
+      if (rc == ORC_OK) {
+        for (int64_t d = 0; d < D; ++d) var_new[d] = Cn[d * D + d];
+        memcpy(st->chol, Ln, sizeof(double) * (size_t)(D * D));
+      }
+      free(Cn);
+      free(Ln);
+    } else {
+      rc = orc_cem_update(K, (int32_t)D, J, theta, Ke, floor_, c->mode == ORC_CEM, mu_new, var_new, elite, &out->diag);
+    }
     if (elite_out && rc >= 0) memcpy(elite_out, elite, sizeof(int64_t) * (size_t)Ke);
     argmin = elite[0];
     free(elite);

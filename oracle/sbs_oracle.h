@@ -53,6 +53,8 @@ typedef struct orc_config {
   /* multiple Gaussians: sample k draws with std sigma_scale[k mod n_sigma_groups] * sigma */
   int32_t n_sigma_groups, _pad2;
   double sigma_scale[8];
+  /* full-covariance CEM (Alg. 1 UpdateCov with a full C; L42) */
+  int32_t full_cov, _pad3;
 } orc_config;
 
 typedef struct orc_diag {
@@ -106,11 +108,21 @@ int orc_cem_update(int64_t K, int32_t D, const double* J, const double* theta,
                    int64_t K_e, const double* var_floor, int32_t update_var,
                    double* mu_new, double* var_new, int64_t* elite, orc_diag* dg);
 
+/* ---- full covariance (f3; L42) ---- */
+int orc_cholesky(int32_t D, const double* C /*[D][D]*/, double* L /*[D][D], lower*/);
+void orc_sample_full(const orc_config* c, const double* mu_shift, const double* L /*[D][D]*/,
+                     int32_t cur_idx, uint32_t iter, uint32_t robot, int64_t k,
+                     double* theta, float* z, int32_t* idx);
+int orc_cem_update_full(int64_t K, int32_t D, const double* J, const double* theta, int64_t K_e,
+                        const double* var_floor, double* mu_new, double* C_new /*[D][D]*/,
+                        double* L_new /*[D][D]*/, int64_t* elite, orc_diag* dg);
+
 /* ---- whole iteration, Alg. 5 ---- */
 typedef struct orc_state {
   double mean[ORC_MAX_D], var[ORC_MAX_D];
   int32_t freq_idx;
   uint32_t iter;
+  double chol[ORC_MAX_D * ORC_MAX_D]; /* full_cov: lower Cholesky factor L of C, row-major [D][D]; var = diag(C) */
 } orc_state;
 
 typedef struct orc_output {

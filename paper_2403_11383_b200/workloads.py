@@ -67,7 +67,10 @@ def initial_distribution(cfg: dict):
     for d in range(D):
         mean[d] = fz if d % 3 == 2 else 0.0
     var = f32(np.array([cfg["sigma"][d % 3] ** 2 for d in range(D)]))
-    return dict(mean=f32(mean), var=var, freq_idx=0, iter=0)
+    st = dict(mean=f32(mean), var=var, freq_idx=0, iter=0)
+    if cfg.get("full_cov", 0):                   # C = diag(sigma^2): L = diag(sigma)
+        st["chol"] = np.diag(np.sqrt(var))
+    return st
 
 
 def robot_input(cfg: dict, robot: int, cmd=(0.0, 0.0, 0.0), phase=0, push=None, perturb=True,
