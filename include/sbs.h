@@ -117,6 +117,10 @@ typedef struct sbs_config {
      excepted).  n_sigma_groups 0 or 1: one Gaussian (sigma_scale ignored); at most 8; scales >= 0. */
   int32_t n_sigma_groups;
   float sigma_scale[8];
+  /* full-covariance CEM (Alg. 1 UpdateCov with a full C; L42): C = L L^T per
+     robot, initially diag(sigma^2); theta2 = mu' + L z; C_new = elite covariance + diag(floor), L_new =
+     Cholesky(C_new); var reports diag(C).  CEM only, n_sigma_groups <= 1. */
+  int32_t full_cov;
 } sbs_config;
 
 /* Per-robot input of one iteration (host for sbs_step, device for sbs_step_device). */
@@ -259,6 +263,13 @@ int sbs_advance(sbs_ctx* ctx, sbs_input* d_in, const sbs_output* d_out, const sb
 int sbs_run_loop(sbs_ctx* ctx, int32_t n_iter, sbs_input* d_in, sbs_output* d_out, const sbs_command* d_cmd,
                  const float* d_wrench, int32_t* d_fallen, float* d_trace, const sbs_loop_config* lc,
                  void* stream);
+
+/* Full covariance (full_cov = 1).  sbs_set_covariance: C [D][D] (host, row-major; its symmetric
+ * part is factored in binary64; SBS_ERR_INVALID_ARG unless positive definite); var := diag(C).
+ * sbs_get_cholesky: the current lower factor L [D][D] (host, row-major, zeros above the
+ * diagonal).  sbs_set_distribution on such a context sets C = diag(var). */
+int sbs_set_covariance(sbs_ctx* ctx, int32_t robot, const float* C);
+int sbs_get_cholesky(sbs_ctx* ctx, int32_t robot, float* L);
 
 /* The context's current reference of one robot (host out [H][12]): the last
  * sbs_set_reference / sbs_set_reference_device, or the rebuild of the last

@@ -39,7 +39,7 @@ class sbs_config(C.Structure):
         ("warm_shift", C.c_int32), ("seed", C.c_uint64),
         ("n_robots", C.c_int32), ("robot_offset", C.c_int32), ("device", C.c_int32),
         ("rank", C.c_int32), ("world", C.c_int32), ("nccl_id", C.c_uint8 * 128),
-        ("n_sigma_groups", C.c_int32), ("sigma_scale", C.c_float * 8),
+        ("n_sigma_groups", C.c_int32), ("sigma_scale", C.c_float * 8), ("full_cov", C.c_int32),
     ]
 
 
@@ -126,6 +126,8 @@ def load_library(path: str = LIB_PATH):
         "sbs_record_floats": ([ctxp], C.c_int),
         "sbs_step_records": ([ctxp, vp, vp, vp], C.c_int),
         "sbs_finish_records": ([ctxp, vp, vp, vp, vp], C.c_int),
+        "sbs_set_covariance": ([ctxp, C.c_int32, P(C.c_float)], C.c_int),
+        "sbs_get_cholesky": ([ctxp, C.c_int32, P(C.c_float)], C.c_int),
         "sbs_get_reference": ([ctxp, C.c_int32, P(C.c_float)], C.c_int),
         "sbs_advance": ([ctxp, vp, vp, vp, vp, vp, P(sbs_loop_config), vp], C.c_int),
         "sbs_run_loop": ([ctxp, C.c_int32, vp, vp, vp, vp, vp, vp, P(sbs_loop_config), vp], C.c_int),
@@ -179,6 +181,7 @@ def make_config(cfg: dict, device: int = 0, rank: int = 0, world: int = 1, nccl_
     sc = list(cfg.get("sigma_scale", [1.0]))
     c.n_sigma_groups = len(sc)
     c.sigma_scale[:len(sc)] = [float(v) for v in sc]
+    c.full_cov = int(cfg.get("full_cov", 0))
     return c
 
 
@@ -332,6 +335,15 @@ class Controller:
         n = (C.c_int64 * nk)()
         self._check(self.L.sbs_kernel_times(self.ctx, ms, n))
         return {KERNELS[i]: (ms[i], n[i]) for i in range(nk)}
+
+    def set_covariance(self, robot: int, Cm):
+        a = np.ascontiguousarray(np.asarray(Cm, dtype=np.float32).reshape(self.D, self.D))
+        return self._check(self.L.sbs_set_covariance(self.ctx, robot, _fp(a)))
+
+    def get_cholesky(self, robot: int = 0):
+        Lm = np.zeros((self.D, self.D), dtype=np.float32)
+        self._check(self.L.sbs_get_cholesky(self.ctx, robot, _fp(Lm)))
+        return Lm
 
     def get_reference(self, robot: int = 0):
         x = np.zeros((self.H, 12), dtype=np.float32)

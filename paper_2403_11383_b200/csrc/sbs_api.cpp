@@ -78,6 +78,7 @@ struct sbs_ctx {
   float* d_part = nullptr;
   float* d_gather = nullptr;  // [world][R][ex_stride] (world > 1)
   float* d_eJ = nullptr;      // [R][K_e] elite costs
+  float* d_L = nullptr;       // [R][D][D] Cholesky factors (full_cov)
   float* d_cand = nullptr;    // [R][world][K_e] CEM world > 1 candidates
   int64_t* d_elite = nullptr;
   int64_t* d_best = nullptr;
@@ -214,6 +215,8 @@ int validate(const sbs_config* c, std::string& why) {
     if (!(c->sigma[a] > 0)) return bad("sigma must be > 0");
   if (!(c->sigma_min_frac >= 0)) return bad("sigma_min_frac must be >= 0");
   if (c->n_sigma_groups < 0 || c->n_sigma_groups > 8) return bad("n_sigma_groups must be in [0, 8]");
+  if (c->full_cov && c->mode != SBS_CEM) return bad("full_cov is a CEM option");
+  if (c->full_cov && c->n_sigma_groups > 1) return bad("full_cov does not combine with multiple sigma groups");
   for (int g = 0; g < c->n_sigma_groups; ++g)
     if (!(c->sigma_scale[g] >= 0) || !std::isfinite(c->sigma_scale[g])) return bad("sigma_scale must be finite, >= 0");
   if (c->n_robots < 1) return bad("n_robots must be >= 1");
@@ -352,7 +355,7 @@ void sbs_destroy(sbs_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
   for (void* p : {(void*)c->d_mean, (void*)c->d_var, (void*)c->d_fidx, (void*)c->d_J,
-                  (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart, (void*)c->d_sdiag, (void*)c->d_eJ, (void*)c->d_cand,
+                  (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart, (void*)c->d_sdiag, (void*)c->d_eJ, (void*)c->d_cand, (void*)c->d_L,
                   (void*)c->d_out})
     if (p) cudaFree(p);
   if (c->h_out) cudaFreeHost(c->h_out);  // (h_in and h_xref point into h_blk)
@@ -491,7 +494,7 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.K_local = cfg->n_samples * (cfg->rank + 1) / cfg->world - P.k_begin;
   P.n_tiles = (int)((P.K_local + sbs::kBlock - 1) / sbs::kBlock);
   {
-    const int occ = sbs::rollout_occupancy(Pk, cfg->mode);
+    const int occ = sbs::rollout_occupancy(Pk, cfg->mode, cfg->full_cov != 0);
     const int64_t slots = (int64_t)occ * c->sm_count;
     P.n_cta = (int)std::max<int64_t>(1, std::min<int64_t>(P.n_tiles, slots / R));
   }
@@ -534,7 +537,9 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaMalloc(&c->d_counter, 2 * R * sizeof(int)));
   CKC(cudaMemset(c->d_counter, 0, 2 * R * sizeof(int)));
   P.n_eblk = P.n_elite > 0 ? (int)((P.n_elite + 31) / 32) : 1;  // 32 elites per elite-kernel CTA
-  CKC(cudaMalloc(&c->d_epart, (size_t)R * P.n_eblk * sbs::kEPartStride * sizeof(float)));
+  P.full_cov = cfg->full_cov ? 1 : 0;
+  const int erec = P.full_cov ? std::max(sbs::kEPartStride, sbs::fc_record_floats(D)) : sbs::kEPartStride;
+  CKC(cudaMalloc(&c->d_epart, (size_t)R * P.n_eblk * erec * sizeof(float)));
   CKC(cudaMalloc(&c->d_sdiag, (size_t)R * 8 * sizeof(float)));
   CKC(cudaMalloc(&c->d_out, R * sizeof(sbs_output)));
   CKC(cudaMallocHost(&c->h_out, R * sizeof(sbs_output)));
@@ -549,6 +554,13 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
     }
     CKC(cudaMemcpy(c->d_mean, m.data(), RD * sizeof(float), cudaMemcpyHostToDevice));
     CKC(cudaMemcpy(c->d_var, v.data(), RD * sizeof(float), cudaMemcpyHostToDevice));
+    if (cfg->full_cov) {  // C = diag(sigma^2): L = diag(sigma)
+      std::vector<float> L((size_t)R * D * D, 0.0f);
+      for (int r = 0; r < R; ++r)
+        for (int d = 0; d < D; ++d) L[((size_t)r * D + d) * D + d] = cfg->sigma[d % 3];
+      CKC(cudaMalloc(&c->d_L, L.size() * sizeof(float)));
+      CKC(cudaMemcpy(c->d_L, L.data(), L.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
     CKC(cudaMemset(c->d_fidx, 0, R * sizeof(int)));
   }
   P.mean = c->d_mean;
@@ -565,6 +577,7 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.epart = c->d_epart;
   P.sdiag = c->d_sdiag;
   P.elite_J = c->d_eJ;
+  P.Lmat = c->d_L;
   P.cand = c->d_cand;
   c->ref_set.assign(R, 0);
   // ---- NCCL (sample sharding) ----
@@ -636,7 +649,56 @@ int sbs_set_distribution(sbs_ctx* c, int32_t robot, const float* mean, const flo
   CK(cudaMemcpyAsync(c->d_mean + (size_t)robot * D, mean, D * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->d_var + (size_t)robot * D, var, D * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->d_fidx + robot, &freq_idx, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  if (c->d_L) {  // full covariance: C = diag(var)
+    std::vector<float> L((size_t)D * D, 0.0f);
+    for (int d = 0; d < D; ++d) L[(size_t)d * D + d] = sqrtf(var[d]);
+    CK(cudaMemcpyAsync(c->d_L + (size_t)robot * D * D, L.data(), L.size() * sizeof(float), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SBS_OK;
+  }
   CK(cudaStreamSynchronize(c->stream));
+  return SBS_OK;
+}
+
+int sbs_set_covariance(sbs_ctx* c, int32_t robot, const float* C) {
+  if (!c || !C) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (!c->d_L) return fail(c, SBS_ERR_STATE, "context has no full covariance (full_cov = 0)");
+  if (robot < 0 || robot >= c->P.R) return fail(c, SBS_ERR_INVALID_ARG, "robot out of range");
+  const int D = c->P.D;
+  if (!finite_all(C, D * D)) return fail(c, SBS_ERR_NONFINITE, "covariance not finite");
+  // Cholesky-Banachiewicz in binary64 of the symmetric part
+  std::vector<double> Ld((size_t)D * D, 0.0);
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = 0.5 * ((double)C[i * D + j] + (double)C[j * D + i]);
+      for (int k = 0; k < j; ++k) s -= Ld[(size_t)i * D + k] * Ld[(size_t)j * D + k];
+      if (i == j) {
+        if (!(s > 0.0)) return fail(c, SBS_ERR_INVALID_ARG, "covariance is not positive definite");
+        Ld[(size_t)i * D + i] = sqrt(s);
+      } else {
+        Ld[(size_t)i * D + j] = s / Ld[(size_t)j * D + j];
+      }
+    }
+  std::vector<float> L((size_t)D * D), v(D);
+  for (size_t i = 0; i < L.size(); ++i) L[i] = (float)Ld[i];
+  for (int d = 0; d < D; ++d) v[d] = C[d * D + d];
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaMemcpyAsync(c->d_L + (size_t)robot * D * D, L.data(), L.size() * sizeof(float), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemcpyAsync(c->d_var + (size_t)robot * D, v.data(), D * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return SBS_OK;
+}
+
+int sbs_get_cholesky(sbs_ctx* c, int32_t robot, float* L) {
+  if (!c || !L) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (!c->d_L) return fail(c, SBS_ERR_STATE, "context has no full covariance (full_cov = 0)");
+  if (robot < 0 || robot >= c->P.R) return fail(c, SBS_ERR_INVALID_ARG, "robot out of range");
+  const int D = c->P.D;
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(L, c->d_L + (size_t)robot * D * D, (size_t)D * D * sizeof(float), cudaMemcpyDeviceToHost));
   return SBS_OK;
 }
 
@@ -921,7 +983,8 @@ int sbs_get_reference(sbs_ctx* c, int32_t robot, float* x_ref) {
 int sbs_get_state(sbs_ctx* c, void* buf, uint64_t* nbytes) {
   if (!c || !nbytes) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
   const int R = c->P.R, D = c->P.D;
-  const uint64_t need = 32 + (uint64_t)R * (2 * D * sizeof(float) + sizeof(int32_t));
+  const uint64_t LD = c->d_L ? (uint64_t)D * D : 0;  // full covariance: the Cholesky factors follow
+  const uint64_t need = 32 + (uint64_t)R * (2 * D * sizeof(float) + sizeof(int32_t)) + (uint64_t)R * LD * sizeof(float);
   if (!buf || *nbytes < need) {
     *nbytes = need;
     return buf ? fail(c, SBS_ERR_INVALID_ARG, "buffer too small") : SBS_OK;
@@ -936,13 +999,17 @@ int sbs_get_state(sbs_ctx* c, void* buf, uint64_t* nbytes) {
   CK(cudaMemcpy(b + 32, c->d_mean, (size_t)R * D * sizeof(float), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(b + 32 + (size_t)R * D * 4, c->d_var, (size_t)R * D * sizeof(float), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(b + 32 + (size_t)R * D * 8, c->d_fidx, R * sizeof(int), cudaMemcpyDeviceToHost));
+  if (LD)
+    CK(cudaMemcpy(b + 32 + (size_t)R * D * 8 + (size_t)R * 4, c->d_L, (size_t)R * LD * sizeof(float),
+                  cudaMemcpyDeviceToHost));
   return SBS_OK;
 }
 
 int sbs_set_state(sbs_ctx* c, const void* buf, uint64_t nbytes) {
   if (!c || !buf) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
   const int R = c->P.R, D = c->P.D;
-  const uint64_t need = 32 + (uint64_t)R * (2 * D * sizeof(float) + sizeof(int32_t));
+  const uint64_t LD = c->d_L ? (uint64_t)D * D : 0;  // full covariance: the Cholesky factors follow
+  const uint64_t need = 32 + (uint64_t)R * (2 * D * sizeof(float) + sizeof(int32_t)) + (uint64_t)R * LD * sizeof(float);
   if (nbytes != need) return fail(c, SBS_ERR_INVALID_ARG, "state size mismatch");
   const char* b = (const char*)buf;
   uint64_t hdr[4];
@@ -954,6 +1021,9 @@ int sbs_set_state(sbs_ctx* c, const void* buf, uint64_t nbytes) {
   CK(cudaMemcpy(c->d_mean, b + 32, (size_t)R * D * sizeof(float), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_var, b + 32 + (size_t)R * D * 4, (size_t)R * D * sizeof(float), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_fidx, b + 32 + (size_t)R * D * 8, R * sizeof(int), cudaMemcpyHostToDevice));
+  if (LD)
+    CK(cudaMemcpy(c->d_L, b + 32 + (size_t)R * D * 8 + (size_t)R * 4, (size_t)R * LD * sizeof(float),
+                  cudaMemcpyHostToDevice));
   c->iter = (uint32_t)hdr[1];
   return SBS_OK;
 }

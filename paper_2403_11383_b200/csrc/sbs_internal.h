@@ -11,6 +11,8 @@ namespace sbs {
 constexpr int kBlock = 128;         // samples per tile = threads per rollout CTA
 constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, nfin, pad]
 constexpr int kEPartStride = 2 * SBS_MAX_D + 4;  // CEM elite-moment record [S1[D], n, S2[D]]
+// full-covariance CEM elite record [S1[D], n, lower triangle of S2 (D (D + 1) / 2)], 16-byte multiple
+__host__ __device__ constexpr int fc_record_floats(int D) { return ((D + 1 + D * (D + 1) / 2) + 3) / 4 * 4; }
 #ifndef SBS_ROLLOUT_MIN_BLOCKS
 #define SBS_ROLLOUT_MIN_BLOCKS 4
 #endif
@@ -45,6 +47,8 @@ struct Params {
   int mode;
   int64_t n_elite;
   float var_floor[3];
+  int full_cov;               // f3 (L42): CEM with a full covariance C = L L^T
+  float* Lmat;                // [R][D][D] lower Cholesky factor (row-major), full_cov only
   int n_sig_groups;           // multiple Gaussians (L41): sample k uses sig_scale[k mod n_sig_groups]
   float sig_scale[8];
   // --- noise ---
@@ -113,7 +117,7 @@ cudaError_t launch_elite(const Params& p, cudaStream_t s);
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                  int* fidx, cudaStream_t s);
 cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s);
-int rollout_occupancy(int P, int mode);
+int rollout_occupancy(int P, int mode, bool fc = false);
 // kernel attributes (dynamic shared memory limits), once per process and P, never inside a capture
 cudaError_t prepare_kernels(int P);  // resident CTAs per SM of the rollout kernel
 

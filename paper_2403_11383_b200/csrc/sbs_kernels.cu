@@ -175,6 +175,70 @@ __device__ __forceinline__ void sample_block(const Params& p, uint32_t robot_g, 
     th4[i] = __fmaf_rn(grp ? __fmul_rn(s.sig[4 * q + i], sc) : s.sig[4 * q + i], z[i], s.mu[4 * q + i]);
 }
 
+// f3 (L42): theta2 = mu' + L z with the same normative noise z.  Lt = L^T staged in
+// shared memory (Lt[j D + i] = L[i][j]); row i accumulates L_ij z_j for ascending j
+// (fmaf from 0), then adds mu'_i.  Broadcast shared-memory reads (all lanes read the
+// same L entry).
+template <int P, bool WITH_Z>
+__device__ __forceinline__ int draw_sample_fc(const Params& p, uint32_t robot_g, int64_t k, const RobotSmem& s,
+                                              const float* Lt, Theta<P>& th, float* z_out = nullptr) {
+  constexpr int D = 12 * P;
+  if (p.elite_preserve && k == 0) {  // L21
+#pragma unroll
+    for (int d = 0; d < D; ++d) theta_set(th, d, s.mu[d]);
+    if (WITH_Z)
+      for (int d = 0; d < D; ++d) z_out[d] = 0.0f;
+    return s.cur_idx;
+  }
+  const uint32_t kk = (uint32_t)k;
+#pragma unroll
+  for (int d = 0; d < D; ++d) theta_set(th, d, 0.0f);
+#pragma unroll
+  for (int q = 0; q < D / 4; ++q) {
+    const U4 w = philox4x32_10_rk((uint32_t)q, kk, s.iter, robot_g, p.rk);
+    float z[4];
+    box_muller(w.x, w.y, z[0], z[1]);
+    box_muller(w.z, w.w, z[2], z[3]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = 4 * q + u;
+#pragma unroll
+      for (int i = j; i < D; ++i) theta_set(th, i, __fmaf_rn(Lt[j * D + i], z[u], theta_get(th, i)));
+      if (WITH_Z) z_out[j] = z[u];
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < D; ++d) theta_set(th, d, __fadd_rn(s.mu[d], theta_get(th, d)));
+  int idx = s.cur_idx;
+  if (p.gait_adapt) {
+    const U4 w = philox4x32_10_rk(0x80000000u, kk, s.iter, robot_g, p.rk);
+    idx = (int)__umulhi(w.x, (uint32_t)p.n_freq);
+  }
+  return idx;
+}
+
+// L (row-major lower [D][D], global) -> Lt (transposed, shared; upper part of L as zeros)
+__device__ __forceinline__ void stage_chol_t(const Params& p, int r, float* Lt) {
+  const int D = p.D;
+  const float* L = p.Lmat + (size_t)r * D * D;
+  for (int idx = threadIdx.x; idx < D * D; idx += blockDim.x) {
+    const int i = idx / D, j = idx - i * D;
+    Lt[j * D + i] = j <= i ? L[idx] : 0.0f;
+  }
+}
+
+// noise z of Philox block q of sample k (elite preservation: z = 0)
+__device__ __forceinline__ void noise_block(const Params& p, uint32_t robot_g, int64_t k, int q, const RobotSmem& s,
+                                            float (&z)[4]) {
+  if (p.elite_preserve && k == 0) {
+    z[0] = z[1] = z[2] = z[3] = 0.0f;
+    return;
+  }
+  const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k, s.iter, robot_g, p.rk);
+  box_muller(w.x, w.y, z[0], z[1]);
+  box_muller(w.z, w.w, z[2], z[3]);
+}
+
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
@@ -621,12 +685,12 @@ __device__ __forceinline__ bool arrive_last(int* counter, int n) {
 // ---------------------------------------------------------------------------
 enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
 
-template <int P, int EPI, bool FUSED>
+template <int P, int EPI, bool FUSED, bool FC = false>
 __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(const __grid_constant__ Params p) {
   constexpr int D = 12 * P;
   constexpr int NR = D + 4;  // reduced rows (MPPI): w theta[D], w, w^2, J (finite), 1 (finite)
   __shared__ RobotSmem s;
-  extern __shared__ float s_red[];  // [NR][kBlock + 1]   (MPPI only)
+  extern __shared__ float s_red[];  // [NR][kBlock + 1] (MPPI) or L^T [D][D] (FC)
   __shared__ float s_wm[kBlock / 32], s_ws[kBlock / 32], s_wn[kBlock / 32];
   __shared__ int s_wk[kBlock / 32], s_wf[kBlock / 32];
   __shared__ float s_tile_m, s_run_m, s_run_sj, s_run_nf;
@@ -635,6 +699,7 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
   const int r = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   load_robot(p, r, s);
+  if (FC) stage_chol_t(p, r, s_red);
   if (tid == 0) {
     s_run_m = kInf;
     s_run_k = 0x7fffffff;
@@ -654,7 +719,8 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
     float J = kInf;
     int fi = 0;
     if (valid) {
-      fi = draw_sample<P, false>(p, robot_g, k, s, th);
+      if (FC) fi = draw_sample_fc<P, false>(p, robot_g, k, s, s_red, th);
+      else fi = draw_sample<P, false>(p, robot_g, k, s, th);
       J = rollout<P>(p, th, fi, s);
       p.J[(size_t)r * p.K_local + kl] = J;
     }
@@ -1247,6 +1313,171 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
                s_diag[1] > 0.f ? s_diag[0] / s_diag[1] : kInf, ne, ne, (int)((float)p.K_global - s_diag[1]));
 }
 
+// ---------------------------------------------------------------------------
+// sbs_cov_kernel (f3, L42: CEM with a full covariance C = L L^T): grid (n_eblk, R),
+// block 32 x 3P.  Warp q regenerates noise block q of the CTA's 32 elites, the CTA
+// forms their deviations d = L z (= theta - mu') and reduces S1 = sum d and the
+// lower triangle of S2 = sum d d^T (elites in order).  The last CTA of a robot
+// merges the records in order, forms C = S2/n - m m^T + diag(floor) with
+// m = S1/n, factors it (right-looking Cholesky in shared memory) and finishes:
+// mean = mu' + m, var = diag(C), L = chol(C).
+// dynamic smem: max(Lt [D][D] + Z [32][D+1] + Dv [32][D+1],  tot [fc] + C [D][D])
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int cov_smem_floats(int D) {
+  return (D * D + 64 * (D + 1)) > (fc_record_floats(D) + D * D) ? (D * D + 64 * (D + 1))
+                                                                  : (fc_record_floats(D) + D * D);
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * 3 * P) sbs_cov_kernel(const __grid_constant__ Params p) {
+  constexpr int D = 12 * P, NT = 32 * 3 * P, NL = D * (D + 1) / 2, FS = fc_record_floats(D);
+  __shared__ RobotSmem s;
+  __shared__ float s_mean[D], s_var[D];
+  __shared__ float s_diag[2];
+  __shared__ int s_fail;
+  extern __shared__ float dsm[];
+  float* Lt = dsm;                   // [D][D]
+  float* Z = dsm + D * D;            // [32][D + 1]
+  float* Dv = Z + 32 * (D + 1);      // [32][D + 1]
+  const int r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
+  load_robot(p, r, s, false);
+  stage_chol_t(p, r, Lt);
+  __syncthreads();
+  const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
+  const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
+  bool ok = false;
+  int64_t k = 0;
+  if (e < p.n_elite) {
+    k = p.elite[(size_t)r * p.n_elite + e];
+    ok = p.elite_J[(size_t)r * p.n_elite + e] < kInf;  // diverged samples never enter the moments (L17)
+  }
+  {
+    float z4[4] = {0.f, 0.f, 0.f, 0.f};
+    if (ok) noise_block(p, robot_g, k, q, s, z4);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) Z[lane * (D + 1) + 4 * q + u] = z4[u];
+  }
+  const unsigned okb = __ballot_sync(0xffffffffu, ok);
+  __syncthreads();
+  for (int o = tid; o < 32 * D; o += NT) {  // d = L z, row i in ascending j
+    const int ee = o / D, i = o - ee * D;
+    const float* zr = Z + ee * (D + 1);
+    float a = 0.0f;
+    for (int j = 0; j <= i; ++j) a = fmaf(Lt[j * D + i], zr[j], a);
+    Dv[ee * (D + 1) + i] = a;
+  }
+  __syncthreads();
+  float* rec = p.epart + ((size_t)r * gridDim.x + blockIdx.x) * FS;
+  for (int o = tid; o < D + NL; o += NT) {
+    float a = 0.0f;
+    if (o < D) {
+      for (int ee = 0; ee < 32; ++ee) a += Dv[ee * (D + 1) + o];
+      rec[o] = a;
+    } else {
+      const int t = o - D;
+      int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+      while ((i + 1) * (i + 2) / 2 <= t) ++i;
+      while (i * (i + 1) / 2 > t) --i;
+      const int j = t - i * (i + 1) / 2;
+      for (int ee = 0; ee < 32; ++ee) a = fmaf(Dv[ee * (D + 1) + i], Dv[ee * (D + 1) + j], a);
+      rec[D + 1 + t] = a;
+    }
+  }
+  if (tid == 0) rec[D] = (float)__popc(okb);
+  if (!arrive_last(p.ecounter + r, gridDim.x)) return;
+  // ---- last CTA: merge the records in order ----
+  float* tot = dsm;            // [FS]
+  float* Cm = dsm + FS;        // [D][D] lower
+  for (int o = tid; o < D + 1 + NL; o += NT) {
+    float a = 0.0f;
+    int b = 0;
+    for (; b + 4 <= (int)gridDim.x; b += 4) {
+      const float* r0 = p.epart + ((size_t)r * gridDim.x + b) * FS + o;
+      const float v0 = __ldcg(r0), v1 = __ldcg(r0 + FS), v2 = __ldcg(r0 + 2 * FS), v3 = __ldcg(r0 + 3 * FS);
+      a += v0;
+      a += v1;
+      a += v2;
+      a += v3;
+    }
+    for (; b < (int)gridDim.x; ++b) a += __ldcg(p.epart + ((size_t)r * gridDim.x + b) * FS + o);
+    tot[o] = a;
+  }
+  const float* sd = p.sdiag + (size_t)r * 8;
+  const Best best{sd[0], __float_as_int(sd[1]), __float_as_int(sd[2])};
+  if (tid == 0) {
+    s_diag[0] = sd[3];
+    s_diag[1] = sd[4];
+    s_fail = 0;
+  }
+  __syncthreads();
+  const float ne = tot[D];
+  const bool all_div = !(ne > 0.f);
+  const float inv = all_div ? 0.f : 1.0f / ne;
+  if (!all_div) {
+    for (int t = tid; t < NL; t += NT) {
+      int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+      while ((i + 1) * (i + 2) / 2 <= t) ++i;
+      while (i * (i + 1) / 2 > t) --i;
+      const int j = t - i * (i + 1) / 2;
+      const float mi = tot[i] * inv, mj = tot[j] * inv;
+      float c = fmaf(-mi, mj, tot[D + 1 + t] * inv);
+      if (i == j) c += p.var_floor[i % 3];
+      Cm[i * D + j] = c;
+    }
+    __syncthreads();
+    for (int d = tid; d < D; d += NT) {
+      s_mean[d] = s.mu[d] + tot[d] * inv;
+      s_var[d] = Cm[d * D + d];
+    }
+    // right-looking Cholesky of the lower triangle, in place
+    for (int kk = 0; kk < D; ++kk) {
+      if (tid == 0) {
+        const float c = Cm[kk * D + kk];
+        if (!(c > 0.0f)) s_fail = 1;
+        Cm[kk * D + kk] = sqrtf(fmaxf(c, 1e-30f));
+      }
+      __syncthreads();
+      const float lkk = Cm[kk * D + kk];
+      for (int i = kk + 1 + tid; i < D; i += NT) Cm[i * D + kk] = Cm[i * D + kk] / lkk;
+      __syncthreads();
+      const int m = D - 1 - kk;  // trailing block (kk, D) x (kk, D), lower triangle: m (m + 1) / 2 entries
+      for (int t = tid; t < m * (m + 1) / 2; t += NT) {
+        int a = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+        while ((a + 1) * (a + 2) / 2 <= t) ++a;
+        while (a * (a + 1) / 2 > t) --a;
+        const int b2 = t - a * (a + 1) / 2;
+        const int i = kk + 1 + a, j = kk + 1 + b2;
+        Cm[i * D + j] = fmaf(-Cm[i * D + kk], Cm[j * D + kk], Cm[i * D + j]);
+      }
+      __syncthreads();
+    }
+  }
+  const bool keep = all_div || s_fail;  // L27 (or a failed factorisation): keep the distribution
+  for (int d = tid; d < D; d += NT) {
+    if (keep) {
+      s_mean[d] = p.mean[(size_t)r * D + d];
+      s_var[d] = p.var[(size_t)r * D + d];
+    }
+  }
+  __syncthreads();
+  const int fi = all_div ? s.cur_idx : best.f;
+  for (int d = tid; d < D; d += NT) {
+    p.mean[(size_t)r * D + d] = s_mean[d];
+    p.var[(size_t)r * D + d] = s_var[d];
+  }
+  if (!keep)
+    for (int idx = tid; idx < D * D; idx += NT) {
+      const int i = idx / D, j = idx - i * D;
+      p.Lmat[(size_t)r * D * D + idx] = j <= i ? Cm[idx] : 0.0f;
+    }
+  if (tid == 0) {
+    p.fidx[r] = fi;
+    p.best[r] = best.k;
+  }
+  write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, best.m,
+               s_diag[1] > 0.f ? s_diag[0] / s_diag[1] : kInf, ne, ne, (int)((float)p.K_global - s_diag[1]));
+}
+
 // Naive with world > 1, after the all-gather (p.part = [world][R] rank records)
 template <int P>
 __global__ void __launch_bounds__(128) sbs_naive_finalize_kernel(const __grid_constant__ Params p) {
@@ -1264,13 +1495,16 @@ __global__ void __launch_bounds__(128) sbs_debug_samples_kernel(const __grid_con
                                                                 int64_t n, float* z, float* theta, int* fidx) {
   constexpr int D = 12 * P;
   __shared__ RobotSmem s;
+  extern __shared__ float Lt[];  // full covariance: L^T [D][D]
   load_robot(p, r, s, false);
+  if (p.full_cov) stage_chol_t(p, r, Lt);
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   Theta<P> th;
   float zz[D];
-  const int f = draw_sample<P, true>(p, (uint32_t)(p.robot_offset + r), k0 + i, s, th, zz);
+  const int f = p.full_cov ? draw_sample_fc<P, true>(p, (uint32_t)(p.robot_offset + r), k0 + i, s, Lt, th, zz)
+                           : draw_sample<P, true>(p, (uint32_t)(p.robot_offset + r), k0 + i, s, th, zz);
 #pragma unroll
   for (int d = 0; d < D; ++d) {
     z[i * D + d] = zz[d];
@@ -1287,7 +1521,7 @@ __global__ void __launch_bounds__(128) sbs_debug_samples_kernel(const __grid_con
 template <int P>
 struct PEntry {
   static cudaError_t rollout(const Params& p, int mode, bool fused, cudaStream_t s);
-  static int occupancy(int mode);
+  static int occupancy(int mode, bool fc);
   static cudaError_t elite(const Params& p, cudaStream_t s);
   static cudaError_t naive_finalize(const Params& p, cudaStream_t s);
   static cudaError_t debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
@@ -1296,12 +1530,13 @@ struct PEntry {
 };
 
 #if defined(SBS_TU_P)
-template <int P, int EPI, bool FUSED>
+template <int P, int EPI, bool FUSED, bool FC = false>
 static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
   constexpr int D = 12 * P;
-  const size_t smem = EPI == EPI_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : 0;
+  const size_t smem = EPI == EPI_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float)
+                                      : (FC ? (size_t)D * D * sizeof(float) : 0);
   dim3 grid(p.n_cta, p.R);
-  sbs_rollout_kernel<P, EPI, FUSED><<<grid, kBlock, smem, s>>>(p);
+  sbs_rollout_kernel<P, EPI, FUSED, FC><<<grid, kBlock, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -1309,15 +1544,18 @@ template <int P>
 cudaError_t PEntry<P>::rollout(const Params& p, int mode, bool fused, cudaStream_t s) {
   if (mode == SBS_MPPI) return fused ? launch_rollout_t<P, EPI_MPPI, true>(p, s) : launch_rollout_t<P, EPI_MPPI, false>(p, s);
   if (mode == SBS_NAIVE && fused) return launch_rollout_t<P, EPI_ARGMIN, true>(p, s);
+  if (p.full_cov) return launch_rollout_t<P, EPI_ARGMIN, false, true>(p, s);  // CEM, full covariance (f3)
   return launch_rollout_t<P, EPI_ARGMIN, false>(p, s);  // CEM, or sharded Naive: records only
 }
 
 template <int P>
-int PEntry<P>::occupancy(int mode) {
+int PEntry<P>::occupancy(int mode, bool fc) {
   constexpr int D = 12 * P;
-  const size_t smem = mode == SBS_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : 0;
+  const size_t smem = mode == SBS_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float)
+                                       : (fc ? (size_t)D * D * sizeof(float) : 0);
   const void* f = mode == SBS_MPPI ? (const void*)sbs_rollout_kernel<P, EPI_MPPI, true>
-                                   : (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false>;
+                                   : (fc ? (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false, true>
+                                         : (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false>);
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, kBlock, smem) != cudaSuccess) return 1;
@@ -1327,7 +1565,10 @@ int PEntry<P>::occupancy(int mode) {
 template <int P>
 cudaError_t PEntry<P>::elite(const Params& p, cudaStream_t s) {
   dim3 grid(p.n_eblk, p.R);
-  sbs_elite_kernel<P><<<grid, 32 * 3 * P, 0, s>>>(p);
+  if (p.full_cov)
+    sbs_cov_kernel<P><<<grid, 32 * 3 * P, (size_t)cov_smem_floats(12 * P) * sizeof(float), s>>>(p);
+  else
+    sbs_elite_kernel<P><<<grid, 32 * 3 * P, 0, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -1341,7 +1582,8 @@ template <int P>
 cudaError_t PEntry<P>::debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                      int* fidx, cudaStream_t s) {
   const int blocks = (int)((n + 127) / 128);
-  sbs_debug_samples_kernel<P><<<blocks, 128, 0, s>>>(p, robot, k0, n, z, theta, fidx);
+  const size_t smem = p.full_cov ? (size_t)144 * P * P * sizeof(float) : 0;  // L^T [D][D]
+  sbs_debug_samples_kernel<P><<<blocks, 128, smem, s>>>(p, robot, k0, n, z, theta, fidx);
   return cudaGetLastError();
 }
 
@@ -1355,6 +1597,12 @@ cudaError_t PEntry<P>::prepare() {
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             big);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(sbs_cov_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_debug_samples_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   return e;
 }
 
@@ -1379,8 +1627,8 @@ cudaError_t launch_rollout(const Params& p, int mode, bool fused, cudaStream_t s
   return cudaErrorInvalidValue;
 }
 
-int rollout_occupancy(int P, int mode) {
-  SBS_DISPATCH_P(P, occupancy(mode));
+int rollout_occupancy(int P, int mode, bool fc) {
+  SBS_DISPATCH_P(P, occupancy(mode, fc));
   return 1;
 }
 
