@@ -279,6 +279,17 @@ def run_sbs(args):
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
            "api": "sbs_set_reference + sbs_step (host buffers, synchronous)"}
 
+    # ---- the other BASELINE configs on this GPU (rank 0, N = 1): where the ALU roofline is
+    #      meaningful (config 4 at K = 2^22) and the CEM iteration (config 3) ----
+    extra = None
+    if world == 1:
+        extra = {"config4_K4M": _time_config(B, W, C, np, torch, W.config4(4194304), steps=20, warmup=3,
+                                             peak=peak, label="config4: MPPI, K=2^22, H=12 (BASELINE configs[3], 1 GPU)"),
+                 "config3_cem": _time_config(B, W, C, np, torch, W.config3("cem"), steps=200, warmup=10,
+                                             peak=peak, label="config3: CEM K_e=1000, K=10000, gait adaptation"),
+                 "config5_batched": _time_config(B, W, C, np, torch, W.config5(), steps=20, warmup=3, peak=peak,
+                                                 label="config5: 4096 robots x 1024 samples, MPPI (1 GPU)")}
+
     line = None
     if rank == 0:
         cpu = None
@@ -298,7 +309,7 @@ def run_sbs(args):
                        "K_total": K_total, "K_per_gpu": K_PER_GPU, "H": H, "mode": "mppi",
                        "parallelism": f"samples sharded over {world} GPU(s)" + (" + NCCL all-gather" if world > 1 else ""),
                        "l2": "flushed between timed iterations (256 MiB memset, outside the events)"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "other_configs": extra,
             "gpu_launches": int(ctrl.launches_per_step() * args.steps), "clocks": clk,
         }
         print(json.dumps(line), flush=True)
@@ -307,6 +318,44 @@ def run_sbs(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def _time_config(B, W, C, np, torch, cfg_inputs, steps, warmup, peak, label):
+    """Device time per iteration of another BASELINE config (inputs resident, L2 flushed
+    between iterations), with the rollout kernel's live roofline fraction."""
+    cfg, inputs = cfg_inputs
+    R = len(inputs)
+    ctrl = B.Controller(cfg)
+    for r, inp in enumerate(inputs):
+        ctrl.set_reference(r, inp["xref"])
+    d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
+    d_out = torch.zeros(R * C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(warmup):
+        ctrl.step_device(d_in.data_ptr(), d_out.data_ptr(), stream.cuda_stream)
+    torch.cuda.synchronize()
+    ctrl.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        ctrl.step_device(d_in.data_ptr(), d_out.data_ptr(), stream.cuda_stream)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    kt = ctrl.kernel_times()
+    ctrl.profile(False)
+    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    K = cfg["n_samples"] * R
+    r_ms, r_n = kt["rollout"]
+    r_s = r_ms / max(r_n, 1) * 1e-3
+    achieved = ALG_FLOP_PER_SAMPLE_STEP * K * H / r_s / 1e12
+    ctrl.close()
+    return {"workload": label, "K_total": K, "steps": steps, "ms_per_step": ms,
+            "value": K * H / (ms * 1e-3), "unit": "sample-steps/s",
+            "kernels_us": {k: 1e3 * v[0] / v[1] for k, v in kt.items() if v[1]},
+            "rollout_roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                                 "frac": achieved / peak}}
 
 
 def main():

@@ -9,6 +9,7 @@
 namespace sbs {
 
 constexpr int kBlock = 128;         // samples per tile = threads per rollout CTA
+constexpr int kSplitTile = 32;      // samples per tile of the latency-mode (SPLIT) rollout
 constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, nfin, pad]
 constexpr int kEPartStride = 2 * SBS_MAX_D + 4;  // CEM elite-moment record [S1[D], n, S2[D]]
 // full-covariance CEM elite record [S1[D], n, lower triangle of S2 (D (D + 1) / 2)], 16-byte multiple
@@ -47,6 +48,7 @@ struct Params {
   int mode;
   int64_t n_elite;
   float var_floor[3];
+  int split;                  // latency mode: kSplitTile samples per tile, sampler split over 4 lanes
   int full_cov;               // f3 (L42): CEM with a full covariance C = L L^T
   float* Lmat;                // [R][D][D] lower Cholesky factor (row-major), full_cov only
   int n_sig_groups;           // multiple Gaussians (L41): sample k uses sig_scale[k mod n_sig_groups]
@@ -117,7 +119,7 @@ cudaError_t launch_elite(const Params& p, cudaStream_t s);
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                  int* fidx, cudaStream_t s);
 cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s);
-int rollout_occupancy(int P, int mode, bool fc = false);
+int rollout_occupancy(int P, int mode, bool fc = false, bool split = false);
 // kernel attributes (dynamic shared memory limits), once per process and P, never inside a capture
 cudaError_t prepare_kernels(int P);  // resident CTAs per SM of the rollout kernel
 

@@ -682,15 +682,23 @@ __device__ __forceinline__ bool arrive_last(int* counter, int n) {
 //   EPI_ARGMIN: (J, k) argmin + finite-cost sum/count (Naive, CEM)
 // FUSED: the last CTA of each robot merges the records and finishes the
 // iteration (MPPI, Naive): one launch per MPC iteration.
+// SPLIT (latency mode, few samples): a tile is kSplitTile samples; the CTA's
+// 128 threads first draw them 4 lanes per sample (Philox blocks q = u, u + 4,
+// ... into shared memory), then the first warp rolls them out.  The same draw
+// code and rounding as draw_sample, so the samples are bitwise identical; the
+// per-sample dependent chain loses ~3/4 of the sampler.
 // ---------------------------------------------------------------------------
 enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
 
-template <int P, int EPI, bool FUSED, bool FC = false>
+template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false>
 __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(const __grid_constant__ Params p) {
   constexpr int D = 12 * P;
   constexpr int NR = D + 4;  // reduced rows (MPPI): w theta[D], w, w^2, J (finite), 1 (finite)
+  constexpr int TS = SPLIT ? kSplitTile : kBlock;  // samples per tile
   __shared__ RobotSmem s;
-  extern __shared__ float s_red[];  // [NR][kBlock + 1] (MPPI) or L^T [D][D] (FC)
+  extern __shared__ float s_red[];  // [NR][kBlock + 1] (MPPI) or L^T [D][D] (FC); SPLIT: + theta [TS][D + 1], fidx [TS]
+  float* s_th = s_red + (EPI == EPI_MPPI ? NR * (kBlock + 1) : 0);
+  int* s_fi = reinterpret_cast<int*>(s_th + TS * (D + 1));
   __shared__ float s_wm[kBlock / 32], s_ws[kBlock / 32], s_wn[kBlock / 32];
   __shared__ int s_wk[kBlock / 32], s_wf[kBlock / 32];
   __shared__ float s_tile_m, s_run_m, s_run_sj, s_run_nf;
@@ -712,15 +720,57 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
   float run = 0.0f;  // running partial of row `tid` (MPPI)
 
   for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-    const int64_t kl = (int64_t)tile * kBlock + tid;
-    const bool valid = kl < p.K_local;
+    const int64_t kl = (int64_t)tile * TS + tid;
+    const bool valid = (!SPLIT || tid < TS) && kl < p.K_local;
     const int64_t k = p.k_begin + kl;
     Theta<P> th;
     float J = kInf;
     int fi = 0;
+    if (SPLIT) {  // phase 1: 4 lanes per sample draw its Philox blocks into shared memory
+      const int sl = tid >> 2, u = tid & 3;
+      const int64_t kl1 = (int64_t)tile * TS + sl;
+      if (kl1 < p.K_local) {
+        const int64_t k1 = p.k_begin + kl1;
+        float* dst = s_th + sl * (D + 1);
+        if (p.elite_preserve && k1 == 0) {  // L21
+          for (int d = u; d < D; d += 4) dst[d] = s.mu[d];
+          if (u == 0) s_fi[sl] = s.cur_idx;
+        } else {
+          const bool grp = p.n_sig_groups > 1;
+          const float sc = grp ? p.sig_scale[(int)(k1 % p.n_sig_groups)] : 1.0f;
+          for (int q = u; q < D / 4; q += 4) {
+            const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k1, s.iter, robot_g, p.rk);
+            float z[4];
+            box_muller(w.x, w.y, z[0], z[1]);
+            box_muller(w.z, w.w, z[2], z[3]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float sg = grp ? __fmul_rn(s.sig[4 * q + i], sc) : s.sig[4 * q + i];
+              dst[4 * q + i] = __fmaf_rn(sg, z[i], s.mu[4 * q + i]);
+            }
+          }
+          if (u == 0) {
+            int idx = s.cur_idx;
+            if (p.gait_adapt) {
+              const U4 w = philox4x32_10_rk(0x80000000u, (uint32_t)k1, s.iter, robot_g, p.rk);
+              idx = (int)__umulhi(w.x, (uint32_t)p.n_freq);
+            }
+            s_fi[sl] = idx;
+          }
+        }
+      }
+      __syncthreads();
+    }
     if (valid) {
-      if (FC) fi = draw_sample_fc<P, false>(p, robot_g, k, s, s_red, th);
-      else fi = draw_sample<P, false>(p, robot_g, k, s, th);
+      if (SPLIT) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) theta_set(th, d, s_th[tid * (D + 1) + d]);
+        fi = s_fi[tid];
+      } else if (FC) {
+        fi = draw_sample_fc<P, false>(p, robot_g, k, s, s_red, th);
+      } else {
+        fi = draw_sample<P, false>(p, robot_g, k, s, th);
+      }
       J = rollout<P>(p, th, fi, s);
       p.J[(size_t)r * p.K_local + kl] = J;
     }
@@ -1521,7 +1571,7 @@ __global__ void __launch_bounds__(128) sbs_debug_samples_kernel(const __grid_con
 template <int P>
 struct PEntry {
   static cudaError_t rollout(const Params& p, int mode, bool fused, cudaStream_t s);
-  static int occupancy(int mode, bool fc);
+  static int occupancy(int mode, bool fc, bool split);
   static cudaError_t elite(const Params& p, cudaStream_t s);
   static cudaError_t naive_finalize(const Params& p, cudaStream_t s);
   static cudaError_t debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
@@ -1530,18 +1580,29 @@ struct PEntry {
 };
 
 #if defined(SBS_TU_P)
-template <int P, int EPI, bool FUSED, bool FC = false>
-static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
+template <int P, int EPI, bool FC, bool SPLIT>
+constexpr size_t rollout_smem() {
   constexpr int D = 12 * P;
-  const size_t smem = EPI == EPI_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float)
-                                      : (FC ? (size_t)D * D * sizeof(float) : 0);
+  return (EPI == EPI_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : (FC ? (size_t)D * D * sizeof(float) : 0)) +
+         (SPLIT ? (size_t)kSplitTile * (D + 2) * sizeof(float) : 0);
+}
+
+template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false>
+static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
   dim3 grid(p.n_cta, p.R);
-  sbs_rollout_kernel<P, EPI, FUSED, FC><<<grid, kBlock, smem, s>>>(p);
+  sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT><<<grid, kBlock, rollout_smem<P, EPI, FC, SPLIT>(), s>>>(p);
   return cudaGetLastError();
 }
 
 template <int P>
 cudaError_t PEntry<P>::rollout(const Params& p, int mode, bool fused, cudaStream_t s) {
+  if (p.split) {  // latency mode (few samples)
+    if (mode == SBS_MPPI)
+      return fused ? launch_rollout_t<P, EPI_MPPI, true, false, true>(p, s)
+                   : launch_rollout_t<P, EPI_MPPI, false, false, true>(p, s);
+    if (mode == SBS_NAIVE && fused) return launch_rollout_t<P, EPI_ARGMIN, true, false, true>(p, s);
+    return launch_rollout_t<P, EPI_ARGMIN, false, false, true>(p, s);
+  }
   if (mode == SBS_MPPI) return fused ? launch_rollout_t<P, EPI_MPPI, true>(p, s) : launch_rollout_t<P, EPI_MPPI, false>(p, s);
   if (mode == SBS_NAIVE && fused) return launch_rollout_t<P, EPI_ARGMIN, true>(p, s);
   if (p.full_cov) return launch_rollout_t<P, EPI_ARGMIN, false, true>(p, s);  // CEM, full covariance (f3)
@@ -1549,13 +1610,21 @@ cudaError_t PEntry<P>::rollout(const Params& p, int mode, bool fused, cudaStream
 }
 
 template <int P>
-int PEntry<P>::occupancy(int mode, bool fc) {
-  constexpr int D = 12 * P;
-  const size_t smem = mode == SBS_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float)
-                                       : (fc ? (size_t)D * D * sizeof(float) : 0);
-  const void* f = mode == SBS_MPPI ? (const void*)sbs_rollout_kernel<P, EPI_MPPI, true>
-                                   : (fc ? (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false, true>
-                                         : (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false>);
+int PEntry<P>::occupancy(int mode, bool fc, bool split) {
+  size_t smem;
+  const void* f;
+  if (mode == SBS_MPPI) {
+    smem = split ? rollout_smem<P, EPI_MPPI, false, true>() : rollout_smem<P, EPI_MPPI, false, false>();
+    f = split ? (const void*)sbs_rollout_kernel<P, EPI_MPPI, true, false, true>
+              : (const void*)sbs_rollout_kernel<P, EPI_MPPI, true>;
+  } else if (fc) {
+    smem = rollout_smem<P, EPI_ARGMIN, true, false>();
+    f = (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false, true>;
+  } else {
+    smem = split ? rollout_smem<P, EPI_ARGMIN, false, true>() : rollout_smem<P, EPI_ARGMIN, false, false>();
+    f = split ? (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false, false, true>
+              : (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false>;
+  }
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, kBlock, smem) != cudaSuccess) return 1;
@@ -1602,6 +1671,18 @@ cudaError_t PEntry<P>::prepare() {
                              big);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(sbs_cov_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, true, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, false, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, true, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, false, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_debug_samples_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   return e;
 }
@@ -1627,8 +1708,8 @@ cudaError_t launch_rollout(const Params& p, int mode, bool fused, cudaStream_t s
   return cudaErrorInvalidValue;
 }
 
-int rollout_occupancy(int P, int mode, bool fc) {
-  SBS_DISPATCH_P(P, occupancy(mode, fc));
+int rollout_occupancy(int P, int mode, bool fc, bool split) {
+  SBS_DISPATCH_P(P, occupancy(mode, fc, split));
   return 1;
 }
 

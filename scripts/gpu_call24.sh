@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?; tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python scripts/quick_time.py 2>&1 | grep -E "config|2\^"
-timeout 600 python bench.py --steps 3000 > gpurun_out/bench.log 2>&1; echo bench rc=$?; python -c "
-import json; d=json.loads([l for l in open('gpurun_out/bench.log') if l.startswith('{')][-1]); print(d['value'], d['latency_us'], d['e2e'], d['roofline']['kernel_us'])"
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_all.log 2>&1; echo pytest-all rc=$?; tail -3 gpurun_out/pytest_gpu_all.log
+grep -E "^E " gpurun_out/pytest_gpu_all.log | head
+timeout 600 python bench.py > gpurun_out/bench.jsonl 2> gpurun_out/bench.err; echo bench rc=$?; tail -3 gpurun_out/bench.err

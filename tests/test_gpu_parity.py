@@ -175,6 +175,21 @@ def test_multiple_gaussians(B, orc, mode, scales):
     _run_pair(B, orc, cfg, inputs, n_steps=2)
 
 
+@pytest.mark.parametrize("gait", ["pace", "bound", "fine_grid"])
+def test_gait_variants(B, orc, gait):
+    """f4: other periodic gaits and a finer theta1 grid are configuration ("a more
+    fine-grained discretization step can be employed"; P:301 pacing)."""
+    kw = dict(pace=dict(phase_offset=[0.0, 0.5, 0.0, 0.5]),
+              bound=dict(phase_offset=[0.0, 0.0, 0.5, 0.5], duty_factor=0.4),
+              fine_grid=dict(freq_hz=[1.3, 1.45, 1.6, 1.75, 1.9, 2.05, 2.2, 2.4]))[gait]
+    cfg = W.base_config(n_samples=800, mode="naive", gait_adapt=1, **kw)
+    inputs = [W.robot_input(cfg, 0, cmd=(0.3, 0.0, 0.0), phase=W.q32(0.15))]
+    c, _ = _run_pair(B, orc, cfg, inputs, n_steps=2)
+    if gait == "fine_grid":
+        _, _, f = c.debug_samples(0, 0, 800)
+        assert set(np.unique(f)) == set(range(8))
+
+
 def test_full_inertia_and_no_warm_shift(B, orc):
     cfg = W.base_config(n_samples=500, inertia=[0.135, 0.01, -0.02, 0.01, 0.54, 0.03, -0.02, 0.03, 0.58],
                         warm_shift=0, elite_preserve=0, duty_factor=1.0)
