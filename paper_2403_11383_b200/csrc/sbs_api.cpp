@@ -493,19 +493,14 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.k_begin = cfg->n_samples * cfg->rank / cfg->world;
   P.K_local = cfg->n_samples * (cfg->rank + 1) / cfg->world - P.k_begin;
   {
-    // latency mode when every kSplitTile-sample tile of every robot fits one resident wave:
-    // the sampler is spread over 4 lanes per sample (shorter per-sample dependent chain).
-    // MPPI only while its (larger) per-CTA records stay few: at most one CTA per SM
-    // (measured: config 2, K = 10^4, is slower split, its merge of 313 records costs more
-    // than the shorter chain saves; CEM rollouts at K = 10^4 gain 10 %).
-    const int64_t tiles32 = (P.K_local + sbs::kSplitTile - 1) / sbs::kSplitTile;
+    // latency mode when every 128-sample tile of every robot fits one resident wave of
+    // 4 x 128-thread CTAs: the sampler is spread over 4 lanes per sample (shorter
+    // per-sample dependent chain; the machine is mostly idle at these sizes anyway)
+    P.n_tiles = (int)((P.K_local + sbs::kBlock - 1) / sbs::kBlock);
     const int occ_s = sbs::rollout_occupancy(Pk, cfg->mode, false, true);
-    const int64_t cap = cfg->mode == SBS_MPPI ? (int64_t)c->sm_count : (int64_t)occ_s * c->sm_count;
-    bool split = !cfg->full_cov && (int64_t)R * tiles32 <= cap;
+    bool split = !cfg->full_cov && (int64_t)R * P.n_tiles <= (int64_t)occ_s * c->sm_count;
     if (const char* e = getenv("SBS_SPLIT")) split = split && atoi(e) != 0;  // experiments: SBS_SPLIT=0 disables
     P.split = split ? 1 : 0;
-    const int tile = split ? sbs::kSplitTile : sbs::kBlock;
-    P.n_tiles = (int)((P.K_local + tile - 1) / tile);
     const int occ = sbs::rollout_occupancy(Pk, cfg->mode, cfg->full_cov != 0, split);
     const int64_t slots = (int64_t)occ * c->sm_count;
     P.n_cta = (int)std::max<int64_t>(1, std::min<int64_t>(P.n_tiles, slots / R));

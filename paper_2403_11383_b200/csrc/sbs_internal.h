@@ -9,7 +9,7 @@
 namespace sbs {
 
 constexpr int kBlock = 128;         // samples per tile = threads per rollout CTA
-constexpr int kSplitTile = 32;      // samples per tile of the latency-mode (SPLIT) rollout
+constexpr int kSplitLanes = 4;      // latency-mode (SPLIT) rollout: lanes per sample in the sampler phase
 constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, nfin, pad]
 constexpr int kEPartStride = 2 * SBS_MAX_D + 4;  // CEM elite-moment record [S1[D], n, S2[D]]
 // full-covariance CEM elite record [S1[D], n, lower triangle of S2 (D (D + 1) / 2)], 16-byte multiple

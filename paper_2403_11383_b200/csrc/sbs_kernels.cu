@@ -18,6 +18,21 @@
 #include "sbs_noise.cuh"
 
 namespace sbs {
+#if defined(SBS_TIMING)  // experiments only: phase timestamps (%globaltimer) of CTA 0 / the last CTA
+__device__ unsigned long long g_sbs_ts[16];
+#define SBS_TS(i)                                                               \
+  do {                                                                          \
+    if (threadIdx.x == 0) {                                                     \
+      unsigned long long t_;                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
+      g_sbs_ts[i] = t_;                                                         \
+    }                                                                           \
+  } while (0)
+#else
+#define SBS_TS(i) \
+  do {            \
+  } while (0)
+#endif
 
 #define kInf __int_as_float(0x7f800000)
 constexpr float kPitchMax = 1.5697963267948966f;  // pi/2 - 1e-3 (L26)
@@ -456,11 +471,13 @@ __device__ __forceinline__ void stage_copy(float* dst, const float* src, int n) 
 // ---------------------------------------------------------------------------
 // Output (a7): u0 = delta_0-masked cone projection of knot 0.
 // ---------------------------------------------------------------------------
+// pre: {phase_q32 of the robot's input, iteration counter} already in shared memory, or null (loaded here)
 static __device__ void write_output(const Params& p, int r, int status, const float* mean_new, const float* var_new,
-                             int fi, float jmin, float jmean, float omega, float ess, int ndiv) {
+                             int fi, float jmin, float jmean, float omega, float ess, int ndiv,
+                             const uint32_t* pre = nullptr) {
   sbs_output* o = p.out + r;
   const int D = p.D;
-  const uint32_t ph0 = p.in[r].phase_q32;
+  const uint32_t ph0 = pre ? pre[0] : p.in[r].phase_q32;
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
     o->mean[d] = mean_new[d];
     o->var[d] = var_new[d];
@@ -480,7 +497,7 @@ static __device__ void write_output(const Params& p, int r, int status, const fl
     o->freq_idx = fi;
     o->freq_hz = p.freq_hz[fi];
     o->status = status;
-    o->iter = step_iter(p);
+    o->iter = pre ? pre[1] : step_iter(p);
     o->j_min = jmin;
     o->j_mean = jmean;
     o->omega = omega;
@@ -537,19 +554,104 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   __shared__ float s_row[1][SBS_MAX_D + 4];
   __shared__ float s_sc[128];
   __shared__ float s_mean[SBS_MAX_D], s_var[SBS_MAX_D];
-  const Best b = merge_argmin(p, r);
-  const float beta = b.m;
+  __shared__ uint32_t s_pre[2];
+  __shared__ float s_bm[32];
+  __shared__ int s_bk[32], s_bf[32];
+  __shared__ float s_part[16 * (SBS_MAX_D + 4)];
   const int nc = p.n_cta;
-  const int CH = min(128, max(1, stage_floats / RL));
+  const bool one_pass = nc <= 128 && nc * RL <= stage_floats;
+  Best b;
+  if (one_pass) {
+    // one load round trip: every record, this robot's variance, input phase and iteration counter
+    if (p.part_c_stride == 1) {
+      stage_copy(stage, part_rec(p, r, 0), nc * RL);  // records of a robot are contiguous
+    } else {
+      for (int c = 0; c < nc; ++c) stage_copy(stage + c * RL, part_rec(p, r, c), RL);
+    }
+    if (!EMIT) {
+      for (int d = tid; d < D; d += blockDim.x) s_var[d] = p.var[(size_t)r * D + d];
+      if (tid == 0) {
+        s_pre[0] = p.in[r].phase_q32;
+        s_pre[1] = step_iter(p);
+      }
+    }
+    __syncthreads();
+    SBS_TS(7);
+    if (tid < 32) {  // warp 0: argmin over the staged headers, then the per-record scales
+      float m = kInf;
+      int mk = 0x7fffffff, mf = 0;
+      for (int c = tid; c < nc; c += 32) {
+        const float* h = stage + c * RL;
+        const int kc = __float_as_int(h[1]);
+        if (jk_less(h[0], kc, m, mk)) {
+          m = h[0];
+          mk = kc;
+          mf = __float_as_int(h[2]);
+        }
+      }
+      warp_argmin(m, mk, mf);
+      for (int c = tid; c < nc; c += 32) {
+        const float mc = stage[c * RL];
+        s_sc[c] = (mc < kInf) ? __expf((m - mc) * p.inv_lambda) : 0.0f;
+      }
+      if (tid == 0) {
+        s_bm[0] = m;
+        s_bk[0] = mk;
+        s_bf[0] = mf;
+      }
+    }
+    __syncthreads();
+    b = Best{s_bm[0], s_bk[0], s_bf[0]};
+  } else {
+    b = merge_argmin(p, r);
+  }
+  SBS_TS(8);
+  const float beta = b.m;
+  const int CH = one_pass ? nc : min(128, max(1, stage_floats / RL));
   float acc = 0.f;  // thread tid < NR owns row tid: 0..D-1 V, D S, D+1 S2, D+2 sumJ, D+3 nfin
   for (int c0 = 0; c0 < nc; c0 += CH) {
     const int n = min(CH, nc - c0);
-    if (p.part_c_stride == 1) {
-      stage_copy(stage, part_rec(p, r, c0), n * RL);  // records of a robot are contiguous
-    } else {
-      for (int c = 0; c < n; ++c) stage_copy(stage + c * RL, part_rec(p, r, c0 + c), RL);
+    if (!one_pass) {
+      if (p.part_c_stride == 1) {
+        stage_copy(stage, part_rec(p, r, c0), n * RL);
+      } else {
+        for (int c = 0; c < n; ++c) stage_copy(stage + c * RL, part_rec(p, r, c0 + c), RL);
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    if (one_pass) {  // scales already in s_sc (warp 0); (row, record-chunk) per thread, then chunk sums
+      const int nch = max(1, min((int)blockDim.x / NR, 16));  // record chunks
+      const int per = (n + nch - 1) / nch;
+      float* part = s_part;                                    // [nch][NR]
+      if (tid < nch * NR) {
+        const int row = tid % NR, ch = tid / NR;
+        const int col = row < D ? kPartHdr + row : 3 + (row - D);
+        const int kind = row < D + 1 ? 0 : (row == D + 1 ? 1 : 2);
+        const int c_end = min(n, (ch + 1) * per);
+        float a0 = 0.f, a1 = 0.f;
+        int c = ch * per;
+        for (; c + 1 < c_end; c += 2) {
+          float s0 = s_sc[c], s1 = s_sc[c + 1];
+          if (kind == 1) { s0 *= s0; s1 *= s1; }
+          if (kind == 2) { s0 = 1.f; s1 = 1.f; }
+          a0 = fmaf(stage[c * RL + col], s0, a0);
+          a1 = fmaf(stage[(c + 1) * RL + col], s1, a1);
+        }
+        if (c < c_end) {
+          float s0 = kind == 2 ? 1.f : s_sc[c];
+          if (kind == 1) s0 *= s0;
+          a0 = fmaf(stage[c * RL + col], s0, a0);
+        }
+        part[ch * NR + row] = a0 + a1;
+      }
+      __syncthreads();
+      if (tid < NR) {
+        float a = 0.f;
+        for (int ch = 0; ch < nch; ++ch) a += part[ch * NR + tid];
+        s_row[0][tid] = a;
+      }
+      break;  // single chunk
+    }
     for (int c = tid; c < n; c += blockDim.x) {
       const float mc = stage[c * RL];
       s_sc[c] = (mc < kInf) ? __expf((beta - mc) * p.inv_lambda) : 0.0f;
@@ -576,8 +678,9 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
     }
     __syncthreads();
   }
-  if (tid < NR) s_row[0][tid] = acc;
+  if (!one_pass && tid < NR) s_row[0][tid] = acc;
   __syncthreads();
+  SBS_TS(9);
   if (EMIT) {  // this rank's merged record, relative to its own beta
     float* o = emit + (size_t)r * p.part_stride;
     if (tid < D) o[kPartHdr + tid] = s_row[0][tid];
@@ -596,14 +699,16 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   const float* var = p.var + (size_t)r * D;
   for (int d = tid; d < D; d += blockDim.x) {
     s_mean[d] = all_div ? mean[d] : s_row[0][d] / S;
-    s_var[d] = var[d];
+    if (!one_pass) s_var[d] = var[d];
   }
   const int fi = all_div ? p.fidx[r] : b.f;
   __syncthreads();
   for (int d = tid; d < D; d += blockDim.x) mean[d] = s_mean[d];
   if (tid == 0) p.fidx[r] = fi;
+  SBS_TS(10);
   write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, beta,
-               nfin > 0.f ? sumJ / nfin : kInf, S, all_div ? 0.f : S * S / S2, (int)((float)p.K_global - nfin));
+               nfin > 0.f ? sumJ / nfin : kInf, S, all_div ? 0.f : S * S / S2, (int)((float)p.K_global - nfin),
+               one_pass ? s_pre : nullptr);
 }
 
 // Naive UpdateMean (Alg. 3): the best sample theta* becomes the mean,
@@ -613,7 +718,14 @@ static __device__ void naive_finalize_block(const Params& p, int r, const RobotS
   constexpr int D = 12 * P;
   __shared__ float s_mean[D], s_var[D];
   __shared__ float s_sum[2];
+  __shared__ uint32_t s_pre[2];
   const int tid = threadIdx.x;
+  // issued with the record loads of merge_argmin (one round trip): variance, input phase, iteration
+  for (int d = tid; d < D; d += blockDim.x) s_var[d] = p.var[(size_t)r * D + d];
+  if (tid == 0) {
+    s_pre[0] = p.in[r].phase_q32;
+    s_pre[1] = step_iter(p);
+  }
   const Best b = merge_argmin(p, r);
   if (tid < 32) {
     float sj = 0.f, nf = 0.f;
@@ -641,11 +753,9 @@ static __device__ void naive_finalize_block(const Params& p, int r, const RobotS
     for (int i = 0; i < 4; ++i) s_mean[4 * tid + i] = th4[i];
   }
   __syncthreads();
-  for (int d = tid; d < D; d += blockDim.x) {
+  for (int d = tid; d < D; d += blockDim.x)
     if (all_div) s_mean[d] = mean[d];
-    s_var[d] = p.var[(size_t)r * D + d];
-  }
-  const int fi = all_div ? p.fidx[r] : b.f;
+  const int fi = all_div ? s.cur_idx : b.f;
   __syncthreads();
   for (int d = tid; d < D; d += blockDim.x) mean[d] = s_mean[d];
   if (tid == 0) {
@@ -656,7 +766,7 @@ static __device__ void naive_finalize_block(const Params& p, int r, const RobotS
   const float nf = s_sum[1];
   write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, b.m,
                nf > 0.f ? s_sum[0] / nf : kInf, all_div ? 0.f : 1.f, all_div ? 0.f : 1.f,
-               (int)((float)p.K_global - nf));
+               (int)((float)p.K_global - nf), s_pre);
 }
 
 // last CTA of a grid row (robot) to arrive returns true (threadfence pattern)
@@ -682,23 +792,27 @@ __device__ __forceinline__ bool arrive_last(int* counter, int n) {
 //   EPI_ARGMIN: (J, k) argmin + finite-cost sum/count (Naive, CEM)
 // FUSED: the last CTA of each robot merges the records and finishes the
 // iteration (MPPI, Naive): one launch per MPC iteration.
-// SPLIT (latency mode, few samples): a tile is kSplitTile samples; the CTA's
-// 128 threads first draw them 4 lanes per sample (Philox blocks q = u, u + 4,
-// ... into shared memory), then the first warp rolls them out.  The same draw
-// code and rounding as draw_sample, so the samples are bitwise identical; the
-// per-sample dependent chain loses ~3/4 of the sampler.
+// SPLIT (latency mode, few samples): kSplitLanes x 128 threads per CTA; every
+// tile's 128 samples are first drawn kSplitLanes lanes per sample (Philox
+// blocks q = u, u + kSplitLanes, ... into shared memory), then the first 128
+// threads roll them out while the others wait.  The same draw code and rounding
+// as draw_sample, so the samples are bitwise identical; the per-sample dependent
+// chain loses (kSplitLanes - 1) / kSplitLanes of the sampler.
 // ---------------------------------------------------------------------------
 enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
 
+
 template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false>
-__global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ? 1 : kRolloutMinBlocks)
+    sbs_rollout_kernel(const __grid_constant__ Params p) {
   constexpr int D = 12 * P;
   constexpr int NR = D + 4;  // reduced rows (MPPI): w theta[D], w, w^2, J (finite), 1 (finite)
-  constexpr int TS = SPLIT ? kSplitTile : kBlock;  // samples per tile
+  constexpr int TS = kBlock;  // samples per tile
   __shared__ RobotSmem s;
   extern __shared__ float s_red[];  // [NR][kBlock + 1] (MPPI) or L^T [D][D] (FC); SPLIT: + theta [TS][D + 1], fidx [TS]
   float* s_th = s_red + (EPI == EPI_MPPI ? NR * (kBlock + 1) : 0);
   int* s_fi = reinterpret_cast<int*>(s_th + TS * (D + 1));
+  const bool sampler_thread = !SPLIT || threadIdx.x < kBlock;  // holds a sample in phase 2 / the epilogue
   __shared__ float s_wm[kBlock / 32], s_ws[kBlock / 32], s_wn[kBlock / 32];
   __shared__ int s_wk[kBlock / 32], s_wf[kBlock / 32];
   __shared__ float s_tile_m, s_run_m, s_run_sj, s_run_nf;
@@ -706,6 +820,7 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
 
   const int r = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (blockIdx.x == 0) SBS_TS(0);
   load_robot(p, r, s);
   if (FC) stage_chol_t(p, r, s_red);
   if (tid == 0) {
@@ -716,29 +831,30 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
     s_run_nf = 0.f;
   }
   __syncthreads();
+  if (blockIdx.x == 0) SBS_TS(1);
   const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
   float run = 0.0f;  // running partial of row `tid` (MPPI)
 
   for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
     const int64_t kl = (int64_t)tile * TS + tid;
-    const bool valid = (!SPLIT || tid < TS) && kl < p.K_local;
+    const bool valid = sampler_thread && kl < p.K_local;
     const int64_t k = p.k_begin + kl;
     Theta<P> th;
     float J = kInf;
     int fi = 0;
-    if (SPLIT) {  // phase 1: 4 lanes per sample draw its Philox blocks into shared memory
-      const int sl = tid >> 2, u = tid & 3;
+    if (SPLIT) {  // phase 1: kSplitLanes lanes per sample draw its Philox blocks into shared memory
+      const int sl = tid / kSplitLanes, u = tid % kSplitLanes;
       const int64_t kl1 = (int64_t)tile * TS + sl;
       if (kl1 < p.K_local) {
         const int64_t k1 = p.k_begin + kl1;
         float* dst = s_th + sl * (D + 1);
         if (p.elite_preserve && k1 == 0) {  // L21
-          for (int d = u; d < D; d += 4) dst[d] = s.mu[d];
+          for (int d = u; d < D; d += kSplitLanes) dst[d] = s.mu[d];
           if (u == 0) s_fi[sl] = s.cur_idx;
         } else {
           const bool grp = p.n_sig_groups > 1;
           const float sc = grp ? p.sig_scale[(int)(k1 % p.n_sig_groups)] : 1.0f;
-          for (int q = u; q < D / 4; q += 4) {
+          for (int q = u; q < D / 4; q += kSplitLanes) {
             const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k1, s.iter, robot_g, p.rk);
             float z[4];
             box_muller(w.x, w.y, z[0], z[1]);
@@ -771,7 +887,9 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
       } else {
         fi = draw_sample<P, false>(p, robot_g, k, s, th);
       }
+      if (blockIdx.x == 0) SBS_TS(2);
       J = rollout<P>(p, th, fi, s);
+      if (blockIdx.x == 0) SBS_TS(3);
       p.J[(size_t)r * p.K_local + kl] = J;
     }
     // ---- per-tile argmin (J, k) ----
@@ -786,7 +904,7 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
         sj += __shfl_xor_sync(0xffffffffu, sj, o);
         nf += __shfl_xor_sync(0xffffffffu, nf, o);
       }
-      if (lane == 0) {
+      if (lane == 0 && sampler_thread) {
         s_wm[warp] = m;
         s_wk[warp] = mk;
         s_wf[warp] = mf;
@@ -810,7 +928,7 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
     }
     // ---- step a5 (MPPI), per tile: weights relative to the tile min, then an
     //      online-softmax merge into this CTA's running record ----
-    if (lane == 0) {
+    if (lane == 0 && sampler_thread) {
       s_wm[warp] = m;
       s_wk[warp] = mk;
       s_wf[warp] = mf;
@@ -835,14 +953,16 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
     if (valid) {
 #pragma unroll
       for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = w * theta_get(th, d);
-    } else {
+    } else if (sampler_thread) {
 #pragma unroll
       for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = 0.0f;
     }
-    s_red[(D + 0) * (kBlock + 1) + tid] = w;
-    s_red[(D + 1) * (kBlock + 1) + tid] = w * w;
-    s_red[(D + 2) * (kBlock + 1) + tid] = fin ? J : 0.0f;
-    s_red[(D + 3) * (kBlock + 1) + tid] = fin ? 1.0f : 0.0f;
+    if (sampler_thread) {
+      s_red[(D + 0) * (kBlock + 1) + tid] = w;
+      s_red[(D + 1) * (kBlock + 1) + tid] = w * w;
+      s_red[(D + 2) * (kBlock + 1) + tid] = fin ? J : 0.0f;
+      s_red[(D + 3) * (kBlock + 1) + tid] = fin ? 1.0f : 0.0f;
+    }
     __syncthreads();
     const float mr = s_run_m;
     const float mn = fminf(mr, mt);
@@ -887,10 +1007,13 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
     out[2] = __int_as_float(s_run_f);
     out[7] = 0.0f;
   }
+  if (blockIdx.x == 0) SBS_TS(4);
   if (FUSED) {
     if (arrive_last(p.counter + r, gridDim.x)) {
+      SBS_TS(5);
       if (EPI == EPI_MPPI) mppi_merge_block<false>(p, r, nullptr, s_red, NR * (kBlock + 1));
       else naive_finalize_block<P>(p, r, s);
+      SBS_TS(6);
     }
   }
 }
@@ -898,7 +1021,7 @@ __global__ void __launch_bounds__(kBlock, kRolloutMinBlocks) sbs_rollout_kernel(
 // stand-alone merge (world > 1: rank partial before / final merge after the all-gather)
 template <bool EMIT>
 __global__ void __launch_bounds__(128) sbs_mppi_finalize(const __grid_constant__ Params p, float* emit) {
-  __shared__ float stage[4096];
+  __shared__ __align__(16) float stage[4096];
   mppi_merge_block<EMIT>(p, blockIdx.x, emit, stage, 4096);
 }
 
@@ -1316,6 +1439,11 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   }
   if (!arrive_last(p.ecounter + r, gridDim.x)) return;
   // ---- last CTA: merge the elite records in order, finish the iteration ----
+  __shared__ uint32_t s_pre[2];
+  if (tid == 0) {  // issued with the record loads below
+    s_pre[0] = p.in[r].phase_q32;
+    s_pre[1] = step_iter(p);
+  }
   {
     float a0 = 0.f;  // row tid (2D + 1 <= blockDim = 3D / 4 * 32 / 12 ... = 8D)
     for (int b0 = 0; b0 < (int)gridDim.x; b0 += 16) {
@@ -1360,7 +1488,7 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
     p.best[r] = b.k;
   }
   write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, b.m,
-               s_diag[1] > 0.f ? s_diag[0] / s_diag[1] : kInf, ne, ne, (int)((float)p.K_global - s_diag[1]));
+               s_diag[1] > 0.f ? s_diag[0] / s_diag[1] : kInf, ne, ne, (int)((float)p.K_global - s_diag[1]), s_pre);
 }
 
 // ---------------------------------------------------------------------------
@@ -1584,13 +1712,14 @@ template <int P, int EPI, bool FC, bool SPLIT>
 constexpr size_t rollout_smem() {
   constexpr int D = 12 * P;
   return (EPI == EPI_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : (FC ? (size_t)D * D * sizeof(float) : 0)) +
-         (SPLIT ? (size_t)kSplitTile * (D + 2) * sizeof(float) : 0);
+         (SPLIT ? (size_t)kBlock * (D + 2) * sizeof(float) : 0);
 }
 
 template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false>
 static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
   dim3 grid(p.n_cta, p.R);
-  sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT><<<grid, kBlock, rollout_smem<P, EPI, FC, SPLIT>(), s>>>(p);
+  sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT>
+      <<<grid, SPLIT ? kBlock * kSplitLanes : kBlock, rollout_smem<P, EPI, FC, SPLIT>(), s>>>(p);
   return cudaGetLastError();
 }
 
@@ -1625,9 +1754,8 @@ int PEntry<P>::occupancy(int mode, bool fc, bool split) {
     f = split ? (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false, false, true>
               : (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false>;
   }
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, kBlock, smem) != cudaSuccess) return 1;
+  int n = 0;  // (dynamic shared memory limits: prepare(), which sbs_create runs first)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, split && !fc ? kBlock * kSplitLanes : kBlock, smem) != cudaSuccess) return 1;
   return n > 0 ? n : 1;
 }
 
@@ -1658,7 +1786,7 @@ cudaError_t PEntry<P>::debug_samples(const Params& p, int robot, int64_t k0, int
 
 template <int P>
 cudaError_t PEntry<P>::prepare() {
-  const int big = 96 * 1024;
+  const int big = 96 * 1024, huge = 200 * 1024;
   cudaError_t e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -1672,22 +1800,30 @@ cudaError_t PEntry<P>::prepare() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(sbs_cov_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, true, false, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, false, false, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, true, false, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, false, false, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_debug_samples_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   return e;
 }
 
 template struct PEntry<SBS_TU_P>;
+
+#if defined(SBS_TIMING)  // experiments only
+#define SBS_CAT2(a, b) a##b
+#define SBS_CAT(a, b) SBS_CAT2(a, b)
+extern "C" int SBS_CAT(sbs_debug_ts_p, SBS_TU_P)(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_sbs_ts, sizeof(g_sbs_ts));
+}
+#endif
 #endif  // SBS_TU_P
 
 #if defined(SBS_TU_COMMON)
