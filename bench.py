@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--impl", default="sbs", choices=["sbs", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=500)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true", help="skip the configs 3/4/5 lines (ncu launch lists)")
     return ap.parse_args()
 
 
@@ -246,7 +247,7 @@ def run_sbs(args):
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("rollout_config2_bytes_per_launch")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "sbs_rollout_kernel<4,true>",
+            "traffic": traffic, "kernel": "sbs_rollout_kernel<4,MPPI,fused>",
             "kernel_us": r_avg_s * 1e6, "kernel_share_of_step": (r_avg_s * 1e3) / ms,
             "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz (clocks.max.sm)",
             "flop_per_sample_step": ALG_FLOP_PER_SAMPLE_STEP}
@@ -282,7 +283,7 @@ def run_sbs(args):
     # ---- the other BASELINE configs on this GPU (rank 0, N = 1): where the ALU roofline is
     #      meaningful (config 4 at K = 2^22) and the CEM iteration (config 3) ----
     extra = None
-    if world == 1:
+    if world == 1 and not args.no_other_configs:
         extra = {"config4_K4M": _time_config(B, W, C, np, torch, W.config4(4194304), steps=20, warmup=3,
                                              peak=peak, label="config4: MPPI, K=2^22, H=12 (BASELINE configs[3], 1 GPU)"),
                  "config3_cem": _time_config(B, W, C, np, torch, W.config3("cem"), steps=200, warmup=10,
