@@ -94,7 +94,8 @@ struct sbs_ctx {
   size_t blk_in_off = 0, blk_ref_off = 0, blk_bytes = 0;
   sbs_input* h_in = nullptr;   // = h_blk + blk_in_off
   float* h_xref = nullptr;     // = h_blk + blk_ref_off
-  sbs_output* h_out = nullptr; // pinned
+  sbs_output* h_out = nullptr; // pinned, mapped: the host path's kernels write the outputs here directly
+  sbs_output* h_out_dev = nullptr;  // device address of h_out (null: copied back by a D2H node)
   cudaEvent_t blk_ev = nullptr;  // last H2D of h_blk (the host rewrites it only after this completed)
   bool ref_dirty = false;
   cudaGraphExec_t graph = nullptr;
@@ -549,7 +550,11 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaMalloc(&c->d_epart, (size_t)R * P.n_eblk * erec * sizeof(float)));
   CKC(cudaMalloc(&c->d_sdiag, (size_t)R * 8 * sizeof(float)));
   CKC(cudaMalloc(&c->d_out, R * sizeof(sbs_output)));
-  CKC(cudaMallocHost(&c->h_out, R * sizeof(sbs_output)));
+  CKC(cudaHostAlloc(&c->h_out, R * sizeof(sbs_output), cudaHostAllocMapped));
+  {
+    const char* e = getenv("SBS_MAPPED_OUT");  // experiments: SBS_MAPPED_OUT=0 copies the outputs back instead
+    if (!e || atoi(e) != 0) CKC(cudaHostGetDevicePointer((void**)&c->h_out_dev, c->h_out, 0));
+  }
   // initial distribution: mean (0, 0, m|g_z|/4) per leg and knot, var = sigma^2, freq_idx 0
   {
     std::vector<float> m(RD), v(RD);
@@ -732,15 +737,19 @@ namespace {
 // one host-path iteration on c->stream: upload [iter | inputs | reference] in one
 // copy, the kernels, the outputs back (captured once into a CUDA graph when possible)
 int enqueue_host_step(sbs_ctx* c, cudaStream_t s) {
+  // inputs go up with one H2D copy (measured: kernels reading them over PCIe from mapped
+  // memory are slower, every CTA pays the PCIe latency); outputs come back written by the
+  // finishing CTA straight into mapped pinned memory (no D2H node)
   CK(cudaMemcpyAsync(c->d_blk, c->h_blk, c->blk_bytes, cudaMemcpyHostToDevice, s));
   Params saved = c->P;
   c->P.in = c->d_in;
-  c->P.out = c->d_out;
   c->P.iter_dev = reinterpret_cast<const uint32_t*>(c->d_blk);
+  c->P.out = c->h_out_dev ? c->h_out_dev : c->d_out;  // mapped: the finishing CTA writes over PCIe, no D2H node
   int rc = enqueue_step(c, s);
   c->P = saved;
   if (rc != SBS_OK) return rc;
-  CK(cudaMemcpyAsync(c->h_out, c->d_out, c->P.R * sizeof(sbs_output), cudaMemcpyDeviceToHost, s));
+  if (!c->h_out_dev)
+    CK(cudaMemcpyAsync(c->h_out, c->d_out, c->P.R * sizeof(sbs_output), cudaMemcpyDeviceToHost, s));
   return SBS_OK;
 }
 }  // namespace
