@@ -103,7 +103,7 @@ def load_library(path: str = LIB_PATH):
         "sbs_last_error": ([ctxp], C.c_char_p),
         "sbs_create": ([P(sbs_config), P(ctxp)], C.c_int),
         "sbs_destroy": ([ctxp], None),
-        "sbs_set_reference": ([ctxp, C.c_int32, P(C.c_float)], C.c_int),
+        "sbs_set_reference": ([ctxp, C.c_int32, vp], C.c_int),
         "sbs_set_reference_device": ([ctxp, vp, vp], C.c_int),
         "sbs_set_distribution": ([ctxp, C.c_int32, P(C.c_float), P(C.c_float), C.c_int32], C.c_int),
         "sbs_get_distribution": ([ctxp, C.c_int32, P(C.c_float), P(C.c_float), P(C.c_int32)], C.c_int),
@@ -235,8 +235,10 @@ class Controller:
 
     # ---- state --------------------------------------------------------------
     def set_reference(self, robot: int, xref):
-        a = np.ascontiguousarray(np.asarray(xref, dtype=np.float32).reshape(self.H, 12))
-        return self._check(self.L.sbs_set_reference(self.ctx, robot, _fp(a)))
+        a = xref
+        if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous and a.size == self.H * 12):
+            a = np.ascontiguousarray(np.asarray(xref, dtype=np.float32).reshape(self.H, 12))
+        return self._check(self.L.sbs_set_reference(self.ctx, robot, a.ctypes.data))
 
     def set_reference_device(self, d_ptr: int, stream: int = 0):
         return self._check(self.L.sbs_set_reference_device(self.ctx, C.c_void_p(d_ptr), C.c_void_p(stream)))

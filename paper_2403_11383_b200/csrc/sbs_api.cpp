@@ -766,6 +766,29 @@ int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
   if (c->external) return fail(c, SBS_ERR_STATE, "external exchange: use sbs_step_records / sbs_finish_records");
   CK(cudaSetDevice(c->cfg.device));
   cudaStream_t s = c->stream;
+  if (R == 1 && c->P.H * 12 <= sbs::kInlineRefFloats && c->cfg.world == 1) {
+    // inputs, reference and iteration counter ride in the kernel parameters: no copy node,
+    // no graph (direct launches); outputs land in mapped pinned memory
+    Params saved = c->P;
+    c->P.inline_in = 1;
+    c->P.in_inline = in[0];
+    memcpy(c->P.xref_inline, c->h_xref, (size_t)c->P.H * 12 * sizeof(float));
+    c->P.iter_dev = nullptr;
+    c->P.out = c->h_out_dev ? c->h_out_dev : c->d_out;
+    CK(cudaEventRecord(c->ev0, s));
+    const int rc = enqueue_step(c, s);
+    c->P = saved;
+    if (rc != SBS_OK) return rc;
+    if (!c->h_out_dev) CK(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(sbs_output), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(c->ev1, s));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    c->h_out[0].device_us = ms * 1000.f;
+    memcpy(out, c->h_out, sizeof(sbs_output));
+    c->iter += 1;
+    return c->h_out[0].status == SBS_WARN_ALL_DIVERGED ? SBS_WARN_ALL_DIVERGED : SBS_OK;
+  }
   CK(cudaEventSynchronize(c->blk_ev));
   memcpy(c->h_blk, &c->iter, sizeof(uint32_t));
   memcpy(c->h_in, in, R * sizeof(sbs_input));

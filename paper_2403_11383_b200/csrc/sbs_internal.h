@@ -9,6 +9,7 @@
 namespace sbs {
 
 constexpr int kBlock = 128;         // samples per tile = threads per rollout CTA
+constexpr int kInlineRefFloats = 16 * 12;  // host path, R = 1, H <= 16: inputs and reference ride in the kernel parameters
 constexpr int kSplitLanes = 4;      // latency-mode (SPLIT) rollout: lanes per sample in the sampler phase
 constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, nfin, pad]
 constexpr int kEPartStride = 2 * SBS_MAX_D + 4;  // CEM elite-moment record [S1[D], n, S2[D]]
@@ -66,6 +67,10 @@ struct Params {
   int n_tiles, n_cta;         // per robot
   int part_stride;             // floats per partial record = kPartHdr + D (tight, 16-byte multiple)
   int part_c_stride;          // 1: CTA partials [R][n_cta]; R: NCCL-gathered rank partials [world][R]
+  // --- host path with inline inputs (R = 1): no H2D copy ---
+  int inline_in;
+  sbs_input in_inline;
+  float xref_inline[kInlineRefFloats];
   // --- device buffers ---
   float* mean;                // [R][D]
   float* var;                 // [R][D]

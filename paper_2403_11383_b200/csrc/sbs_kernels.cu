@@ -54,6 +54,12 @@ struct RobotSmem {
   int cur_idx;
 };
 
+// robot r's inputs / reference: device buffers, or (host path, R = 1) the kernel parameters themselves
+__device__ __forceinline__ const sbs_input* robot_in(const Params& p, int r) { return p.inline_in ? &p.in_inline : p.in + r; }
+__device__ __forceinline__ const float* robot_xref(const Params& p, int r) {
+  return p.inline_in ? p.xref_inline : p.xref + (size_t)r * p.H * 12;
+}
+
 // iteration counter: kernel parameter, or device memory when the step runs as a
 // captured CUDA graph (the host writes it with the inputs every step)
 __device__ __forceinline__ uint32_t step_iter(const Params& p) { return p.iter_dev ? *p.iter_dev + p.iter_add : p.iter; }
@@ -79,7 +85,7 @@ static __device__ void load_robot(const Params& p, int r, RobotSmem& s, bool rol
     s.mu[d] = v;
     s.sig[d] = __fsqrt_rn(var[d]);
   }
-  const sbs_input* in = p.in + r;
+  const sbs_input* in = robot_in(p, r);
   if (threadIdx.x == 0) {
     s.cur_idx = p.fidx[r];
     s.iter = step_iter(p);
@@ -90,7 +96,7 @@ static __device__ void load_robot(const Params& p, int r, RobotSmem& s, bool rol
     s.feet[a] = in->feet_cur[a];
     s.feet[12 + a] = in->feet_next[a];
   }
-  const float* xr = p.xref + (size_t)r * p.H * 12;
+  const float* xr = robot_xref(p, r);
   for (int a = threadIdx.x; a < p.H * 12; a += blockDim.x) {
     const int j = a / 12, c = a - 12 * j;
     s.xref[12 * j + xref_slot(c)] = xr[a];
@@ -477,7 +483,7 @@ static __device__ void write_output(const Params& p, int r, int status, const fl
                              const uint32_t* pre = nullptr) {
   sbs_output* o = p.out + r;
   const int D = p.D;
-  const uint32_t ph0 = pre ? pre[0] : p.in[r].phase_q32;
+  const uint32_t ph0 = pre ? pre[0] : robot_in(p, r)->phase_q32;
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
     o->mean[d] = mean_new[d];
     o->var[d] = var_new[d];
@@ -571,7 +577,7 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
     if (!EMIT) {
       for (int d = tid; d < D; d += blockDim.x) s_var[d] = p.var[(size_t)r * D + d];
       if (tid == 0) {
-        s_pre[0] = p.in[r].phase_q32;
+        s_pre[0] = robot_in(p, r)->phase_q32;
         s_pre[1] = step_iter(p);
       }
     }
@@ -723,7 +729,7 @@ static __device__ void naive_finalize_block(const Params& p, int r, const RobotS
   // issued with the record loads of merge_argmin (one round trip): variance, input phase, iteration
   for (int d = tid; d < D; d += blockDim.x) s_var[d] = p.var[(size_t)r * D + d];
   if (tid == 0) {
-    s_pre[0] = p.in[r].phase_q32;
+    s_pre[0] = robot_in(p, r)->phase_q32;
     s_pre[1] = step_iter(p);
   }
   const Best b = merge_argmin(p, r);
@@ -1441,7 +1447,7 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   // ---- last CTA: merge the elite records in order, finish the iteration ----
   __shared__ uint32_t s_pre[2];
   if (tid == 0) {  // issued with the record loads below
-    s_pre[0] = p.in[r].phase_q32;
+    s_pre[0] = robot_in(p, r)->phase_q32;
     s_pre[1] = step_iter(p);
   }
   {
