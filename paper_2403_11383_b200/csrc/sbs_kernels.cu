@@ -1045,6 +1045,11 @@ __device__ __forceinline__ uint32_t cost_key(float J) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// inverse of cost_key (for the normalised costs)
+__device__ __forceinline__ float key_cost(uint32_t key) {
+  return __uint_as_float((key & 0x80000000u) ? (key ^ 0x80000000u) : ~key);
+}
+
 constexpr int kSelBlock = 1024;
 constexpr int kHistPad = 257;                       // per-warp histogram stride (bank-conflict free)
 constexpr int kSelHistWords = (kSelBlock / 32) * kHistPad;
@@ -1259,9 +1264,12 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
   uint32_t key[kSelKPT];
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i) key[i] = i < nk ? cost_key(J[k0 + i]) : 0xFFFFFFFFu;
+  if (blockIdx.x == 0) SBS_TS(2);
   digit16_pass(key, nk, 0u, 0u, 16, (uint32_t)K_e, hist, s_w, s_res);
+  if (blockIdx.x == 0) SBS_TS(3);
   const uint32_t hi = s_res[0], below_hi = s_res[1];
   digit16_pass(key, nk, 0xFFFF0000u, hi << 16, 0, (uint32_t)K_e - below_hi, hist, s_w, s_res);
+  if (blockIdx.x == 0) SBS_TS(4);
   const uint32_t T = (hi << 16) | s_res[0];
   const uint32_t n_eq = (uint32_t)K_e - below_hi - s_res[1];  // ties at T to take, lowest indices first
   uint32_t lt = 0, eq = 0;
@@ -1275,12 +1283,13 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
   const uint32_t lt_before = block_excl_scan(lt, s_w, &t1);
   uint32_t eq_before = block_excl_scan(eq, s_w, &t2);
   uint32_t pos = lt_before + min(eq_before, n_eq);
+  if (blockIdx.x == 0) SBS_TS(5);
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i)
     if (i < nk) {
       const bool take = key[i] < T || (key[i] == T && eq_before++ < n_eq);
       if (take) {
-        if (eJ) eJ[pos] = J[k0 + i];
+        if (eJ) eJ[pos] = key_cost(key[i]);  // (J itself up to NaN -> +inf, -0 -> +0)
         elite[pos++] = k_begin + k0 + i;
       }
     }
@@ -1290,33 +1299,40 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
 // records) into d: sdiag layout (J_min, k_best, theta1_best, sum J, n finite),
 // or, with part_layout, a rank record header [m, k, f, 0, 0, sum J, n finite, 0]
 static __device__ void merge_diag(const Params& p, int r, float* d, bool part_layout) {
-  const Best b = merge_argmin(p, r);
-  if (threadIdx.x < 32) {
-    float sj = 0.f, nf = 0.f;
-    for (int c = threadIdx.x; c < p.n_cta; c += 32) {
-      const float* pc = part_rec(p, r, c);
-      sj += __ldcg(pc + 5);
-      nf += __ldcg(pc + 6);
+  if (threadIdx.x >= 32) return;  // one warp, one load round trip; the other warps go on (no block barrier)
+  float m = kInf, sj = 0.f, nf = 0.f;
+  int mk = 0x7fffffff, mf = 0;
+  for (int c = threadIdx.x; c < p.n_cta; c += 32) {
+    const float* pc = part_rec(p, r, c);
+    const float mc = __ldcg(pc), sc = __ldcg(pc + 5), nc = __ldcg(pc + 6);
+    const int kc = __float_as_int(__ldcg(pc + 1)), fc = __float_as_int(__ldcg(pc + 2));
+    if (jk_less(mc, kc, m, mk)) {
+      m = mc;
+      mk = kc;
+      mf = fc;
     }
+    sj += sc;
+    nf += nc;
+  }
+  warp_argmin(m, mk, mf);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sj += __shfl_xor_sync(0xffffffffu, sj, o);
-      nf += __shfl_xor_sync(0xffffffffu, nf, o);
-    }
-    if (threadIdx.x == 0) {
-      d[0] = b.m;
-      d[1] = __int_as_float(b.k);
-      d[2] = __int_as_float(b.f);
-      if (part_layout) {
-        d[3] = 0.f;
-        d[4] = 0.f;
-        d[5] = sj;
-        d[6] = nf;
-        d[7] = 0.f;
-      } else {
-        d[3] = sj;
-        d[4] = nf;
-      }
+  for (int o = 16; o > 0; o >>= 1) {
+    sj += __shfl_xor_sync(0xffffffffu, sj, o);
+    nf += __shfl_xor_sync(0xffffffffu, nf, o);
+  }
+  if (threadIdx.x == 0) {
+    d[0] = m;
+    d[1] = __int_as_float(mk);
+    d[2] = __int_as_float(mf);
+    if (part_layout) {
+      d[3] = 0.f;
+      d[4] = 0.f;
+      d[5] = sj;
+      d[6] = nf;
+      d[7] = 0.f;
+    } else {
+      d[3] = sj;
+      d[4] = nf;
     }
   }
 }
@@ -1338,7 +1354,9 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_cons
   const int r = blockIdx.x, tid = threadIdx.x;
   const int64_t Ke = p.n_elite;
   float* hdr = MODE == SEL_EMIT ? emit + (size_t)r * p.ex_stride : p.sdiag + (size_t)r * 8;
+  if (blockIdx.x == 0) SBS_TS(0);
   merge_diag(p, r, hdr, MODE == SEL_EMIT);
+  if (blockIdx.x == 0) SBS_TS(1);
   const float* J = p.J + (size_t)r * p.K_local;
   int64_t K = p.K_local, kb = p.k_begin;
   if (MODE == SEL_MERGE) {
@@ -1355,6 +1373,7 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_cons
   if (SMALL) select_block_small(J, (int)K, (int)Ke, kb, el, eJ, sel_smem);
   else select_block(J, K, Ke, kb, el, eJ, sel_smem);
   __syncthreads();
+  if (blockIdx.x == 0) SBS_TS(6);
   if (MODE == SEL_EMIT) {
     float* o = emit + (size_t)r * p.ex_stride + kPartHdr;
     for (int64_t e = tid; e < Ke; e += blockDim.x) {
@@ -1935,6 +1954,11 @@ cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* i
   else sbs_select_raw_kernel<<<1, kSelBlock, smem, s>>>(J, K, K_e, idx);
   return cudaGetLastError();
 }
+#if defined(SBS_TIMING)  // experiments only
+extern "C" int sbs_debug_ts_common(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_sbs_ts, sizeof(g_sbs_ts));
+}
+#endif
 #endif  // SBS_TU_COMMON
 
 }  // namespace sbs
