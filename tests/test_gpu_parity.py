@@ -282,6 +282,53 @@ def test_batched_robots_match_oracle(B, orc):
         _check_outputs(outs[r], ro, cfg)
 
 
+@pytest.mark.parametrize("mode", ["cem", "naive", "mppi"])
+def test_batched_robots_two_steps_all_modes(B, orc, mode):
+    """R = 3 robots through the host path (captured graph, iteration counter in device
+    memory): two consecutive iterations against the oracle, per robot."""
+    R = 3
+    cfg = W.base_config(n_samples=600, n_robots=R, gait_adapt=1, mode=mode, n_elite=60 if mode == "cem" else 1)
+    rng = np.random.default_rng(11)
+    inputs = [W.robot_input(cfg, r, cmd=(rng.uniform(-.5, .5), rng.uniform(-.5, .5), 0), phase=int(rng.integers(0, 2**32)))
+              for r in range(R)]
+    c = B.Controller(cfg)
+    states = [W.initial_distribution(cfg) for _ in range(R)]
+    for r in range(R):
+        c.set_reference(r, inputs[r]["xref"])
+    for it in range(2):
+        status, outs = c.step(inputs)
+        Jg = c.debug_costs()
+        for r in range(R):
+            ro = orc.step(cfg, r, inputs[r], states[r])
+            _check_costs(Jg[r], ro.J)
+            if mode != "mppi" and _certified_near_tie(ro.J, 1 if mode == "naive" else cfg["n_elite"]):
+                continue
+            _check_outputs(outs[r], ro, cfg)
+            c.set_distribution(r, states[r]["mean"], states[r]["var"], states[r]["freq_idx"])  # oracle -> GPU
+        assert c.iter == it + 1
+
+
+def test_host_path_equals_device_path(B):
+    """sbs_step (one robot: inputs and reference inside the kernel parameters) and
+    sbs_step_device (inputs in device memory) run the same arithmetic: bitwise equal."""
+    import ctypes as C
+
+    import torch
+    for cfg, inputs in (W.config2(K=3000), W.config3("cem", K=3000), W.config3("naive", K=3000)):
+        a = _ctrl(B, cfg, inputs)
+        b = _ctrl(B, cfg, inputs)
+        d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
+        d_out = torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+        for _ in range(2):
+            _, oa = a.step(inputs)
+            b.step_device(d_in.data_ptr(), d_out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            ob = B.output_dict(B.sbs_output.from_buffer_copy(d_out.cpu().numpy().tobytes()), 48)
+            for key in ("mean", "var", "u0"):
+                np.testing.assert_array_equal(oa[0][key], ob[key])
+            assert oa[0]["iter"] == ob["iter"] and oa[0]["freq_idx"] == ob["freq_idx"]
+
+
 def test_determinism_and_checkpoint(B):
     cfg, inputs = W.config2(K=5000)
     a = _ctrl(B, cfg, inputs)
