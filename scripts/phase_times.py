@@ -16,7 +16,10 @@ for name, (cfg, inputs) in [("c1", W.config1()), ("c2", W.config2()), ("c3cem", 
     d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
     d_out = torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
     acc = []
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda") if os.environ.get("FLUSH") else None
     for it in range(30):
+        if flush is not None:
+            flush.zero_()
         c.step_device(d_in.data_ptr(), d_out.data_ptr(), 0)
         torch.cuda.synchronize()
         ts = (C.c_uint64 * 16)()
