@@ -769,6 +769,7 @@ int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
   if (R == 1 && c->P.H * 12 <= sbs::kInlineRefFloats && c->cfg.world == 1) {
     // inputs, reference and iteration counter ride in the kernel parameters: no copy node,
     // no graph (direct launches); outputs land in mapped pinned memory
+    CK(cudaEventSynchronize(c->blk_ev));  // a reference staged by sbs_set_reference_device has landed in h_xref
     Params saved = c->P;
     c->P.inline_in = 1;
     c->P.in_inline = in[0];

@@ -329,6 +329,24 @@ def test_host_path_equals_device_path(B):
             assert oa[0]["iter"] == ob["iter"] and oa[0]["freq_idx"] == ob["freq_idx"]
 
 
+def test_reference_from_device_memory(B):
+    """sbs_set_reference_device (device buffer, stream-ordered) is the same reference as
+    sbs_set_reference for both the host path and the device path."""
+    import torch
+    cfg, inputs = W.config2(K=2000)
+    xr = np.asarray(inputs[0]["xref"], dtype=np.float32)
+    a = _ctrl(B, cfg, inputs)
+    b = _ctrl(B, cfg, inputs)
+    b.set_reference(0, np.zeros_like(xr))                     # overwritten below
+    d_x = torch.from_numpy(xr.copy()).cuda()
+    b.set_reference_device(d_x.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    np.testing.assert_array_equal(b.get_reference(0), xr)
+    _, oa = a.step(inputs)
+    _, ob = b.step(inputs)
+    np.testing.assert_array_equal(oa[0]["mean"], ob[0]["mean"])
+    np.testing.assert_array_equal(a.debug_costs(), b.debug_costs())
+
+
 def test_determinism_and_checkpoint(B):
     cfg, inputs = W.config2(K=5000)
     a = _ctrl(B, cfg, inputs)
