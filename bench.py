@@ -295,7 +295,8 @@ def run_sbs(args):
                  "config3_cem": _time_config(B, W, C, np, torch, W.config3("cem"), steps=200, warmup=10,
                                              peak=peak, label="config3: CEM K_e=1000, K=10000, gait adaptation"),
                  "config5_batched": _time_config(B, W, C, np, torch, W.config5(), steps=20, warmup=3, peak=peak,
-                                                 label="config5: 4096 robots x 1024 samples, MPPI (1 GPU)")}
+                                                 label="config5: 4096 robots x 1024 samples, MPPI (1 GPU)"),
+                 "config5_closed_loop": _time_closed_loop(B, W, C, np, torch, W.config5(), n_iter=50)}
 
     line = None
     if rank == 0:
@@ -366,6 +367,37 @@ def _time_config(B, W, C, np, torch, cfg_inputs, steps, warmup, peak, label):
             "kernels_us": {k: 1e3 * v[0] / v[1] for k, v in kt.items() if v[1]},
             "rollout_roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                                  "frac": achieved / peak}}
+
+
+def _time_closed_loop(B, W, C, np, torch, cfg_inputs, n_iter):
+    """Config 5 as a batched closed loop (sbs_run_loop): every control step is the MPC
+    iteration for all robots plus the on-device plant / footholds / reference advance."""
+    cfg, inputs = cfg_inputs
+    R = len(inputs)
+    ctrl = B.Controller(cfg)
+    for r, inp in enumerate(inputs):
+        ctrl.set_reference(r, inp["xref"])
+    d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
+    d_out = torch.zeros(R * C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+    fallen = torch.zeros(R, dtype=torch.int32, device="cuda")
+    lc = W.loop_config()
+    s = torch.cuda.current_stream()
+    ctrl.run_loop(3, d_in.data_ptr(), d_out.data_ptr(), 0, 0, fallen.data_ptr(), 0, lc, s.cuda_stream)  # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    ctrl.run_loop(n_iter, d_in.data_ptr(), d_out.data_ptr(), 0, 0, fallen.data_ptr(), 0, lc, s.cuda_stream)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n_iter
+    K = cfg["n_samples"] * R
+    n_fallen = int(fallen.sum().item())
+    ctrl.close()
+    return {"workload": "config5 closed loop: 4096 robots x 1024 samples, MPPI + SRBD plant, Eq. 3 footholds, "
+                        "reference rebuild per control step (sbs_run_loop, one graph per step)",
+            "K_total": K, "control_steps": n_iter, "ms_per_control_step": ms,
+            "value": K * H / (ms * 1e-3), "unit": "sample-steps/s",
+            "robot_control_steps_per_s": R / (ms * 1e-3), "fallen": n_fallen}
 
 
 def main():
