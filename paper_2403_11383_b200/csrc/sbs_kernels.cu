@@ -1,16 +1,26 @@
 // sbs_kernels.cu -- sm_100a kernels of one SBS MPC iteration (arxiv 2403.11383).
 //
-//   sbs_rollout_kernel   steps a0-a4 (+ a5 partial for MPPI): warm shift, Philox
+//   sbs_rollout_kernel   steps a0-a4 (+ a5 / a6 tile epilogue): warm shift, Philox
 //                        sampling, contact sequence, GRF spline + cone, SRBD RK4,
 //                        cost; one thread per sample, everything in registers;
-//                        MPPI: online (min, sum w, sum w theta) partial per CTA.
-//   sbs_mppi_finalize    step a5/a7: merge the CTA partials, new mean, output.
-//   sbs_select_kernel    step a6: radix select of the K_e smallest (J, k).
-//   sbs_elite_kernel     step a6/a7: regenerate the elites' theta from the counter
-//                        RNG, elite mean / variance, output.
+//                        MPPI: online (min, sum w, sum w theta) record per CTA;
+//                        Naive/CEM: (J, k) argmin + finite-cost sums.  FUSED: the
+//                        last CTA of each robot merges the records and finishes
+//                        the iteration (MPPI a5/a7, Naive a6/a7).  Variants: SPLIT
+//                        (latency mode: 4 lanes per sample in the sampler), FC
+//                        (full-covariance sampling, L42).
+//   sbs_select_kernel    step a6 (CEM): exact radix select of the K_e smallest (J, k);
+//                        EMIT / MERGE modes for sample sharding (world > 1).
+//   sbs_elite_kernel     step a6/a7 (CEM): regenerate the elites' theta from the
+//                        counter RNG, elite mean / variance, output.
+//   sbs_cov_kernel       the same with a full covariance (elite covariance, Cholesky).
+//   sbs_mppi_finalize, sbs_argmin_emit_kernel, sbs_naive_finalize_kernel
+//                        world > 1: rank records and rank-order merges.
+//   sbs_debug_samples_kernel   the draws of given sample indices (tests).
+// The closed-loop advance kernel is in sbs_loop.cu.
 //
-// The rollout is FP32 CUDA-core work (not a contraction): it is bound by the FMA
-// pipe, not by HBM (4 bytes written per sample).  See DESIGN.md sec. 7.
+// The rollout is FP32 CUDA-core work (not a contraction): it is bound by FP32
+// issue and latency, not by HBM (4 bytes written per sample).  See DESIGN.md sec. 7.
 #include <float.h>
 #include <math.h>
 
