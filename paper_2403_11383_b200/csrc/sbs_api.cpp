@@ -266,10 +266,16 @@ int enqueue_records(sbs_ctx* c, cudaStream_t s, float* dst) {
   Params& P = c->P;
   P.iter = c->iter;
   const int mode = c->cfg.mode;
-  CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, mode, false, s); }));
-  if (mode == SBS_MPPI) CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_merge(P, dst, s); }));
-  else if (mode == SBS_NAIVE) CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_argmin_emit(P, dst, s); }));
-  else CK(timed(c, SBS_KERNEL_SELECT, s, [&] { return sbs::launch_select_emit(P, dst, s); }));
+  if (mode == SBS_CEM) {
+    CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, mode, false, s); }));
+    CK(timed(c, SBS_KERNEL_SELECT, s, [&] { return sbs::launch_select_emit(P, dst, s); }));
+    return SBS_OK;
+  }
+  // MPPI / Naive: one launch, the last CTA of each robot emits the rank record
+  P.emit = dst;
+  const cudaError_t e = timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, mode, true, s); });
+  P.emit = nullptr;
+  CK(e);
   return SBS_OK;
 }
 

@@ -91,6 +91,7 @@ struct Params {
   float* elite_J;             // [R][n_elite] costs of the elites (select kernel)
   float* cand;                // [R][world * n_elite] CEM world > 1: gathered candidate costs
   int ex_stride;              // floats per robot in a rank record (world > 1 exchange)
+  float* emit;                // non-null: the fused rollout's last CTA writes the rank record here (MPPI, Naive)
 };
 
 // closed loop (sbs_loop.cu)
@@ -111,14 +112,11 @@ cudaError_t launch_advance(const Params& p, const LoopArgs& a, sbs_input* in, co
 // mode: SBS_MPPI / SBS_NAIVE (fused: merge + finish in the last CTA; else records only), SBS_CEM (records only)
 cudaError_t launch_rollout(const Params& p, int mode, bool fused, cudaStream_t s);
 cudaError_t launch_mppi_finalize(const Params& p, cudaStream_t s);
-// merge this rank's CTA partials into one record per robot at dst[R][part_stride]
-cudaError_t launch_mppi_merge(const Params& p, float* dst, cudaStream_t s);
 cudaError_t launch_select(const Params& p, cudaStream_t s);
 // world > 1 CEM: rank record [8 | K_e J | K_e k] per robot at emit[R][ex_stride]; merge of the gathered records
 cudaError_t launch_select_emit(const Params& p, float* emit, cudaStream_t s);
 cudaError_t launch_select_merge(const Params& p, cudaStream_t s);
-// world > 1 Naive: rank argmin record per robot at emit[R][ex_stride]; merge of the gathered records + finish
-cudaError_t launch_argmin_emit(const Params& p, float* emit, cudaStream_t s);
+// world > 1 Naive: merge of the gathered rank argmin records + finish
 cudaError_t launch_naive_finalize(const Params& p, cudaStream_t s);
 cudaError_t launch_elite(const Params& p, cudaStream_t s);
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,

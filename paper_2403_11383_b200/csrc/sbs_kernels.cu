@@ -14,8 +14,9 @@
 //   sbs_elite_kernel     step a6/a7 (CEM): regenerate the elites' theta from the
 //                        counter RNG, elite mean / variance, output.
 //   sbs_cov_kernel       the same with a full covariance (elite covariance, Cholesky).
-//   sbs_mppi_finalize, sbs_argmin_emit_kernel, sbs_naive_finalize_kernel
-//                        world > 1: rank records and rank-order merges.
+//   sbs_mppi_finalize, sbs_naive_finalize_kernel
+//                        world > 1: rank-order merges of the gathered rank records
+//                        (the fused rollout's last CTA emits each rank's record).
 //   sbs_debug_samples_kernel   the draws of given sample indices (tests).
 // The closed-loop advance kernel is in sbs_loop.cu.
 //
@@ -727,6 +728,48 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
                one_pass ? s_pre : nullptr);
 }
 
+// merges robot r's records (the rollout's CTA records, or the gathered rank
+// records) into d: sdiag layout (J_min, k_best, theta1_best, sum J, n finite),
+// or, with part_layout, a rank record header [m, k, f, 0, 0, sum J, n finite, 0]
+static __device__ void merge_diag(const Params& p, int r, float* d, bool part_layout) {
+  if (threadIdx.x >= 32) return;  // one warp, one load round trip; the other warps go on (no block barrier)
+  float m = kInf, sj = 0.f, nf = 0.f;
+  int mk = 0x7fffffff, mf = 0;
+  for (int c = threadIdx.x; c < p.n_cta; c += 32) {
+    const float* pc = part_rec(p, r, c);
+    const float mc = __ldcg(pc), sc = __ldcg(pc + 5), nc = __ldcg(pc + 6);
+    const int kc = __float_as_int(__ldcg(pc + 1)), fc = __float_as_int(__ldcg(pc + 2));
+    if (jk_less(mc, kc, m, mk)) {
+      m = mc;
+      mk = kc;
+      mf = fc;
+    }
+    sj += sc;
+    nf += nc;
+  }
+  warp_argmin(m, mk, mf);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sj += __shfl_xor_sync(0xffffffffu, sj, o);
+    nf += __shfl_xor_sync(0xffffffffu, nf, o);
+  }
+  if (threadIdx.x == 0) {
+    d[0] = m;
+    d[1] = __int_as_float(mk);
+    d[2] = __int_as_float(mf);
+    if (part_layout) {
+      d[3] = 0.f;
+      d[4] = 0.f;
+      d[5] = sj;
+      d[6] = nf;
+      d[7] = 0.f;
+    } else {
+      d[3] = sj;
+      d[4] = nf;
+    }
+  }
+}
+
 // Naive UpdateMean (Alg. 3): the best sample theta* becomes the mean,
 // regenerated from the counter RNG; C unchanged.
 template <int P>
@@ -1027,8 +1070,13 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
   if (FUSED) {
     if (arrive_last(p.counter + r, gridDim.x)) {
       SBS_TS(5);
-      if (EPI == EPI_MPPI) mppi_merge_block<false>(p, r, nullptr, s_red, NR * (kBlock + 1));
-      else naive_finalize_block<P>(p, r, s);
+      if (p.emit) {  // world > 1: this rank's record per robot (the all-gather and rank-order merge follow)
+        if (EPI == EPI_MPPI) mppi_merge_block<true>(p, r, p.emit, s_red, NR * (kBlock + 1));
+        else merge_diag(p, r, p.emit + (size_t)r * p.ex_stride, true);
+      } else {
+        if (EPI == EPI_MPPI) mppi_merge_block<false>(p, r, nullptr, s_red, NR * (kBlock + 1));
+        else naive_finalize_block<P>(p, r, s);
+      }
       SBS_TS(6);
     }
   }
@@ -1305,47 +1353,6 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
     }
 }
 
-// merges robot r's records (the rollout's CTA records, or the gathered rank
-// records) into d: sdiag layout (J_min, k_best, theta1_best, sum J, n finite),
-// or, with part_layout, a rank record header [m, k, f, 0, 0, sum J, n finite, 0]
-static __device__ void merge_diag(const Params& p, int r, float* d, bool part_layout) {
-  if (threadIdx.x >= 32) return;  // one warp, one load round trip; the other warps go on (no block barrier)
-  float m = kInf, sj = 0.f, nf = 0.f;
-  int mk = 0x7fffffff, mf = 0;
-  for (int c = threadIdx.x; c < p.n_cta; c += 32) {
-    const float* pc = part_rec(p, r, c);
-    const float mc = __ldcg(pc), sc = __ldcg(pc + 5), nc = __ldcg(pc + 6);
-    const int kc = __float_as_int(__ldcg(pc + 1)), fc = __float_as_int(__ldcg(pc + 2));
-    if (jk_less(mc, kc, m, mk)) {
-      m = mc;
-      mk = kc;
-      mf = fc;
-    }
-    sj += sc;
-    nf += nc;
-  }
-  warp_argmin(m, mk, mf);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    sj += __shfl_xor_sync(0xffffffffu, sj, o);
-    nf += __shfl_xor_sync(0xffffffffu, nf, o);
-  }
-  if (threadIdx.x == 0) {
-    d[0] = m;
-    d[1] = __int_as_float(mk);
-    d[2] = __int_as_float(mf);
-    if (part_layout) {
-      d[3] = 0.f;
-      d[4] = 0.f;
-      d[5] = sj;
-      d[6] = nf;
-      d[7] = 0.f;
-    } else {
-      d[3] = sj;
-      d[4] = nf;
-    }
-  }
-}
 
 // Select kernels, one CTA per robot.
 //   SEL_LOCAL (world = 1): rollout records -> p.sdiag; K_e smallest of J -> p.elite, p.elite_J.
@@ -1399,10 +1406,6 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_cons
   }
 }
 
-// Naive with world > 1, before the all-gather: this rank's argmin record per robot
-__global__ void __launch_bounds__(128) sbs_argmin_emit_kernel(const __grid_constant__ Params p, float* emit) {
-  merge_diag(p, blockIdx.x, emit + (size_t)blockIdx.x * p.ex_stride, true);
-}
 
 __global__ void __launch_bounds__(kSelBlock) sbs_select_raw_kernel(const float* J, int64_t K, int64_t K_e,
                                                                    int64_t* idx) {
@@ -1894,11 +1897,6 @@ cudaError_t launch_naive_finalize(const Params& p, cudaStream_t s) {
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_argmin_emit(const Params& p, float* emit, cudaStream_t s) {
-  sbs_argmin_emit_kernel<<<p.R, 128, 0, s>>>(p, emit);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                  int* fidx, cudaStream_t s) {
   SBS_DISPATCH_P(p.P, debug_samples(p, robot, k0, n, z, theta, fidx, s));
@@ -1910,10 +1908,6 @@ cudaError_t launch_mppi_finalize(const Params& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_mppi_merge(const Params& p, float* dst, cudaStream_t s) {
-  sbs_mppi_finalize<true><<<p.R, 128, 0, s>>>(p, dst);
-  return cudaGetLastError();
-}
 
 static size_t select_smem(int64_t K) {
   if (K <= kSelSmallMax) return (size_t)kSelSmallSmemBytes;
