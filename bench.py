@@ -235,8 +235,11 @@ def run_sbs(args):
     ms = tot / args.steps
     value = K_total * H / (ms * 1e-3)
     per_sorted = sorted(per)
-    lat = {"p50": 1e3 * per_sorted[len(per) // 2], "p99": 1e3 * per_sorted[min(len(per) - 1, int(0.99 * len(per)))],
-           "mean": 1e3 * ms}
+    def pct(q):
+        return 1e3 * per_sorted[min(len(per) - 1, int(q * len(per)))]
+
+    lat = {"p5": pct(0.05), "p50": pct(0.5), "p95": pct(0.95), "p99": pct(0.99), "mean": 1e3 * ms,
+           "note": "per-iteration device time, L2 flushed before each; every 10th step carries per-kernel events"}
 
     # ---- roofline of the dominant kernel (rollout), timed live in the same region ----
     r_ms, r_n = ktimes["rollout"]
