@@ -1437,18 +1437,22 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   __shared__ RobotSmem s;
   __shared__ float s_mean[D], s_var[D];
   __shared__ float s_tot[2 * D + 1];
-  __shared__ __align__(16) float s_stage[16 * kEPartStride];
-  __shared__ float s_diag[2];
+  constexpr int kChunk = 32;  // elite records staged per round trip in the last CTA
+  __shared__ __align__(16) float s_stage[kChunk * kEPartStride];
+  __shared__ float s_diag[5];
   const int r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
+  const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
+  // the elite's index and cost are loaded with the robot inputs (one round trip)
+  const bool has_e = e < p.n_elite;
+  const int64_t k = has_e ? p.elite[(size_t)r * p.n_elite + e] : 0;
+  const float Je = has_e ? p.elite_J[(size_t)r * p.n_elite + e] : kInf;
   load_robot(p, r, s, false);
   __syncthreads();
   const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
-  const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
   float dev[4] = {0.f, 0.f, 0.f, 0.f};
   float n = 0.f;
-  if (e < p.n_elite) {
-    const int64_t k = p.elite[(size_t)r * p.n_elite + e];
-    if (p.elite_J[(size_t)r * p.n_elite + e] < kInf) {  // diverged samples never enter the moments (L17)
+  if (has_e) {
+    if (Je < kInf) {  // diverged samples never enter the moments (L17)
       float th4[4];
       sample_block(p, robot_g, k, q, s, th4);
 #pragma unroll
@@ -1478,14 +1482,16 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   if (!arrive_last(p.ecounter + r, gridDim.x)) return;
   // ---- last CTA: merge the elite records in order, finish the iteration ----
   __shared__ uint32_t s_pre[2];
+  const float* sd = p.sdiag + (size_t)r * 8;
   if (tid == 0) {  // issued with the record loads below
     s_pre[0] = robot_in(p, r)->phase_q32;
     s_pre[1] = step_iter(p);
+    for (int i = 0; i < 5; ++i) s_diag[i] = sd[i];  // rank-1 sample and diagnostics (select kernel)
   }
   {
-    float a0 = 0.f;  // row tid (2D + 1 <= blockDim = 3D / 4 * 32 / 12 ... = 8D)
-    for (int b0 = 0; b0 < (int)gridDim.x; b0 += 16) {
-      const int nb = min(16, (int)gridDim.x - b0);
+    float a0 = 0.f;  // row tid (2D + 1 <= blockDim = 8D); records summed in block order
+    for (int b0 = 0; b0 < (int)gridDim.x; b0 += kChunk) {
+      const int nb = min(kChunk, (int)gridDim.x - b0);
       stage_copy(s_stage, p.epart + ((size_t)r * gridDim.x + b0) * kEPartStride, nb * kEPartStride);
       __syncthreads();
       if (tid < 2 * D + 1)
@@ -1494,14 +1500,8 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
     }
     if (tid < 2 * D + 1) s_tot[tid] = a0;
   }
-  // rank-1 sample and diagnostics, merged from the rollout records by the select kernel
-  const float* sd = p.sdiag + (size_t)r * 8;
-  const Best b{sd[0], __float_as_int(sd[1]), __float_as_int(sd[2])};
-  if (tid == 0) {
-    s_diag[0] = sd[3];
-    s_diag[1] = sd[4];
-  }
   __syncthreads();
+  const Best b{s_diag[0], __float_as_int(s_diag[1]), __float_as_int(s_diag[2])};
   const float ne = s_tot[D];
   const bool all_div = !(ne > 0.f);
   const float inv = all_div ? 0.f : 1.0f / ne;
@@ -1526,7 +1526,7 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
     p.best[r] = b.k;
   }
   write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, b.m,
-               s_diag[1] > 0.f ? s_diag[0] / s_diag[1] : kInf, ne, ne, (int)((float)p.K_global - s_diag[1]), s_pre);
+               s_diag[4] > 0.f ? s_diag[3] / s_diag[4] : kInf, ne, ne, (int)((float)p.K_global - s_diag[4]), s_pre);
 }
 
 // ---------------------------------------------------------------------------
