@@ -11,7 +11,8 @@
  * SRBD model (Eq. 1) for H steps while accumulating the cost of
  * P:342-351, and reduce the samples into the next distribution by MPPI
  * (Alg. 4) or by elite selection (CEM = Alg. 1 with K_e elites and
- * a diagonal covariance refit, Naive = Alg. 3, K_e = 1, C unchanged).  The
+ * a diagonal or, with full_cov, a full covariance refit; Naive = Alg. 3,
+ * K_e = 1, C unchanged).  The
  * updated mean is the control: its first knot, masked by the contact
  * flags and projected onto the friction cone, is returned as u0.
  *
@@ -145,7 +146,7 @@ typedef struct sbs_output {
   float omega;            /* MPPI: sum of weights Omega; CEM/Naive: number of elites used */
   float ess;              /* MPPI effective sample size Omega^2 / sum w^2 */
   int32_t n_diverged;     /* rollouts with J = +inf */
-  float device_us;        /* device time of the step (sbs_step only; 0 otherwise) */
+  float device_us;        /* device time of the step, CUDA events (sbs_step only; 0 otherwise) */
   float mean[SBS_MAX_D];  /* new mean theta2 (first D entries valid) */
   float var[SBS_MAX_D];   /* new diagonal covariance */
 } sbs_output;
@@ -176,7 +177,12 @@ int sbs_set_iter(sbs_ctx* ctx, uint32_t iter);
 /* One iteration for all R robots.  in/out: host arrays of R entries.
  * Synchronous: outputs are valid on return.  Validates x0 on the host
  * (SBS_ERR_NONFINITE / SBS_ERR_SINGULAR).  Returns SBS_WARN_ALL_DIVERGED if
- * any robot had every rollout diverge.  iter += 1 on OK or WARN. */
+ * any robot had every rollout diverge.  iter += 1 on OK or WARN.
+ * Transport: with R = 1 (and H <= 16) the inputs, the staged reference and the
+ * iteration counter travel inside the kernel parameters (direct launch, no
+ * copy); otherwise one pinned block [iter | inputs | references] is copied up
+ * by a captured CUDA graph.  The finishing kernel writes the outputs straight
+ * into the context's mapped pinned memory; they are copied to `out` on return. */
 int sbs_step(sbs_ctx* ctx, const sbs_input* in, sbs_output* out);
 
 /* Same iteration with device-resident inputs/outputs (R entries each),
