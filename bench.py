@@ -128,6 +128,26 @@ def oracle_rate(K_sample: int, n_steps: int, warmup: int = 1):
     return K_sample * H * n_steps / tot, times
 
 
+def _oracle_worker(args):
+    K_sample, n_steps = args
+    rate, times = oracle_rate(K_sample, n_steps, warmup=0)
+    return K_sample * H * n_steps, sum(times)
+
+
+def oracle_rate_all_cores(K_sample: int, n_steps: int):
+    """The same oracle iteration run concurrently in one process per host core (each on its
+    own K_sample-sample slice-sized iteration): the oracle as it stands, parallelised by the
+    harness only.  Returns (sample-steps/s over the wall time, processes)."""
+    import multiprocessing as mp
+    n = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    t = time.perf_counter()
+    with ctx.Pool(n) as pool:
+        res = pool.map(_oracle_worker, [(K_sample, n_steps)] * n)
+    wall = time.perf_counter() - t
+    return sum(r[0] for r in res) / wall, n
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -310,6 +330,12 @@ def run_sbs(args):
             cpu = {"value": cv, "unit": "sample-steps/s", "cores": 1, "kind": "oracle",
                    "sample": f"{len(ctimes)} oracle iterations of config 2 on {K_s} of its 10000 samples "
                              f"({sum(ctimes):.1f} s, single thread)"}
+            try:  # the same oracle on every host core (one process each), for context
+                av, ncores = oracle_rate_all_cores(2000, 150)
+                cpu["all_cores"] = {"value": av, "unit": "sample-steps/s", "cores": ncores,
+                                    "sample": f"{ncores} processes x 150 oracle iterations of config 2 on 2000 samples (wall clock incl. process start)"}
+            except Exception as exc:  # noqa: BLE001
+                cpu["all_cores"] = {"error": str(exc)[:200]}
         line = {
             "metric": "sample-steps/sec and MPC-iteration latency (us) at N samples",
             "value": value, "unit": "sample-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
