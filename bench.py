@@ -7,7 +7,9 @@ Workload at N = 1: BASELINE.json configs[1] -- MPPI at the paper's settings,
 K = 10,000 samples, H = 12, dt = 0.02 s, fixed trot.  With N > 1
 (torchrun, one process per GPU) every rank owns 10,000 samples of one
 K = 10,000 N MPPI iteration (weak scaling): the ranks' (min, sum w, sum w theta)
-partials are combined by one NCCL all-gather inside the library.
+records are exchanged over peer memory (each rank's finishing CTA stores its
+record into every peer's buffer over NVLink; the peers' streams wait on a flag)
+with an NCCL all-gather as the fallback.
 
 One JSON line on rank 0.  `value` = sample-steps/s (K_total H / device time
 per iteration, inputs resident in HBM, L2 flushed between timed iterations);
@@ -208,6 +210,19 @@ def run_sbs(args):
         nccl_id = obj[0]
     ctrl = B.Controller(cfg, device=local, rank=rank, world=world, nccl_id=nccl_id)
     ctrl.set_reference(0, inputs[0]["xref"])
+    exchange = "none"
+    if world > 1:
+        # rank records exchanged over peer memory (the finishing CTA stores into every peer's
+        # buffer over NVLink; streams wait on the peers' flags); NCCL all-gather as fallback
+        try:
+            handle, _ = ctrl.peer_handle()
+            handles = [None] * world
+            dist.all_gather_object(handles, handle)
+            ctrl.peer_connect(handles=handles)
+            exchange = "peer memory (NVLink stores + stream flag waits)"
+        except Exception as exc:  # noqa: BLE001
+            exchange = f"NCCL all-gather (peer exchange unavailable: {str(exc)[:80]})"
+        dist.barrier()
     in_arr = B.make_inputs(inputs)
     d_in = torch.from_numpy(np.frombuffer(bytes(in_arr), dtype=np.uint8).copy()).cuda()
     d_out = torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
@@ -344,7 +359,7 @@ def run_sbs(args):
             "config": {"workload": "config2: MPPI, K=10000 samples per GPU, H=12, dt=0.02 s, fixed trot 1.3 Hz, "
                                    "cmd 0.5 m/s (BASELINE.json configs[1])",
                        "K_total": K_total, "K_per_gpu": K_PER_GPU, "H": H, "mode": "mppi",
-                       "parallelism": f"samples sharded over {world} GPU(s)" + (" + NCCL all-gather" if world > 1 else ""),
+                       "parallelism": f"samples sharded over {world} GPU(s)" + (f", rank records by {exchange}" if world > 1 else ""),
                        "l2": "flushed between timed iterations (256 MiB memset, outside the events)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "other_configs": extra,
             "gpu_launches": int(ctrl.launches_per_step() * args.steps), "clocks": clk,

@@ -211,6 +211,22 @@ int sbs_step_device(sbs_ctx* ctx, const sbs_input* d_in, sbs_output* d_out, void
  * same with one ncclAllGather in between.  Noise, costs, elites and (MPPI
  * aside, whose sums regroup) the new distribution are independent of world. */
 int sbs_record_floats(const sbs_ctx* ctx);
+
+/* Peer-memory exchange of the rank records (world > 1, one process per GPU of a
+ * node, or several contexts in one process), in place of the NCCL all-gather.
+ * Each rank calls sbs_peer_handle (its exchange buffer as a CUDA IPC handle, and
+ * its device address for same-process use); the caller exchanges them (e.g. a
+ * torch.distributed all_gather_object) and calls sbs_peer_connect with either the
+ * addresses (same process; peer access is enabled) or the IPC handles [world][64].
+ * From then on every sbs_step / sbs_step_device has the rank's last record-writing
+ * CTA store the rank's records straight into every peer's buffer (NVLink stores,
+ * system-scope fence, then a per-rank flag = exchange sequence number), and the
+ * stream waits in the GPU front-end (cuStreamWaitValue32, no SM held) for the
+ * peers' flags before the rank-order merge.  Two buffers alternate, so a fast rank
+ * never overwrites records a slower peer is still merging.  Collective: every rank
+ * steps in the same order.  world <= 8. */
+int sbs_peer_handle(sbs_ctx* ctx, uint8_t handle[64], void** base);
+int sbs_peer_connect(sbs_ctx* ctx, void* const* bases, const uint8_t* handles);
 int sbs_step_records(sbs_ctx* ctx, const sbs_input* d_in, float* d_rec, void* stream);
 int sbs_finish_records(sbs_ctx* ctx, const float* d_recs, const sbs_input* d_in, sbs_output* d_out, void* stream);
 

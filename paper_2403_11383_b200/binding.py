@@ -125,6 +125,8 @@ def load_library(path: str = LIB_PATH):
         "sbs_launches_per_step": ([ctxp], C.c_int),
         "sbs_record_floats": ([ctxp], C.c_int),
         "sbs_step_records": ([ctxp, vp, vp, vp], C.c_int),
+        "sbs_peer_handle": ([ctxp, P(C.c_uint8), P(vp)], C.c_int),
+        "sbs_peer_connect": ([ctxp, P(vp), P(C.c_uint8)], C.c_int),
         "sbs_finish_records": ([ctxp, vp, vp, vp, vp], C.c_int),
         "sbs_set_covariance": ([ctxp, C.c_int32, P(C.c_float)], C.c_int),
         "sbs_get_cholesky": ([ctxp, C.c_int32, P(C.c_float)], C.c_int),
@@ -297,6 +299,23 @@ class Controller:
     def step_records(self, d_in: int, d_rec: int, stream: int = 0):
         return self._check(self.L.sbs_step_records(self.ctx, C.c_void_p(d_in), C.c_void_p(d_rec),
                                                    C.c_void_p(stream)))
+
+    # ---- peer-memory exchange (replaces the NCCL all-gather) -----------------------
+    def peer_handle(self):
+        """(IPC handle bytes, device address) of this rank's exchange buffer."""
+        h = (C.c_uint8 * 64)()
+        base = C.c_void_p()
+        self._check(self.L.sbs_peer_handle(self.ctx, h, C.byref(base)))
+        return bytes(h), int(base.value or 0)
+
+    def peer_connect(self, bases=None, handles=None):
+        """bases: every rank's device address (same process), or handles: every rank's IPC handle."""
+        if bases is not None:
+            arr = (C.c_void_p * len(bases))(*bases)
+            return self._check(self.L.sbs_peer_connect(self.ctx, arr, None))
+        blob = b"".join(handles)
+        harr = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        return self._check(self.L.sbs_peer_connect(self.ctx, None, harr))
 
     def finish_records(self, d_recs: int, d_in: int, d_out: int, stream: int = 0):
         return self._check(self.L.sbs_finish_records(self.ctx, C.c_void_p(d_recs), C.c_void_p(d_in),

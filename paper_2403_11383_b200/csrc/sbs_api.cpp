@@ -62,6 +62,22 @@ constexpr int kNcclFloat32 = 7;  // ncclFloat32 in nccl.h
 
 thread_local std::string g_create_err;
 
+// cuStreamWaitValue32 (driver API, resolved through the runtime): a stream waits in the
+// GPU front-end until a 32-bit word reaches a value (GEQ, wrap-around safe)
+typedef int (*PFN_WaitValue32)(void* stream, unsigned long long addr, uint32_t value, unsigned int flags);
+PFN_WaitValue32 g_wait_fn = nullptr;
+int g_wait_value32(cudaStream_t s, const uint32_t* addr, uint32_t value) {
+  if (!g_wait_fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return -1;
+    g_wait_fn = reinterpret_cast<PFN_WaitValue32>(fn);
+  }
+  return g_wait_fn((void*)s, (unsigned long long)(uintptr_t)addr, value, 0x0 /*CU_STREAM_WAIT_VALUE_GEQ*/);
+}
+
 }  // namespace
 
 struct sbs_ctx {
@@ -76,7 +92,15 @@ struct sbs_ctx {
   float* d_xref = nullptr;
   float* d_J = nullptr;
   float* d_part = nullptr;
-  float* d_gather = nullptr;  // [world][R][ex_stride] (world > 1)
+  float* d_gather = nullptr;  // [world][R][ex_stride] (world > 1), inside d_xbuf
+  char* d_xbuf = nullptr;      // world > 1: exchange buffer [gather 0 | gather 1 | flags[kMaxWorld] uint32]
+  size_t xgather_bytes = 0;    // (aligned) bytes of one gather buffer; peers alternate between the two
+  size_t xflags_off = 0;
+  std::vector<char*> peer_base;  // every rank's exchange buffer, as addressable from this device
+  uint32_t* d_xflags = nullptr;  // flags[j] = last exchange sequence number published by rank j
+  bool peer = false;             // rank records exchanged over peer memory (sbs_peer_connect)
+  uint32_t xseq = 0;             // exchange sequence number (identical on every rank)
+  std::vector<void*> ipc_opened; // peer buffers opened with cudaIpcOpenMemHandle
   float* d_eJ = nullptr;      // [R][K_e] elite costs
   float* d_L = nullptr;       // [R][D][D] Cholesky factors (full_cov)
   float* d_cand = nullptr;    // [R][world][K_e] CEM world > 1 candidates
@@ -302,10 +326,33 @@ int enqueue_step(sbs_ctx* c, cudaStream_t s) {
   Params& P = c->P;
   P.iter = c->iter;
   const int mode = c->cfg.mode;
-  if (c->cfg.world > 1) {  // rank record -> all-gather -> merge in rank order
-    if (c->external) return fail(c, SBS_ERR_STATE, "external exchange: use sbs_step_records / sbs_finish_records");
+  if (c->cfg.world > 1) {  // rank record -> exchange -> merge in rank order
     const size_t n = (size_t)P.R * P.ex_stride;
     float* mine = c->d_gather + (size_t)c->cfg.rank * n;
+    if (c->peer) {
+      // the publishing CTA stores this rank's records into every peer's gather buffer and
+      // raises the peer's flag; this stream waits (front-end, no SM) for the peers' flags
+      // (two gather buffers alternate with the sequence number: a rank publishing step t + 1
+      // cannot overwrite what a slower peer still reads for step t)
+      const uint32_t seq = ++c->xseq;
+      const size_t par = (seq & 1u) * c->xgather_bytes;
+      float* gat = reinterpret_cast<float*>(c->d_xbuf + par);
+      P.n_peers = c->cfg.world;
+      P.my_rank = c->cfg.rank;
+      P.flag_value = seq;
+      for (int j = 0; j < c->cfg.world; ++j) P.peer_gather[j] = reinterpret_cast<float*>(c->peer_base[j] + par);
+      int rc = enqueue_records(c, s, gat + (size_t)c->cfg.rank * n);
+      P.n_peers = 0;
+      if (rc != SBS_OK) return rc;
+      static const bool no_wait = getenv("SBS_PEER_NOWAIT") && atoi(getenv("SBS_PEER_NOWAIT")) != 0;  // debugging
+      for (int j = 0; j < c->cfg.world && !no_wait; ++j) {
+        if (j == c->cfg.rank) continue;
+        const int r2 = g_wait_value32(s, c->d_xflags + j, seq);
+        if (r2 != 0) return fail(c, SBS_ERR_CUDA, "cuStreamWaitValue32 failed");
+      }
+      return enqueue_finish(c, s, gat);
+    }
+    if (c->external) return fail(c, SBS_ERR_STATE, "external exchange: use sbs_step_records / sbs_finish_records");
     int rc = enqueue_records(c, s, mine);
     if (rc != SBS_OK) return rc;
     rc = g_nccl.all_gather(mine, c->d_gather, n, kNcclFloat32, c->comm, s);
@@ -361,8 +408,9 @@ void sbs_destroy(sbs_ctx* c) {
   cudaSetDevice(c->cfg.device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
+  for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
   for (void* p : {(void*)c->d_mean, (void*)c->d_var, (void*)c->d_fidx, (void*)c->d_J,
-                  (void*)c->d_part, (void*)c->d_gather, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart, (void*)c->d_sdiag, (void*)c->d_eJ, (void*)c->d_cand, (void*)c->d_L,
+                  (void*)c->d_part, (void*)c->d_xbuf, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart, (void*)c->d_sdiag, (void*)c->d_eJ, (void*)c->d_cand, (void*)c->d_L,
                   (void*)c->d_out})
     if (p) cudaFree(p);
   if (c->h_out) cudaFreeHost(c->h_out);  // (h_in and h_xref point into h_blk)
@@ -538,8 +586,15 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaEventRecord(c->blk_ev, c->stream));
   CKC(cudaMalloc(&c->d_J, (size_t)R * P.K_local * sizeof(float)));
   CKC(cudaMalloc(&c->d_part, (size_t)R * P.n_cta * P.part_stride * sizeof(float)));
-  if (cfg->world > 1)
-    CKC(cudaMalloc(&c->d_gather, (size_t)cfg->world * R * P.ex_stride * sizeof(float)));
+  if (cfg->world > 1) {
+    const size_t gbytes = (size_t)cfg->world * R * P.ex_stride * sizeof(float);
+    c->xgather_bytes = (gbytes + 255) / 256 * 256;
+    c->xflags_off = 2 * c->xgather_bytes;
+    CKC(cudaMalloc(&c->d_xbuf, c->xflags_off + sbs::kMaxWorld * sizeof(uint32_t)));  // (2 gathers + flags)
+    CKC(cudaMemset(c->d_xbuf, 0, c->xflags_off + sbs::kMaxWorld * sizeof(uint32_t)));
+    c->d_gather = reinterpret_cast<float*>(c->d_xbuf);
+    c->d_xflags = reinterpret_cast<uint32_t*>(c->d_xbuf + c->xflags_off);
+  }
   if (P.n_elite > 0) {
     CKC(cudaMalloc(&c->d_elite, (size_t)R * P.n_elite * sizeof(int64_t)));
     CKC(cudaMalloc(&c->d_eJ, (size_t)R * P.n_elite * sizeof(float)));
@@ -548,8 +603,8 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
     CKC(cudaMalloc(&c->d_cand, (size_t)R * cfg->world * P.n_elite * sizeof(float)));
   CKC(cudaMalloc(&c->d_best, R * sizeof(int64_t)));
   CKC(cudaMalloc(&c->d_status, R * sizeof(int)));
-  CKC(cudaMalloc(&c->d_counter, 2 * R * sizeof(int)));
-  CKC(cudaMemset(c->d_counter, 0, 2 * R * sizeof(int)));
+  CKC(cudaMalloc(&c->d_counter, (2 * R + 1) * sizeof(int)));  // rollout, elite, peer-publish arrival counters
+  CKC(cudaMemset(c->d_counter, 0, (2 * R + 1) * sizeof(int)));
   P.n_eblk = P.n_elite > 0 ? (int)((P.n_elite + 31) / 32) : 1;  // 32 elites per elite-kernel CTA
   P.full_cov = cfg->full_cov ? 1 : 0;
   const int erec = P.full_cov ? std::max(sbs::kEPartStride, sbs::fc_record_floats(D)) : sbs::kEPartStride;
@@ -592,6 +647,7 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.status = c->d_status;
   P.counter = c->d_counter;
   P.ecounter = c->d_counter + R;
+  P.gcounter = c->d_counter + 2 * R;
   P.epart = c->d_epart;
   P.sdiag = c->d_sdiag;
   P.elite_J = c->d_eJ;
@@ -857,6 +913,66 @@ int sbs_step_device(sbs_ctx* c, const sbs_input* d_in, sbs_output* d_out, void* 
 }
 
 int sbs_record_floats(const sbs_ctx* c) { return c ? c->P.ex_stride : 0; }
+
+int sbs_peer_handle(sbs_ctx* c, uint8_t handle[64], void** base) {
+  if (!c) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (c->cfg.world < 2) return fail(c, SBS_ERR_STATE, "peer exchange needs world > 1");
+  if (c->cfg.world > sbs::kMaxWorld) return fail(c, SBS_ERR_INVALID_ARG, "peer exchange supports at most 8 ranks");
+  CK(cudaSetDevice(c->cfg.device));
+  if (handle) {
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c->d_xbuf));
+    memcpy(handle, &h, 64);
+  }
+  if (base) *base = c->d_xbuf;
+  return SBS_OK;
+}
+
+int sbs_debug_xflags(sbs_ctx* c, uint32_t* flags) {
+  if (!c || !flags || !c->d_xflags) return SBS_ERR_INVALID_ARG;
+  CK(cudaSetDevice(c->cfg.device));
+  CK(cudaMemcpyAsync(flags, c->d_xflags, sbs::kMaxWorld * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return SBS_OK;
+}
+
+int sbs_peer_connect(sbs_ctx* c, void* const* bases, const uint8_t* handles) {
+  if (!c || (!bases && !handles)) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  const int W = c->cfg.world, me = c->cfg.rank;
+  if (W < 2 || W > sbs::kMaxWorld) return fail(c, SBS_ERR_STATE, "peer exchange needs 2 <= world <= 8");
+  CK(cudaSetDevice(c->cfg.device));
+  if (g_wait_value32(c->stream, c->d_xflags + me, 0) != 0)  // probes cuStreamWaitValue32 (the own flag is >= 0)
+    return fail(c, SBS_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  CK(cudaStreamSynchronize(c->stream));
+  c->peer_base.clear();
+  for (int j = 0; j < W; ++j) {
+    char* b = nullptr;
+    if (j == me) {
+      b = c->d_xbuf;
+    } else if (bases) {
+      b = static_cast<char*>(bases[j]);  // same-process contexts (tests, one process driving several GPUs)
+      int dev_other = -1;
+      cudaPointerAttributes pa;
+      if (cudaPointerGetAttributes(&pa, b) == cudaSuccess) dev_other = pa.device;
+      if (dev_other >= 0 && dev_other != c->cfg.device) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(dev_other, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+        (void)cudaGetLastError();
+      }
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, handles + 64 * (size_t)j, 64);
+      void* q = nullptr;
+      CK(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_opened.push_back(q);
+      b = static_cast<char*>(q);
+    }
+    c->peer_base.push_back(b);
+    c->P.peer_flags[j] = reinterpret_cast<uint32_t*>(b + c->xflags_off);
+  }
+  c->peer = true;
+  return SBS_OK;
+}
 
 int sbs_step_records(sbs_ctx* c, const sbs_input* d_in, float* d_rec, void* stream) {
   if (!c || !d_in || !d_rec) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
@@ -1182,7 +1298,7 @@ int sbs_kernel_times(sbs_ctx* c, double* total_ms, int64_t* launches) {
 
 int sbs_launches_per_step(const sbs_ctx* c) {
   if (!c) return 0;
-  if (c->cfg.world > 1) return c->cfg.mode == SBS_CEM ? 4 : 2;  // + one ncclAllGather
+  if (c->cfg.world > 1) return c->cfg.mode == SBS_CEM ? 4 : 2;  // + the exchange (peer stores or ncclAllGather)
   return c->cfg.mode == SBS_CEM ? 3 : 1;
 }
 

@@ -9,6 +9,7 @@
 namespace sbs {
 
 constexpr int kBlock = 128;         // samples per tile = threads per rollout CTA
+constexpr int kMaxWorld = 8;               // ranks of one node (peer-memory exchange)
 constexpr int kInlineRefFloats = 16 * 12;  // host path, R = 1, H <= 16: inputs and reference ride in the kernel parameters
 constexpr int kSplitLanes = 4;      // latency-mode (SPLIT) rollout: lanes per sample in the sampler phase
 constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, nfin, pad]
@@ -92,6 +93,15 @@ struct Params {
   float* cand;                // [R][world * n_elite] CEM world > 1: gathered candidate costs
   int ex_stride;              // floats per robot in a rank record (world > 1 exchange)
   float* emit;                // non-null: the fused rollout's last CTA writes the rank record here (MPPI, Naive)
+  // --- peer-memory exchange (world > 1 without NCCL): after the last robot's record is
+  //     written, the publishing CTA copies [R][ex_stride] into every peer's gather slot
+  //     (NVLink stores), fences at system scope and raises the peer's flag [my_rank] ---
+  int n_peers;                // 0: no peer publishing
+  int my_rank;
+  uint32_t flag_value;        // exchange sequence number of this iteration
+  int* gcounter;              // arrival counter of the robots' record writers (re-armed to 0)
+  float* peer_gather[kMaxWorld];
+  uint32_t* peer_flags[kMaxWorld];
 };
 
 // closed loop (sbs_loop.cu)

@@ -844,6 +844,28 @@ __device__ __forceinline__ bool arrive_last(int* counter, int n) {
   return s_last;
 }
 
+// Peer-memory exchange of the rank records (world > 1 without NCCL):
+// called by every CTA that completed a robot's rank record; the last of them
+// copies this rank's records [R][ex_stride] (p.emit = its own gather slot) into
+// every peer's gather buffer over NVLink, fences at system scope and raises the
+// peer's flag for this rank.  The peers' streams wait on those flags in the
+// front-end (cuStreamWaitValue32), not in a kernel.
+static __device__ void publish_to_peers(const Params& p) {
+  if (p.n_peers == 0 || !arrive_last(p.gcounter, p.R)) return;
+  const size_t n = (size_t)p.R * p.ex_stride;
+  for (int j = 0; j < p.n_peers; ++j) {
+    if (j == p.my_rank) continue;
+    float* dst = p.peer_gather[j] + (size_t)p.my_rank * n;
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldcg(p.emit + i);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int j = 0; j < p.n_peers; ++j)
+      if (j != p.my_rank) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.peer_flags[j] + p.my_rank), "r"(p.flag_value) : "memory");
+  }
+}
+
 // ---------------------------------------------------------------------------
 // sbs_rollout_kernel: grid (n_cta, R), block kBlock.  CTA c processes tiles c,
 // c + n_cta, ... of its robot's K_local samples and leaves one partial record.
@@ -1070,9 +1092,10 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
   if (FUSED) {
     if (arrive_last(p.counter + r, gridDim.x)) {
       SBS_TS(5);
-      if (p.emit) {  // world > 1: this rank's record per robot (the all-gather and rank-order merge follow)
+      if (p.emit) {  // world > 1: this rank's record per robot (the exchange and rank-order merge follow)
         if (EPI == EPI_MPPI) mppi_merge_block<true>(p, r, p.emit, s_red, NR * (kBlock + 1));
         else merge_diag(p, r, p.emit + (size_t)r * p.ex_stride, true);
+        publish_to_peers(p);
       } else {
         if (EPI == EPI_MPPI) mppi_merge_block<false>(p, r, nullptr, s_red, NR * (kBlock + 1));
         else naive_finalize_block<P>(p, r, s);
@@ -1397,6 +1420,7 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_cons
       o[e] = eJ[e];
       o[Ke + e] = __int_as_float((int)el[e]);
     }
+    publish_to_peers(p);
   }
   if (MODE == SEL_MERGE) {
     for (int64_t e = tid; e < Ke; e += blockDim.x) {
@@ -1850,6 +1874,12 @@ cudaError_t PEntry<P>::prepare() {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_debug_samples_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  // load every remaining kernel of this P now: with CUDA's lazy module loading the first
+  // launch of a kernel can wait for the device, which must never happen behind a stream
+  // that waits on a peer's flag (peer-memory exchange)
+  cudaFuncAttributes fa;
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, sbs_elite_kernel<P>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, sbs_naive_finalize_kernel<P>);
   return e;
 }
 
@@ -1931,6 +1961,9 @@ cudaError_t prepare_kernels(int P) {
   if (e == cudaSuccess) e = set_select_attr<SEL_EMIT, false>();
   if (e == cudaSuccess) e = set_select_attr<SEL_MERGE, true>();
   if (e == cudaSuccess) e = set_select_attr<SEL_MERGE, false>();
+  cudaFuncAttributes fa;  // (lazy loading: see PEntry<P>::prepare)
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, sbs_mppi_finalize<false>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, sbs_mppi_finalize<true>);
   if (e != cudaSuccess || P == 0) return e;
   SBS_DISPATCH_P(P, prepare());
   return cudaErrorInvalidValue;
@@ -1946,7 +1979,9 @@ static cudaError_t launch_select_t(const Params& p, int64_t K, float* emit, cuda
 
 cudaError_t launch_select(const Params& p, cudaStream_t s) { return launch_select_t<SEL_LOCAL>(p, p.K_local, nullptr, s); }
 cudaError_t launch_select_emit(const Params& p, float* emit, cudaStream_t s) {
-  return launch_select_t<SEL_EMIT>(p, p.K_local, emit, s);
+  Params q = p;
+  q.emit = emit;  // (the peer publisher copies from here)
+  return launch_select_t<SEL_EMIT>(q, q.K_local, emit, s);
 }
 cudaError_t launch_select_merge(const Params& p, cudaStream_t s) {
   return launch_select_t<SEL_MERGE>(p, (int64_t)p.n_cta * p.n_elite, nullptr, s);

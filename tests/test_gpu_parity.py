@@ -511,3 +511,54 @@ def test_sharded_cem_rejects_too_few_samples_per_rank(B):
     cfg, _ = W.config3("cem", K=1000)
     with pytest.raises(Exception):
         B.Controller(dict(cfg, n_elite=600), rank=0, world=2)
+
+
+@pytest.mark.parametrize("mode,K,world,ke", [("mppi", 10000, 2, 1), ("mppi", 65536, 4, 1), ("naive", 6000, 2, 1),
+                                             ("cem", 12000, 3, 800)])
+def test_peer_memory_exchange_matches_single_gpu(B, orc, mode, K, world, ke):
+    """The rank-record exchange over peer memory (finishing CTA stores into every peer's
+    buffer + flag; streams wait on the flags in the front end; no NCCL), here with `world`
+    contexts of one process on one GPU, each on its own stream and enqueued in rank order
+    (the waits are stream-front-end waits, no kernel waits on another).  Three consecutive
+    iterations (both exchange buffers); every rank agrees bitwise with the others, and with
+    world = 1 (CEM / Naive bitwise, MPPI within 1e-5: its cross-rank sums regroup)."""
+    import ctypes as C
+
+    import torch
+    if mode == "mppi":
+        cfg, inputs = W.config2(K=K)
+    else:
+        cfg, inputs = W.config3(mode, K=K)
+        cfg = dict(cfg, n_elite=ke)
+    d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
+    ranks = [B.Controller(cfg, rank=g, world=world) for g in range(world)]
+    bases = [c.peer_handle()[1] for c in ranks]
+    for c in ranks:
+        c.set_reference(0, inputs[0]["xref"])
+        c.peer_connect(bases=bases)
+    streams = [torch.cuda.Stream() for _ in ranks]
+    outs = [torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda") for _ in ranks]
+    single = B.Controller(cfg)
+    single.set_reference(0, inputs[0]["xref"])
+    torch.cuda.synchronize()
+    for it in range(3):
+        for g, c in enumerate(ranks):
+            c.step_device(d_in.data_ptr(), outs[g].data_ptr(), streams[g].cuda_stream)
+        torch.cuda.synchronize()
+        _, so = single.step(inputs)
+        res = [B.output_dict(B.sbs_output.from_buffer_copy(o.cpu().numpy().tobytes()), 48) for o in outs]
+        for o in res[1:]:
+            np.testing.assert_array_equal(o["mean"], res[0]["mean"])
+            np.testing.assert_array_equal(o["var"], res[0]["var"])
+            assert o["freq_idx"] == res[0]["freq_idx"]
+        if mode == "mppi":
+            assert np.max(np.abs(res[0]["mean"] - so[0]["mean"])) <= 1e-5 * max(np.max(np.abs(so[0]["mean"])), 1.0)
+            # keep the single-GPU context on the ranks' distribution (the regrouped sums differ in the last bits)
+            m, v, f = ranks[0].get_distribution(0)
+            single.set_distribution(0, m, v, f)
+        else:
+            np.testing.assert_array_equal(res[0]["mean"], so[0]["mean"])
+            np.testing.assert_array_equal(res[0]["var"], so[0]["var"])
+            np.testing.assert_array_equal(ranks[0].debug_elites(0), single.debug_elites(0))
+        assert res[0]["j_min"] == so[0]["j_min"] and res[0]["n_diverged"] == so[0]["n_diverged"]
+    assert all(c.iter == 3 for c in ranks)
