@@ -344,8 +344,7 @@ int enqueue_step(sbs_ctx* c, cudaStream_t s) {
       int rc = enqueue_records(c, s, gat + (size_t)c->cfg.rank * n);
       P.n_peers = 0;
       if (rc != SBS_OK) return rc;
-      static const bool no_wait = getenv("SBS_PEER_NOWAIT") && atoi(getenv("SBS_PEER_NOWAIT")) != 0;  // debugging
-      for (int j = 0; j < c->cfg.world && !no_wait; ++j) {
+      for (int j = 0; j < c->cfg.world; ++j) {
         if (j == c->cfg.rank) continue;
         const int r2 = g_wait_value32(s, c->d_xflags + j, seq);
         if (r2 != 0) return fail(c, SBS_ERR_CUDA, "cuStreamWaitValue32 failed");
@@ -925,14 +924,6 @@ int sbs_peer_handle(sbs_ctx* c, uint8_t handle[64], void** base) {
     memcpy(handle, &h, 64);
   }
   if (base) *base = c->d_xbuf;
-  return SBS_OK;
-}
-
-int sbs_debug_xflags(sbs_ctx* c, uint32_t* flags) {
-  if (!c || !flags || !c->d_xflags) return SBS_ERR_INVALID_ARG;
-  CK(cudaSetDevice(c->cfg.device));
-  CK(cudaMemcpyAsync(flags, c->d_xflags, sbs::kMaxWorld * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
   return SBS_OK;
 }
 
