@@ -190,6 +190,36 @@ def test_gait_variants(B, orc, gait):
         assert set(np.unique(f)) == set(range(8))
 
 
+def test_maximum_horizon_and_knots(B, orc):
+    """The largest supported shape: H = 64 steps (SBS_MAX_HORIZON), P = 8 knots (D = 96).
+    Full stance and a small sigma keep the 1.28 s rollouts upright, away from the
+    divergence thresholds (L35: near them the +inf decision is a binary32-vs-binary64
+    discontinuity that a long open-loop horizon amplifies)."""
+    cfg = W.base_config(n_samples=300, knots=8, horizon=64, gait_adapt=1, mode="naive", sigma=[1.0, 1.0, 2.0],
+                        duty_factor=1.0)
+    inputs = [W.robot_input(cfg, 0, cmd=(0.0, 0.0, 0.0), phase=W.q32(0.6))]
+    _run_pair(B, orc, cfg, inputs)
+
+
+def test_mppi_small_lambda_is_the_argmin_sample(B):
+    """North star: MPPI as lambda -> 0 returns the argmin sample."""
+    cfg, inputs = W.config2(K=3000)
+    cfg = dict(cfg, **{"lambda": 1e-6})
+    c = _ctrl(B, cfg, inputs)
+    _, th, _ = c.debug_samples(0, 0, 3000)
+    _, outs = c.step(inputs)
+    J = c.debug_costs()[0]
+    kmin = int(np.argmin(J))
+    np.testing.assert_allclose(outs[0]["mean"], th[kmin], rtol=0, atol=1e-4 * max(np.max(np.abs(th[kmin])), 1.0))
+
+
+def test_cem_all_samples_elite_is_the_population(B, orc):
+    """K_e = K: CEM's update is the population mean and (floored) variance."""
+    cfg, inputs = W.config3("cem", K=500)
+    cfg = dict(cfg, n_elite=500)
+    _run_pair(B, orc, cfg, inputs, n_steps=2)
+
+
 def test_full_inertia_and_no_warm_shift(B, orc):
     cfg = W.base_config(n_samples=500, inertia=[0.135, 0.01, -0.02, 0.01, 0.54, 0.03, -0.02, 0.03, 0.58],
                         warm_shift=0, elite_preserve=0, duty_factor=1.0)
