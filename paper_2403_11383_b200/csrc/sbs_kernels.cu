@@ -65,6 +65,12 @@ struct RobotSmem {
   int cur_idx;
 };
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the programmatic-
+// serialisation attribute starts while its predecessor drains and waits here until
+// the predecessor has completed and its memory is visible (a no-op otherwise).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // robot r's inputs / reference: device buffers, or (host path, R = 1) the kernel parameters themselves
 __device__ __forceinline__ const sbs_input* robot_in(const Params& p, int r) { return p.inline_in ? &p.in_inline : p.in + r; }
 __device__ __forceinline__ const float* robot_xref(const Params& p, int r) {
@@ -1072,6 +1078,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
     }
     __syncthreads();
   }
+  griddep_launch_dependents();  // (CEM: the select kernel may be scheduled; it waits for this grid)
   float* out = p.part + ((size_t)r * p.n_cta + blockIdx.x) * p.part_stride;
   if (EPI == EPI_MPPI) {
     if (tid < D) out[kPartHdr + tid] = run;
@@ -1392,6 +1399,8 @@ template <int MODE, bool SMALL>
 __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_constant__ Params p, float* emit) {
   extern __shared__ uint32_t sel_smem[];
   const int r = blockIdx.x, tid = threadIdx.x;
+  griddep_wait();               // the rollout's J and records
+  griddep_launch_dependents();  // the elite kernel may be scheduled now (it waits for us)
   const int64_t Ke = p.n_elite;
   float* hdr = MODE == SEL_EMIT ? emit + (size_t)r * p.ex_stride : p.sdiag + (size_t)r * 8;
   if (blockIdx.x == 0) SBS_TS(0);
@@ -1466,11 +1475,11 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   __shared__ float s_diag[5];
   const int r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
   const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
-  // the elite's index and cost are loaded with the robot inputs (one round trip)
+  load_robot(p, r, s, false);  // (not written by the select kernel: may overlap it)
+  griddep_wait();              // the select kernel's elite list and diagnostics
   const bool has_e = e < p.n_elite;
   const int64_t k = has_e ? p.elite[(size_t)r * p.n_elite + e] : 0;
   const float Je = has_e ? p.elite_J[(size_t)r * p.n_elite + e] : kInf;
-  load_robot(p, r, s, false);
   __syncthreads();
   const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
   float dev[4] = {0.f, 0.f, 0.f, 0.f};
@@ -1582,6 +1591,7 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_cov_kernel(const __grid_consta
   const int r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
   load_robot(p, r, s, false);
   stage_chol_t(p, r, Lt);
+  griddep_wait();  // the select kernel's elite list
   __syncthreads();
   const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
   const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
@@ -1758,6 +1768,24 @@ __global__ void __launch_bounds__(128) sbs_debug_samples_kernel(const __grid_con
 // the rollout / elite / debug kernels for that P) and once with -DSBS_TU_COMMON
 // (dispatch, select and merge kernels), in parallel.
 // ---------------------------------------------------------------------------
+// launch with programmatic stream serialisation (PDL): the kernel may start while the
+// previous kernel on the stream drains; it waits in griddep_wait() for its inputs
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int P>
 struct PEntry {
   static cudaError_t rollout(const Params& p, int mode, bool fused, cudaStream_t s);
@@ -1825,10 +1853,8 @@ template <int P>
 cudaError_t PEntry<P>::elite(const Params& p, cudaStream_t s) {
   dim3 grid(p.n_eblk, p.R);
   if (p.full_cov)
-    sbs_cov_kernel<P><<<grid, 32 * 3 * P, (size_t)cov_smem_floats(12 * P) * sizeof(float), s>>>(p);
-  else
-    sbs_elite_kernel<P><<<grid, 32 * 3 * P, 0, s>>>(p);
-  return cudaGetLastError();
+    return launch_pdl(sbs_cov_kernel<P>, grid, dim3(32 * 3 * P), (size_t)cov_smem_floats(12 * P) * sizeof(float), s, p);
+  return launch_pdl(sbs_elite_kernel<P>, grid, dim3(32 * 3 * P), 0, s, p);
 }
 
 template <int P>
@@ -1972,9 +1998,8 @@ cudaError_t prepare_kernels(int P) {
 template <int MODE>
 static cudaError_t launch_select_t(const Params& p, int64_t K, float* emit, cudaStream_t s) {
   const size_t smem = select_smem(K);
-  if (K <= kSelSmallMax) sbs_select_kernel<MODE, true><<<p.R, kSelBlock, smem, s>>>(p, emit);
-  else sbs_select_kernel<MODE, false><<<p.R, kSelBlock, smem, s>>>(p, emit);
-  return cudaGetLastError();
+  if (K <= kSelSmallMax) return launch_pdl(sbs_select_kernel<MODE, true>, dim3(p.R), dim3(kSelBlock), smem, s, p, emit);
+  return launch_pdl(sbs_select_kernel<MODE, false>, dim3(p.R), dim3(kSelBlock), smem, s, p, emit);
 }
 
 cudaError_t launch_select(const Params& p, cudaStream_t s) { return launch_select_t<SEL_LOCAL>(p, p.K_local, nullptr, s); }
