@@ -61,6 +61,7 @@ Nccl g_nccl;
 constexpr int kNcclFloat32 = 7;  // ncclFloat32 in nccl.h
 
 thread_local std::string g_create_err;
+constexpr int kLoopUnroll = 8;  // control steps per replayed graph of sbs_run_loop
 
 // cuStreamWaitValue32 (driver API, resolved through the runtime): a stream waits in the
 // GPU front-end until a 32-bit word reaches a value (GEQ, wrap-around safe)
@@ -127,7 +128,8 @@ struct sbs_ctx {
   // pinned staging of the start value, and one captured iteration keyed by its arguments
   uint32_t* d_loopw = nullptr;
   uint32_t* h_loopw = nullptr;
-  cudaGraphExec_t loop_graph = nullptr;
+  cudaGraphExec_t loop_graph = nullptr;    // one control step
+  cudaGraphExec_t loop_graph_u = nullptr;  // kLoopUnroll control steps
   std::vector<char> loop_key;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<char> ref_set;
@@ -415,6 +417,7 @@ void sbs_destroy(sbs_ctx* c) {
   if (c->h_out) cudaFreeHost(c->h_out);  // (h_in and h_xref point into h_blk)
   if (c->graph) cudaGraphExecDestroy(c->graph);
   if (c->loop_graph) cudaGraphExecDestroy(c->loop_graph);
+  if (c->loop_graph_u) cudaGraphExecDestroy(c->loop_graph_u);
   if (c->d_loopw) cudaFree(c->d_loopw);
   if (c->h_loopw) cudaFreeHost(c->h_loopw);
   if (c->h_blk) cudaFreeHost(c->h_blk);
@@ -1095,25 +1098,33 @@ int sbs_run_loop(sbs_ctx* c, int32_t n_iter, sbs_input* d_in, sbs_output* d_out,
     memcpy(key.data() + sizeof(a), &d_in, sizeof(d_in));
     memcpy(key.data() + sizeof(a) + sizeof(d_in), &d_out, sizeof(d_out));
     if (!c->loop_graph || key != c->loop_key) {
-      if (c->loop_graph) {
-        CK(cudaGraphExecDestroy(c->loop_graph));
-        c->loop_graph = nullptr;
+      // two graphs: one control step, and kLoopUnroll control steps (fewer graph launches;
+      // consecutive kernels inside a graph keep their programmatic-launch overlap)
+      for (cudaGraphExec_t* ge : {&c->loop_graph, &c->loop_graph_u}) {
+        if (*ge) {
+          CK(cudaGraphExecDestroy(*ge));
+          *ge = nullptr;
+        }
       }
-      cudaGraph_t g;
-      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      rc = enqueue_iter(c->stream);
-      const cudaError_t e = cudaStreamEndCapture(c->stream, &g);  // always leave capture mode
-      if (rc != SBS_OK) {
-        if (e == cudaSuccess) cudaGraphDestroy(g);
-        return rc;
+      for (int which = 0; which < 2; ++which) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        for (int u = 0; u < (which ? kLoopUnroll : 1) && rc == SBS_OK; ++u) rc = enqueue_iter(c->stream);
+        const cudaError_t e = cudaStreamEndCapture(c->stream, &g);  // always leave capture mode
+        if (rc != SBS_OK) {
+          if (e == cudaSuccess) cudaGraphDestroy(g);
+          return rc;
+        }
+        CK(e);
+        const cudaError_t ei = cudaGraphInstantiate(which ? &c->loop_graph_u : &c->loop_graph, g, 0);
+        cudaGraphDestroy(g);
+        CK(ei);
       }
-      CK(e);
-      const cudaError_t ei = cudaGraphInstantiate(&c->loop_graph, g, 0);
-      cudaGraphDestroy(g);
-      CK(ei);
       c->loop_key = key;
     }
-    for (int i = 0; i < n_iter; ++i) CK(cudaGraphLaunch(c->loop_graph, s));
+    int i = 0;
+    for (; i + kLoopUnroll <= n_iter; i += kLoopUnroll) CK(cudaGraphLaunch(c->loop_graph_u, s));
+    for (; i < n_iter; ++i) CK(cudaGraphLaunch(c->loop_graph, s));
   }
   c->iter += (uint32_t)n_iter * (uint32_t)lc->n_inner;
   return SBS_OK;

@@ -907,6 +907,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
 
   const int r = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  griddep_wait();  // PDL: the previous iteration's distribution / the closed loop's new inputs
   if (blockIdx.x == 0) SBS_TS(0);
   load_robot(p, r, s);
   if (FC) stage_chol_t(p, r, s_red);
@@ -1808,9 +1809,8 @@ constexpr size_t rollout_smem() {
 template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false>
 static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
   dim3 grid(p.n_cta, p.R);
-  sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT>
-      <<<grid, SPLIT ? kBlock * kSplitLanes : kBlock, rollout_smem<P, EPI, FC, SPLIT>(), s>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT>, grid, dim3(SPLIT ? kBlock * kSplitLanes : kBlock),
+                    rollout_smem<P, EPI, FC, SPLIT>(), s, p);
 }
 
 template <int P>

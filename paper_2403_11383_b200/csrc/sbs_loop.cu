@@ -4,9 +4,9 @@
 // reference in device memory, so an episode runs without host round trips.
 //
 //   plant (L36): one RK4 step of Eq. 1 with u0 held on the stance
-//                legs and an external CoM wrench, binary32 with
-//                correctly rounded libm sin/cos/tan (no SFU approximations:
-//                this is the simulated robot, not a rollout);
+//                legs and an external CoM wrench, binary32, SFU sin/cos
+//                as in the rollout (one thread per robot: the libm versions'
+//                slow paths dominated a single robot's control step);
 //   fall (L40), gait phase (L37), footholds by Eq. 3,
 //   reference (L13).
 #include <math.h>
@@ -20,8 +20,10 @@ namespace {
 // Eq. 1 with the CoM wrench: x = (p, v, (roll, pitch, yaw), omega_body)
 __device__ void plant_f(const Params& p, const float x[12], const float u[12], const int st[4], const float feet[12],
                         const float w[6], float xd[12]) {
-  const float cr = cosf(x[6]), sr = sinf(x[6]), cp = cosf(x[7]), sp = sinf(x[7]);
-  const float cy = cosf(x[8]), sy = sinf(x[8]);
+  float cr, sr, cp, sp, cy, sy;  // SFU sin/cos (abs. error ~4e-7 on the plant's angles), as in the rollout
+  __sincosf(x[6], &sr, &cr);
+  __sincosf(x[7], &sp, &cp);
+  __sincosf(x[8], &sy, &cy);
   // R = Rz(yaw) Ry(pitch) Rx(roll)
   const float R[9] = {cy * cp, cy * sp * sr - sy * cr, cy * sp * cr + sy * sr,
                       sy * cp, sy * sp * sr + cy * cr, sy * sp * cr - cy * sr,
@@ -53,7 +55,7 @@ __device__ void plant_f(const Params& p, const float x[12], const float u[12], c
     xd[9 + a] = p.Iinv[3 * a] * rhs[0] + p.Iinv[3 * a + 1] * rhs[1] + p.Iinv[3 * a + 2] * rhs[2];
   }
   const float s = sr * wb[1] + cr * wb[2];
-  xd[6] = wb[0] + tanf(x[7]) * s;
+  xd[6] = wb[0] + __fdividef(sp, cp) * s;
   xd[7] = cr * wb[1] - sr * wb[2];
   xd[8] = s / cp;
 }
@@ -79,6 +81,8 @@ __device__ __forceinline__ bool stance_at(const Params& p, uint32_t phase, int l
 
 __global__ void __launch_bounds__(128) sbs_advance_kernel(const __grid_constant__ Params p, const LoopArgs a,
                                                           sbs_input* in, const sbs_output* out) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the step's outputs
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < p.R) {
     const uint32_t it = a.loop ? (__ldcg(a.loop) - __ldcg(a.loop + 1)) / (uint32_t)a.n_inner : 0u;  // control step
@@ -109,7 +113,8 @@ __global__ void __launch_bounds__(128) sbs_advance_kernel(const __grid_constant_
       const sbs_command c = a.cmd ? a.cmd[r] : sbs_command{{0.f, 0.f, 0.f}, 0.f};
       const float t_st = p.duty / p.freq_hz[fi];
       const float kfb = sqrtf(fmaxf(x[2], 0.f) / fabsf(p.g[2]));
-      const float cy = cosf(x[8]), sy = sinf(x[8]);
+      float cy, sy;
+      __sincosf(x[8], &sy, &cy);
       for (int i = 0; i < 4; ++i) {
         const float hx = a.hip[3 * i], hy = a.hip[3 * i + 1];
         const float px = x[0] + (cy * hx - sy * hy), py = x[1] + (sy * hx + cy * hy);
@@ -167,9 +172,16 @@ __global__ void __launch_bounds__(128) sbs_advance_kernel(const __grid_constant_
 }
 
 cudaError_t launch_advance(const Params& p, const LoopArgs& a, sbs_input* in, const sbs_output* out, cudaStream_t s) {
-  const int blocks = (p.R + 127) / 128;
-  sbs_advance_kernel<<<blocks, 128, 0, s>>>(p, a, in, out);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};  // programmatic dependent launch after the step's last kernel
+  cfg.gridDim = dim3((p.R + 127) / 128);
+  cfg.blockDim = dim3(128);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, sbs_advance_kernel, p, a, in, out);
 }
 
 }  // namespace sbs
