@@ -543,9 +543,9 @@ def test_sharded_cem_rejects_too_few_samples_per_rank(B):
         B.Controller(dict(cfg, n_elite=600), rank=0, world=2)
 
 
-@pytest.mark.parametrize("mode,K,world,ke", [("mppi", 10000, 2, 1), ("mppi", 65536, 4, 1), ("naive", 6000, 2, 1),
-                                             ("cem", 12000, 3, 800)])
-def test_peer_memory_exchange_matches_single_gpu(B, orc, mode, K, world, ke):
+@pytest.mark.parametrize("mode,K,world,ke,R", [("mppi", 10000, 2, 1, 1), ("mppi", 65536, 4, 1, 1), ("naive", 6000, 2, 1, 1),
+                                               ("cem", 12000, 3, 800, 1), ("mppi", 4000, 2, 1, 3), ("cem", 4000, 2, 300, 2)])
+def test_peer_memory_exchange_matches_single_gpu(B, orc, mode, K, world, ke, R):
     """The rank-record exchange over peer memory (finishing CTA stores into every peer's
     buffer + flag; streams wait on the flags in the front end; no NCCL), here with `world`
     contexts of one process on one GPU, each on its own stream and enqueued in rank order
@@ -556,39 +556,46 @@ def test_peer_memory_exchange_matches_single_gpu(B, orc, mode, K, world, ke):
 
     import torch
     if mode == "mppi":
-        cfg, inputs = W.config2(K=K)
+        cfg, _ = W.config2(K=K)
     else:
-        cfg, inputs = W.config3(mode, K=K)
+        cfg, _ = W.config3(mode, K=K)
         cfg = dict(cfg, n_elite=ke)
+    cfg = dict(cfg, n_robots=R)
+    inputs = [W.robot_input(cfg, r, cmd=(0.4, 0.1 * r, 0.0), phase=W.q32(0.3 + 0.2 * r)) for r in range(R)]
     d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
     ranks = [B.Controller(cfg, rank=g, world=world) for g in range(world)]
     bases = [c.peer_handle()[1] for c in ranks]
     for c in ranks:
-        c.set_reference(0, inputs[0]["xref"])
+        for r in range(R):
+            c.set_reference(r, inputs[r]["xref"])
         c.peer_connect(bases=bases)
     streams = [torch.cuda.Stream() for _ in ranks]
-    outs = [torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda") for _ in ranks]
+    n_out = C.sizeof(B.sbs_output)
+    outs = [torch.zeros(R * n_out, dtype=torch.uint8, device="cuda") for _ in ranks]
     single = B.Controller(cfg)
-    single.set_reference(0, inputs[0]["xref"])
+    for r in range(R):
+        single.set_reference(r, inputs[r]["xref"])
     torch.cuda.synchronize()
     for it in range(3):
         for g, c in enumerate(ranks):
             c.step_device(d_in.data_ptr(), outs[g].data_ptr(), streams[g].cuda_stream)
         torch.cuda.synchronize()
         _, so = single.step(inputs)
-        res = [B.output_dict(B.sbs_output.from_buffer_copy(o.cpu().numpy().tobytes()), 48) for o in outs]
-        for o in res[1:]:
-            np.testing.assert_array_equal(o["mean"], res[0]["mean"])
-            np.testing.assert_array_equal(o["var"], res[0]["var"])
-            assert o["freq_idx"] == res[0]["freq_idx"]
-        if mode == "mppi":
-            assert np.max(np.abs(res[0]["mean"] - so[0]["mean"])) <= 1e-5 * max(np.max(np.abs(so[0]["mean"])), 1.0)
-            # keep the single-GPU context on the ranks' distribution (the regrouped sums differ in the last bits)
-            m, v, f = ranks[0].get_distribution(0)
-            single.set_distribution(0, m, v, f)
-        else:
-            np.testing.assert_array_equal(res[0]["mean"], so[0]["mean"])
-            np.testing.assert_array_equal(res[0]["var"], so[0]["var"])
-            np.testing.assert_array_equal(ranks[0].debug_elites(0), single.debug_elites(0))
-        assert res[0]["j_min"] == so[0]["j_min"] and res[0]["n_diverged"] == so[0]["n_diverged"]
+        for r in range(R):
+            res = [B.output_dict(B.sbs_output.from_buffer_copy(o.cpu().numpy().tobytes()[r * n_out:(r + 1) * n_out]), 48)
+                   for o in outs]
+            for o in res[1:]:
+                np.testing.assert_array_equal(o["mean"], res[0]["mean"])
+                np.testing.assert_array_equal(o["var"], res[0]["var"])
+                assert o["freq_idx"] == res[0]["freq_idx"]
+            if mode == "mppi":
+                assert np.max(np.abs(res[0]["mean"] - so[r]["mean"])) <= 1e-5 * max(np.max(np.abs(so[r]["mean"])), 1.0)
+                # keep the single-GPU context on the ranks' distribution (the regrouped sums differ in the last bits)
+                m, v, f = ranks[0].get_distribution(r)
+                single.set_distribution(r, m, v, f)
+            else:
+                np.testing.assert_array_equal(res[0]["mean"], so[r]["mean"])
+                np.testing.assert_array_equal(res[0]["var"], so[r]["var"])
+                np.testing.assert_array_equal(ranks[0].debug_elites(r), single.debug_elites(r))
+            assert res[0]["j_min"] == so[r]["j_min"] and res[0]["n_diverged"] == so[r]["n_diverged"]
     assert all(c.iter == 3 for c in ranks)
