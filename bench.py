@@ -214,14 +214,22 @@ def run_sbs(args):
     if world > 1:
         # rank records exchanged over peer memory (the finishing CTA stores into every peer's
         # buffer over NVLink; streams wait on the peers' flags); NCCL all-gather as fallback
+        ok, why = True, ""
         try:
             handle, _ = ctrl.peer_handle()
             handles = [None] * world
             dist.all_gather_object(handles, handle)
             ctrl.peer_connect(handles=handles)
-            exchange = "peer memory (NVLink stores + stream flag waits)"
         except Exception as exc:  # noqa: BLE001
-            exchange = f"NCCL all-gather (peer exchange unavailable: {str(exc)[:80]})"
+            ok, why = False, str(exc)[:80]
+        oks = [None] * world
+        dist.all_gather_object(oks, ok)  # every rank must use the same exchange
+        if all(oks):
+            exchange = "peer memory (NVLink stores + stream flag waits)"
+        else:
+            if ok:
+                ctrl.peer_connect()  # disconnect
+            exchange = f"NCCL all-gather (peer exchange unavailable on some rank: {why})"
         dist.barrier()
     in_arr = B.make_inputs(inputs)
     d_in = torch.from_numpy(np.frombuffer(bytes(in_arr), dtype=np.uint8).copy()).cuda()

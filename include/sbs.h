@@ -224,7 +224,9 @@ int sbs_record_floats(const sbs_ctx* ctx);
  * stream waits in the GPU front-end (cuStreamWaitValue32, no SM held) for the
  * peers' flags before the rank-order merge.  Two buffers alternate, so a fast rank
  * never overwrites records a slower peer is still merging.  Collective: every rank
- * steps in the same order.  world <= 8. */
+ * steps in the same order.  world <= 8.  sbs_peer_connect(ctx, NULL, NULL)
+ * disconnects (back to the NCCL or caller-driven exchange); the ranks must agree
+ * on the exchange in use. */
 int sbs_peer_handle(sbs_ctx* ctx, uint8_t handle[64], void** base);
 int sbs_peer_connect(sbs_ctx* ctx, void* const* bases, const uint8_t* handles);
 int sbs_step_records(sbs_ctx* ctx, const sbs_input* d_in, float* d_rec, void* stream);

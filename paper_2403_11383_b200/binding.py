@@ -310,6 +310,8 @@ class Controller:
 
     def peer_connect(self, bases=None, handles=None):
         """bases: every rank's device address (same process), or handles: every rank's IPC handle."""
+        if bases is None and handles is None:  # disconnect
+            return self._check(self.L.sbs_peer_connect(self.ctx, None, None))
         if bases is not None:
             arr = (C.c_void_p * len(bases))(*bases)
             return self._check(self.L.sbs_peer_connect(self.ctx, arr, None))

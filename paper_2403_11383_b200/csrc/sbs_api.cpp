@@ -931,7 +931,16 @@ int sbs_peer_handle(sbs_ctx* c, uint8_t handle[64], void** base) {
 }
 
 int sbs_peer_connect(sbs_ctx* c, void* const* bases, const uint8_t* handles) {
-  if (!c || (!bases && !handles)) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (!c) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
+  if (!bases && !handles) {  // disconnect: back to the NCCL / external exchange
+    CK(cudaSetDevice(c->cfg.device));
+    CK(cudaStreamSynchronize(c->stream));
+    for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+    c->ipc_opened.clear();
+    c->peer_base.clear();
+    c->peer = false;
+    return SBS_OK;
+  }
   const int W = c->cfg.world, me = c->cfg.rank;
   if (W < 2 || W > sbs::kMaxWorld) return fail(c, SBS_ERR_STATE, "peer exchange needs 2 <= world <= 8");
   CK(cudaSetDevice(c->cfg.device));
