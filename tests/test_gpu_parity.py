@@ -599,3 +599,36 @@ def test_peer_memory_exchange_matches_single_gpu(B, orc, mode, K, world, ke, R):
                 np.testing.assert_array_equal(ranks[0].debug_elites(r), single.debug_elites(r))
             assert res[0]["j_min"] == so[r]["j_min"] and res[0]["n_diverged"] == so[r]["n_diverged"]
     assert all(c.iter == 3 for c in ranks)
+
+
+def test_peer_disconnect_falls_back_to_the_caller_exchange(B):
+    """After sbs_peer_connect(NULL, NULL) the contexts are back on the caller-driven exchange."""
+    import ctypes as C
+
+    import torch
+    cfg, inputs = W.config2(K=4000)
+    d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
+    ranks = [B.Controller(cfg, rank=g, world=2) for g in range(2)]
+    bases = [c.peer_handle()[1] for c in ranks]
+    for c in ranks:
+        c.set_reference(0, inputs[0]["xref"])
+        c.peer_connect(bases=bases)
+    outs = [torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda") for _ in ranks]
+    streams = [torch.cuda.Stream() for _ in ranks]
+    for g, c in enumerate(ranks):
+        c.step_device(d_in.data_ptr(), outs[g].data_ptr(), streams[g].cuda_stream)
+    torch.cuda.synchronize()
+    for c in ranks:
+        c.peer_connect()
+    with pytest.raises(Exception):                       # no NCCL, no peers: the host step refuses
+        ranks[0].step_device(d_in.data_ptr(), outs[0].data_ptr(), 0)
+    recs = torch.zeros((2, ranks[0].record_floats()), dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    for g, c in enumerate(ranks):
+        c.step_records(d_in.data_ptr(), recs[g].data_ptr(), s)
+    for g, c in enumerate(ranks):
+        c.finish_records(recs.data_ptr(), d_in.data_ptr(), outs[g].data_ptr(), s)
+    torch.cuda.synchronize()
+    a, b = (B.output_dict(B.sbs_output.from_buffer_copy(o.cpu().numpy().tobytes()), 48) for o in outs)
+    np.testing.assert_array_equal(a["mean"], b["mean"])
+    assert all(c.iter == 2 for c in ranks)
