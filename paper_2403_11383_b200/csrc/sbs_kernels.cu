@@ -1300,10 +1300,15 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_w, u
 
 // 16-bit digit pass: count keys with (key & pmask) == pref by digit (key >> sh) & 0xFFFF,
 // find digit B with rank `want` inside; returns B and the count strictly below it.
+__device__ __forceinline__ void zero_hist16(uint32_t* hist) {  // 32768 words, 16-byte stores
+  uint4* h4 = reinterpret_cast<uint4*>(hist);
+  for (int i = threadIdx.x; i < 32768 / 4; i += kSelBlock) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 static __device__ void digit16_pass(const uint32_t (&key)[kSelKPT], int nk, uint32_t pmask, uint32_t pref, int sh,
-                             uint32_t want, uint32_t* hist, uint32_t* s_w, uint32_t* s_res) {
+                             uint32_t want, uint32_t* hist, uint32_t* s_w, uint32_t* s_res, bool zeroed = false) {
   const int tid = threadIdx.x;
-  for (int i = tid; i < 32768; i += kSelBlock) hist[i] = 0;
+  if (!zeroed) zero_hist16(hist);
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i)
@@ -1343,7 +1348,7 @@ static __device__ void digit16_pass(const uint32_t (&key)[kSelKPT], int nk, uint
 }
 
 static __device__ void select_block_small(const float* J, int K, int K_e, int64_t k_begin, int64_t* elite, float* eJ,
-                                          uint32_t* hist) {
+                                          uint32_t* hist, bool zeroed = false) {
   __shared__ uint32_t s_w[33];
   __shared__ uint32_t s_res[2];
   const int tid = threadIdx.x;
@@ -1354,7 +1359,7 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i) key[i] = i < nk ? cost_key(J[k0 + i]) : 0xFFFFFFFFu;
   if (blockIdx.x == 0) SBS_TS(2);
-  digit16_pass(key, nk, 0u, 0u, 16, (uint32_t)K_e, hist, s_w, s_res);
+  digit16_pass(key, nk, 0u, 0u, 16, (uint32_t)K_e, hist, s_w, s_res, zeroed);
   if (blockIdx.x == 0) SBS_TS(3);
   const uint32_t hi = s_res[0], below_hi = s_res[1];
   digit16_pass(key, nk, 0xFFFF0000u, hi << 16, 0, (uint32_t)K_e - below_hi, hist, s_w, s_res);
@@ -1400,6 +1405,7 @@ template <int MODE, bool SMALL>
 __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_constant__ Params p, float* emit) {
   extern __shared__ uint32_t sel_smem[];
   const int r = blockIdx.x, tid = threadIdx.x;
+  if (SMALL) zero_hist16(sel_smem);  // (independent of the rollout: overlaps its tail under PDL)
   griddep_wait();               // the rollout's J and records
   griddep_launch_dependents();  // the elite kernel may be scheduled now (it waits for us)
   const int64_t Ke = p.n_elite;
@@ -1420,7 +1426,7 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_cons
   }
   int64_t* el = p.elite + (size_t)r * Ke;
   float* eJ = p.elite_J + (size_t)r * Ke;
-  if (SMALL) select_block_small(J, (int)K, (int)Ke, kb, el, eJ, sel_smem);
+  if (SMALL) select_block_small(J, (int)K, (int)Ke, kb, el, eJ, sel_smem, true);
   else select_block(J, K, Ke, kb, el, eJ, sel_smem);
   __syncthreads();
   if (blockIdx.x == 0) SBS_TS(6);
