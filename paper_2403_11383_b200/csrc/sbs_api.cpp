@@ -558,6 +558,10 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
     bool split = !cfg->full_cov && (int64_t)R * P.n_tiles <= (int64_t)occ_s * c->sm_count;
     if (const char* e = getenv("SBS_SPLIT")) split = split && atoi(e) != 0;  // experiments: SBS_SPLIT=0 disables
     P.split = split ? 1 : 0;
+    // producer / integrator warps (latency mode) when the stance-leg table fits
+    bool ab = split && sbs::split_smem_bytes(Pk, cfg->mode == SBS_MPPI, P.H, true) <= sbs::kSplitSmemMax;
+    if (const char* e = getenv("SBS_AB")) ab = ab && atoi(e) != 0;  // experiments: SBS_AB=0 disables
+    P.ab = ab ? 1 : 0;
     const int occ = sbs::rollout_occupancy(Pk, cfg->mode, cfg->full_cov != 0, split);
     const int64_t slots = (int64_t)occ * c->sm_count;
     P.n_cta = (int)std::max<int64_t>(1, std::min<int64_t>(P.n_tiles, slots / R));

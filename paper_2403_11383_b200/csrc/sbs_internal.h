@@ -16,6 +16,13 @@ constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, n
 constexpr int kEPartStride = 2 * SBS_MAX_D + 4;  // CEM elite-moment record [S1[D], n, S2[D]]
 // full-covariance CEM elite record [S1[D], n, lower triangle of S2 (D (D + 1) / 2)], 16-byte multiple
 __host__ __device__ constexpr int fc_record_floats(int D) { return ((D + 1 + D * (D + 1) / 2) + 3) / 4 * 4; }
+// latency-mode shared memory: MPPI reduction rows, theta / theta1 of the tile, and (ab)
+// the producer warps' stance-leg table [H][10][kBlock]
+constexpr size_t kSplitSmemMax = 200 * 1024;
+__host__ __device__ constexpr size_t split_smem_bytes(int P, bool mppi, int H, bool ab) {
+  return (mppi ? (size_t)(12 * P + 4) * (kBlock + 1) * 4 : 0) + (size_t)kBlock * (12 * P + 2) * 4 +
+         (ab ? (size_t)10 * H * kBlock * 4 : 0);
+}
 #ifndef SBS_ROLLOUT_MIN_BLOCKS
 #define SBS_ROLLOUT_MIN_BLOCKS 4
 #endif
@@ -51,6 +58,7 @@ struct Params {
   int64_t n_elite;
   float var_floor[3];
   int split;                  // latency mode: kSplitTile samples per tile, sampler split over 4 lanes
+  int ab;                     // latency mode: 12 producer warps tabulate the stance-leg forces for the 4 integrator warps
   int full_cov;               // f3 (L42): CEM with a full covariance C = L L^T
   float* Lmat;                // [R][D][D] lower Cholesky factor (row-major), full_cov only
   int n_sig_groups;           // multiple Gaussians (L41): sample k uses sig_scale[k mod n_sig_groups]

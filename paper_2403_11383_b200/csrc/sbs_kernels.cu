@@ -24,6 +24,7 @@
 // issue and latency, not by HBM (4 bytes written per sample).  See DESIGN.md sec. 7.
 #include <float.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "sbs_internal.h"
 #include "sbs_noise.cuh"
@@ -39,9 +40,21 @@ __device__ unsigned long long g_sbs_ts[16];
       g_sbs_ts[i] = t_;                                                         \
     }                                                                           \
   } while (0)
+__device__ unsigned long long g_sbs_cta[256][6];  // per CTA: globaltimer x4, clock64 around the rollout
+#define SBS_CTS(i)                                                              \
+  do {                                                                          \
+    if (threadIdx.x == 0 && blockIdx.x < 256 && blockIdx.y == 0) {              \
+      unsigned long long t_;                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
+      g_sbs_cta[blockIdx.x][i] = (i) >= 4 ? (unsigned long long)clock64() : t_; \
+    }                                                                           \
+  } while (0)
 #else
 #define SBS_TS(i) \
   do {            \
+  } while (0)
+#define SBS_CTS(i) \
+  do {             \
   } while (0)
 #endif
 
@@ -135,6 +148,111 @@ static __device__ void load_robot(const Params& p, int r, RobotSmem& s, bool rol
     }
   }
   if (threadIdx.x == 0) s.phase0 = ph0;
+}
+
+// Latency mode: load_robot split in two so that the L2 round trips of the robot's
+// inputs overlap the noise draws.  _issue starts asynchronous global->shared copies
+// (cp.async, no register destination) of the raw inputs; _commit waits for them and
+// applies the same transforms as load_robot (warm shift, sqrt, contact table).
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(__cvta_generic_to_global(src))
+               : "memory");
+}
+static __device__ void load_robot_issue(const Params& p, int r, RobotSmem& s, float* mraw) {
+  const int D = p.D;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    cp_async4(&mraw[d], p.mean + (size_t)r * D + d);
+    cp_async4(&s.sig[d], p.var + (size_t)r * D + d);  // variance; sqrt in _commit
+  }
+  if (threadIdx.x == 0) cp_async4(&s.cur_idx, p.fidx + r);
+  if (p.inline_in) return;  // parameter-space inputs: copied in _commit
+  const sbs_input* in = p.in + r;
+  for (int a = threadIdx.x; a < 12; a += blockDim.x) {
+    cp_async4(&s.x0[a], &in->x0[a]);
+    cp_async4(&s.feet[a], &in->feet_cur[a]);
+    cp_async4(&s.feet[12 + a], &in->feet_next[a]);
+  }
+  const float* xr = p.xref + (size_t)r * p.H * 12;
+  for (int a = threadIdx.x; a < p.H * 12; a += blockDim.x) {
+    const int j = a / 12, c = a - 12 * j;
+    cp_async4(&s.xref[12 * j + xref_slot(c)], xr + a);
+  }
+  if (threadIdx.x == 0) cp_async4(&s.phase0, &in->phase_q32);
+}
+static __device__ void load_robot_commit(const Params& p, RobotSmem& s, const float* mraw, uint32_t iter) {
+  if (p.inline_in) {
+    const sbs_input* in = &p.in_inline;
+    for (int a = threadIdx.x; a < 12; a += blockDim.x) {
+      s.x0[a] = in->x0[a];
+      s.feet[a] = in->feet_cur[a];
+      s.feet[12 + a] = in->feet_next[a];
+    }
+    for (int a = threadIdx.x; a < p.H * 12; a += blockDim.x) {
+      const int j = a / 12, c = a - 12 * j;
+      s.xref[12 * j + xref_slot(c)] = p.xref_inline[a];
+    }
+    if (threadIdx.x == 0) s.phase0 = in->phase_q32;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const int D = p.D, P = p.P;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const int pk = d / 12, ch = d - 12 * pk;
+    float v = 0.0f;
+    if (p.warm_shift) {
+      for (int q = 0; q < P; ++q) v = fmaf(p.WS[pk][q], mraw[q * 12 + ch], v);
+    } else {
+      v = mraw[d];
+    }
+    s.mu[d] = v;
+    s.sig[d] = __fsqrt_rn(s.sig[d]);
+  }
+  const uint32_t ph0 = s.phase0;
+  for (int f = threadIdx.x; f < p.n_freq; f += blockDim.x) {  // as in load_robot
+    uint32_t ph[4];
+    uint32_t prev = 0, td = 0;
+    for (int i = 0; i < 4; ++i) ph[i] = ph0 + p.off[i];
+    for (int j = 0; j < p.H; ++j) {
+      uint32_t st = 0;
+      for (int i = 0; i < 4; ++i) {
+        if (p.all_stance || ph[i] < p.thr) st |= 1u << i;
+        ph[i] += p.inc[f];
+      }
+      if (j > 0) td |= st & ~prev;
+      prev = st;
+      s.ctab[f][j] = (uint8_t)(st | (td << 4));
+    }
+  }
+  if (threadIdx.x == 0) s.iter = iter;
+  __syncthreads();
+}
+
+// Latency mode: the normative noise of this lane's Philox blocks q = u, u + 4, ... of
+// sample k (before the distribution is known), and the gait draw on lane 0.
+template <int P>
+struct SplitNoise {
+  static constexpr int NB = (3 * P + kSplitLanes - 1) / kSplitLanes;
+  float z[NB][4];
+  int fi;
+};
+template <int P>
+__device__ __forceinline__ void split_noise(const Params& p, uint32_t robot_g, int64_t k, uint32_t iter, int u,
+                                            SplitNoise<P>& n) {
+#pragma unroll
+  for (int i = 0; i < SplitNoise<P>::NB; ++i) {
+    const int q = u + kSplitLanes * i;
+    if (q < 3 * P) {
+      const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k, iter, robot_g, p.rk);
+      box_muller(w.x, w.y, n.z[i][0], n.z[i][1]);
+      box_muller(w.z, w.w, n.z[i][2], n.z[i][3]);
+    }
+  }
+  n.fi = -1;
+  if (u == 0 && p.gait_adapt) {
+    const U4 w = philox4x32_10_rk(0x80000000u, (uint32_t)k, iter, robot_g, p.rk);
+    n.fi = (int)__umulhi(w.x, (uint32_t)p.n_freq);
+  }
 }
 
 // theta2 of one sample in registers, organised per leg: (x, y) knot pairs for
@@ -324,6 +442,99 @@ __device__ __forceinline__ void ang_deriv(const Params& p, float2 A, float2 B, f
   dC = dwyz;
 }
 
+// Stance-leg quantities of one horizon step j (state-independent): the spline forces
+// Gamma_j = sigma(theta2, t_j) (O8), their cone projection and penalty (O9), the
+// effort terms and the net force / moment about the origin.  Per-leg work sits behind
+// the stance bit: with a fixed gait every lane of a warp shares the contact schedule,
+// so swing legs cost nothing.
+struct StepForces {
+  float2 F, effxy;
+  float Fz, Mx, My, Mz, pen, effz;
+};
+constexpr int kStepForceFloats = 10;
+
+template <int P>
+__device__ __forceinline__ StepForces step_forces(const Params& p, const Theta<P>& th, uint32_t fl, int j,
+                                                  const RobotSmem& s) {
+  const float urz = p.urz[__popc(fl & 0xFu)];
+  float Wj[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) Wj[q] = p.W[j][q];
+  // accumulators start at -0 (the additive identity), so the first add is not a real op
+  StepForces o;
+  o.F = f2(-0.f, -0.f);
+  o.effxy = f2(-0.f, -0.f);
+  o.Fz = -0.f, o.Mx = -0.f, o.My = -0.f, o.Mz = -0.f, o.pen = -0.f, o.effz = -0.f;
+#pragma unroll
+  for (int leg = 0; leg < 4; ++leg) {
+    if (fl & (1u << leg)) {
+      float2 g = fmul2(f2(Wj[0], Wj[0]), th.xy[0][leg]);
+      float gz = Wj[0] * th.z[0][leg];
+#pragma unroll
+      for (int q = 1; q < P; ++q) {
+        g = ffma2(f2(Wj[q], Wj[q]), th.xy[q][leg], g);
+        gz = fmaf(Wj[q], th.z[q][leg], gz);
+      }
+      const float fzc = fminf(fmaxf(gz, p.fz_min), p.fz_max);
+      const float l = p.mu * fzc;
+      const float vzv = fmaxf(p.fz_min - gz, 0.0f) + fmaxf(gz - p.fz_max, 0.0f);
+      const float vxv = fmaxf(fabsf(g.x) - l, 0.0f), vyv = fmaxf(fabsf(g.y) - l, 0.0f);
+      o.pen += fmaf(vzv, vzv, fmaf(vxv, vxv, vyv * vyv));
+      const float2 c = f2(fminf(fmaxf(g.x, -l), l), fminf(fmaxf(g.y, -l), l));
+      // effort (u - u^r)^T R (u - u^r), u^r = (0, 0, m|g|/n_stance) (L12)
+      o.effxy = ffma2(fmul2(f2(p.Rw[3 * leg], p.Rw[3 * leg + 1]), c), c, o.effxy);
+      const float ez = fzc - urz;
+      o.effz = fmaf(p.Rw[3 * leg + 2] * ez, ez, o.effz);
+      // net force and moment about the origin; feet switch at touchdown (L23)
+      o.F = fadd2(o.F, c);
+      o.Fz += fzc;
+      const int fo = ((fl >> (4 + leg)) & 1u) * 12 + 3 * leg;  // feet_next after touchdown
+      const float fx = s.feet[fo], fy = s.feet[fo + 1], fzz = s.feet[fo + 2];
+      o.Mx += fmaf(fy, fzc, -fzz * c.y);
+      o.My += fmaf(fzz, c.x, -fx * fzc);
+      o.Mz += fmaf(fx, c.y, -fy * c.x);
+    }
+  }
+  return o;
+}
+
+// Latency mode, force-producer side: table [H][kStepForceFloats][kBlock] in shared
+// memory, sample column `col` (conflict-free: consecutive lanes, consecutive words).
+__device__ __forceinline__ void store_forces(float* tab, int j, int col, const StepForces& f) {
+  float* t = tab + (size_t)j * kStepForceFloats * kBlock + col;
+  t[0 * kBlock] = f.F.x;
+  t[1 * kBlock] = f.F.y;
+  t[2 * kBlock] = f.Fz;
+  t[3 * kBlock] = f.Mx;
+  t[4 * kBlock] = f.My;
+  t[5 * kBlock] = f.Mz;
+  t[6 * kBlock] = f.effxy.x;
+  t[7 * kBlock] = f.effxy.y;
+  t[8 * kBlock] = f.pen;
+  t[9 * kBlock] = f.effz;
+}
+__device__ __forceinline__ StepForces load_forces(const float* tab, int j, int col) {
+  const float* t = tab + (size_t)j * kStepForceFloats * kBlock + col;
+  StepForces f;
+  f.F = f2(t[0 * kBlock], t[1 * kBlock]);
+  f.Fz = t[2 * kBlock];
+  f.Mx = t[3 * kBlock];
+  f.My = t[4 * kBlock];
+  f.Mz = t[5 * kBlock];
+  f.effxy = f2(t[6 * kBlock], t[7 * kBlock]);
+  f.pen = t[8 * kBlock];
+  f.effz = t[9 * kBlock];
+  return f;
+}
+
+// Latency mode: the horizon is cut into chunks [ab_chunk(c), ab_chunk(c + 1)) of growing
+// length (1, 2, 3, ...); the producers arrive on named barrier 1 + c once chunk c is in
+// the table, the integrators wait on it before step ab_chunk(c).
+__device__ __forceinline__ int ab_chunk(int c) { return c * (c + 1) / 2; }
+constexpr int kAbWarpsPerSmsp = 3;  // producer warps per integrator warp (the CTA's other 12 warps)
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 // steps a2-a4: Rollout(theta_k, x0), Alg. 2 with policy pi.
 // Per-leg work sits behind the stance bit: with a fixed gait every lane of a warp
 // shares the contact schedule, so swing legs cost nothing.
@@ -442,23 +653,127 @@ static __device__ float rollout(const Params& p, const Theta<P>& th, int fi, con
   return (bad || !(J <= FLT_MAX)) ? kInf : J;
 }
 
+// Latency mode, integrator warps: rollout() with the stance-leg quantities of every
+// step read from the producer warps' table (step_forces: the same arithmetic, the
+// same bits), waiting on the chunk barriers.
+template <int P>
+static __device__ float rollout_ab(const Params& p, int fi, const RobotSmem& s, const float* tab, int col) {
+  float2 pxy = f2(s.x0[0], s.x0[1]), vxy = f2(s.x0[3], s.x0[4]);
+  float pz = s.x0[2], vz = s.x0[5];
+  float2 A = f2(s.x0[6], s.x0[7]), Bq = f2(s.x0[8], s.x0[9]), C = f2(s.x0[10], s.x0[11]);
+  const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt * (1.0f / 6.0f);
+  const float dt2h = 0.5f * p.dt * p.dt, dt2q = 0.25f * p.dt * p.dt;
+  const float2 dt_2 = f2(dt, dt), hdt_2 = f2(hdt, hdt), dt6_2 = f2(dt6, dt6), two_2 = f2(2.f, 2.f);
+  const float2 dt2h_2 = f2(dt2h, dt2h), dt2q_2 = f2(dt2q, dt2q);
+  const float2 Qp = f2(p.Q[0], p.Q[1]), Qv = f2(p.Q[3], p.Q[4]), Qz = f2(p.Q[2], p.Q[5]);
+  const float2 QA = f2(p.Q[6], p.Q[7]), QB = f2(p.Q[8], p.Q[9]), QC = f2(p.Q[10], p.Q[11]);
+  const float2 im_2 = f2(p.inv_mass, p.inv_mass), gxy = f2(p.g[0], p.g[1]);
+  float J = 0.0f;
+  bool bad = false;
+  int next_chunk = 0;
+  for (int j = 0; j < p.H; ++j) {
+    if (j == ab_chunk(next_chunk)) named_sync(1 + next_chunk++, kBlock * (1 + kAbWarpsPerSmsp));
+    const StepForces sf = load_forces(tab, j, col);
+    const float2 F = sf.F;
+    const float Fz = sf.Fz, Mx = sf.Mx, My = sf.My, Mz = sf.Mz;
+    // --- stage cost r(u_j, x_j, x^r_j), packed pairs ---
+    const float* xr = &s.xref[12 * j];
+    const float2 e0 = fadd2(pxy, f2(-xr[0], -xr[1]));
+    const float2 e1 = fadd2(vxy, f2(-xr[2], -xr[3]));
+    const float2 e2 = fadd2(f2(pz, vz), f2(-xr[4], -xr[5]));
+    const float2 e3 = fadd2(A, f2(-xr[6], -xr[7]));
+    float2 e4 = fadd2(Bq, f2(-xr[8], -xr[9]));
+    e4.x = fmaf(-kTwoPi, rintf(e4.x * kInvTwoPi), e4.x);  // yaw wrapped to [-pi, pi]
+    const float2 e5 = fadd2(C, f2(-xr[10], -xr[11]));
+    float2 acc = fmul2(fmul2(Qp, e0), e0);
+    acc = ffma2(fmul2(Qv, e1), e1, acc);
+    acc = ffma2(fmul2(Qz, e2), e2, acc);
+    acc = ffma2(fmul2(QA, e3), e3, acc);
+    acc = ffma2(fmul2(QB, e4), e4, acc);
+    acc = ffma2(fmul2(QC, e5), e5, acc);
+    acc = fadd2(acc, sf.effxy);
+    J += (acc.x + acc.y) + fmaf(p.w_fc, sf.pen, sf.effz);
+    // --- x_{j+1}: v' = F/m + g is constant over the step, so RK4 on (p, v) is
+    //     exact and the stage positions are closed-form; tau = M - p_stage x F ---
+    const float2 axy = ffma2(F, im_2, gxy);
+    const float az = fmaf(Fz, p.inv_mass, p.g[2]);
+    float2 k1A, k1B, k1C, k2A, k2B, k2C, k3A, k3B, k3C, k4A, k4B, k4C;
+    ang_deriv(p, A, Bq, C, Mx - fmaf(pxy.y, Fz, -pz * F.y), My - fmaf(pz, F.x, -pxy.x * Fz),
+              Mz - fmaf(pxy.x, F.y, -pxy.y * F.x), k1A, k1B, k1C);
+    {
+      const float2 q = ffma2(hdt_2, vxy, pxy);
+      const float qz = fmaf(hdt, vz, pz);
+      ang_deriv(p, ffma2(hdt_2, k1A, A), ffma2(hdt_2, k1B, Bq), ffma2(hdt_2, k1C, C),
+                Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
+                k2A, k2B, k2C);
+    }
+    {
+      const float2 q = ffma2(dt2q_2, axy, ffma2(hdt_2, vxy, pxy));
+      const float qz = fmaf(dt2q, az, fmaf(hdt, vz, pz));
+      ang_deriv(p, ffma2(hdt_2, k2A, A), ffma2(hdt_2, k2B, Bq), ffma2(hdt_2, k2C, C),
+                Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
+                k3A, k3B, k3C);
+    }
+    const float2 n = ffma2(dt2h_2, axy, ffma2(dt_2, vxy, pxy));
+    const float nz = fmaf(dt2h, az, fmaf(dt, vz, pz));
+    ang_deriv(p, ffma2(dt_2, k3A, A), ffma2(dt_2, k3B, Bq), ffma2(dt_2, k3C, C), Mx - fmaf(n.y, Fz, -nz * F.y),
+              My - fmaf(nz, F.x, -n.x * Fz), Mz - fmaf(n.x, F.y, -n.y * F.x), k4A, k4B, k4C);
+    A = ffma2(dt6_2, ffma2(two_2, fadd2(k2A, k3A), fadd2(k1A, k4A)), A);
+    Bq = ffma2(dt6_2, ffma2(two_2, fadd2(k2B, k3B), fadd2(k1B, k4B)), Bq);
+    C = ffma2(dt6_2, ffma2(two_2, fadd2(k2C, k3C), fadd2(k1C, k4C)), C);
+    pxy = n;
+    pz = nz;
+    vxy = ffma2(dt_2, axy, vxy);
+    vz = fmaf(dt, az, vz);
+    // --- divergence of x_{j+1} (L26); NaN fails every <= test ---
+    const float big = fmaxf(fmaxf(fmaxf(fabsf(pxy.x), fabsf(pxy.y)), fmaxf(fabsf(pz), fabsf(vxy.x))),
+                            fmaxf(fmaxf(fabsf(vxy.y), fabsf(vz)), fmaxf(fabsf(A.x), fabsf(Bq.x))));
+    const float big2 = fmaxf(fmaxf(fabsf(Bq.y), fabsf(C.x)), fabsf(C.y));
+    bad = bad || !(big <= 1e6f) || !(big2 <= 1e6f) || !(fabsf(A.y) < kPitchMax);
+  }
+  const float df = p.freq_hz[fi] - p.f_nominal;
+  J = fmaf(p.rho * df, df, J);  // P:350, once per rollout (L14)
+  return (bad || !(J <= FLT_MAX)) ? kInf : J;
+}
+
+// Latency mode, producer warps: the stance-leg table of the integrator warp on the same
+// SM sub-partition (warp w: integrator warp w % 4, step class w / 4 - 1), chunk by chunk.
+template <int P>
+__device__ __forceinline__ void produce_forces(const Params& p, const RobotSmem& s, const float* s_th, const int* s_fi,
+                                               float* tab) {
+  constexpr int D = 12 * P;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = 32 * (warp & 3) + lane, cls = (warp >> 2) - 1;
+  Theta<P> th;
+#pragma unroll
+  for (int d = 0; d < D; ++d) theta_set(th, d, s_th[col * (D + 1) + d]);
+  const uint8_t* ct = s.ctab[s_fi[col]];
+  for (int c = 0; ab_chunk(c) < p.H; ++c) {
+    const int j1 = min(ab_chunk(c + 1), p.H);
+    for (int j = ab_chunk(c) + cls; j < j1; j += kAbWarpsPerSmsp) store_forces(tab, j, col, step_forces<P>(p, th, ct[j], j, s));
+    named_arrive(1 + c, kBlock * (1 + kAbWarpsPerSmsp));
+  }
+}
+
 // (J, k) lexicographic order: argmin with lowest-index tie-break (L4, L5)
 __device__ __forceinline__ bool jk_less(float ja, int ka, float jb, int kb) {
   return ja < jb || (ja == jb && ka < kb);
 }
 
+__device__ __forceinline__ uint32_t cost_key(float J);
+// (J, k) argmin of a warp, the winner's theta1 index: two integer min-reductions
+// (REDUX) over the order-preserving cost key and, among the tied lanes, the index.
+// Same result as a jk_less butterfly (k is unique per sample; only the sentinel
+// lanes (+inf, 0x7fffffff) can tie completely, and then lane 0 wins in both).
 __device__ __forceinline__ void warp_argmin(float& m, int& mk, int& mf) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-    const int k2 = __shfl_xor_sync(0xffffffffu, mk, o);
-    const int f2 = __shfl_xor_sync(0xffffffffu, mf, o);
-    if (jk_less(m2, k2, m, mk)) {
-      m = m2;
-      mk = k2;
-      mf = f2;
-    }
-  }
+  const uint32_t key = cost_key(m);
+  const uint32_t kmin = __reduce_min_sync(0xffffffffu, key);
+  const uint32_t kk = __reduce_min_sync(0xffffffffu, key == kmin ? (uint32_t)mk : 0xffffffffu);
+  const uint32_t who = __ballot_sync(0xffffffffu, key == kmin && (uint32_t)mk == kk);
+  const int src = __ffs(who) - 1;
+  m = __shfl_sync(0xffffffffu, m, src);
+  mf = __shfl_sync(0xffffffffu, mf, src);
+  mk = (int)kk;
 }
 
 // Partial record of (robot r, part c): CTA partials [R][n_cta] (part_c_stride = 1)
@@ -900,27 +1215,44 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
   float* s_th = s_red + (EPI == EPI_MPPI ? NR * (kBlock + 1) : 0);
   int* s_fi = reinterpret_cast<int*>(s_th + TS * (D + 1));
   const bool sampler_thread = !SPLIT || threadIdx.x < kBlock;  // holds a sample in phase 2 / the epilogue
-  __shared__ float s_wm[kBlock / 32], s_ws[kBlock / 32], s_wn[kBlock / 32];
-  __shared__ int s_wk[kBlock / 32], s_wf[kBlock / 32];
-  __shared__ float s_tile_m, s_run_m, s_run_sj, s_run_nf;
-  __shared__ int s_tile_k, s_tile_f, s_run_k, s_run_f;
+  __shared__ float s_wm[2][kBlock / 32], s_ws[2][kBlock / 32], s_wn[2][kBlock / 32];  // per warp, by tile parity
+  __shared__ int s_wk[2][kBlock / 32], s_wf[2][kBlock / 32];
+  // the CTA's running record header (MPPI: double-buffered by tile parity, read by the
+  // row threads, advanced by thread 0; argmin epilogue: thread 0 only)
+  __shared__ float s_rm[2], s_rsj, s_rnf;
+  __shared__ int s_rk[2], s_rf[2];
+  if (threadIdx.x == 0) {
+    s_rm[0] = kInf;
+    s_rk[0] = 0x7fffffff;
+    s_rf[0] = 0;
+    s_rsj = 0.f;
+    s_rnf = 0.f;
+  }
+  int par = 0;  // parity of this CTA's current tile
+  // SPLIT (one tile per CTA): the header lives in registers, the same in every thread
+  float h_m = kInf, h_sj = 0.f, h_nf = 0.f;
+  int h_k = 0x7fffffff, h_f = 0;
 
   const int r = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   griddep_wait();  // PDL: the previous iteration's distribution / the closed loop's new inputs
   if (blockIdx.x == 0) SBS_TS(0);
-  load_robot(p, r, s);
-  if (FC) stage_chol_t(p, r, s_red);
-  if (tid == 0) {
-    s_run_m = kInf;
-    s_run_k = 0x7fffffff;
-    s_run_f = 0;
-    s_run_sj = 0.f;
-    s_run_nf = 0.f;
+  SBS_CTS(0);
+  const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
+  SplitNoise<P> zn;  // SPLIT: this lane's noise for the CTA's first tile
+  if (SPLIT) {       // the inputs' round trips overlap the first tile's Philox / Box-Muller draws
+    __shared__ float s_mraw[SBS_MAX_D];
+    load_robot_issue(p, r, s, s_mraw);
+    const uint32_t it = step_iter(p);
+    const int64_t kl1 = (int64_t)blockIdx.x * kBlock + tid / kSplitLanes;
+    if (kl1 < p.K_local) split_noise<P>(p, robot_g, p.k_begin + kl1, it, tid % kSplitLanes, zn);
+    load_robot_commit(p, s, s_mraw, it);
+  } else {
+    load_robot(p, r, s);
   }
+  if (FC) stage_chol_t(p, r, s_red);
   __syncthreads();
   if (blockIdx.x == 0) SBS_TS(1);
-  const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
   float run = 0.0f;  // running partial of row `tid` (MPPI)
 
   for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
@@ -931,6 +1263,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
     float J = kInf;
     int fi = 0;
     if (SPLIT) {  // phase 1: kSplitLanes lanes per sample draw its Philox blocks into shared memory
+      if (tile != (int)blockIdx.x) __syncthreads();  // (one tile per CTA in this mode; s_th readers done)
       const int sl = tid / kSplitLanes, u = tid % kSplitLanes;
       const int64_t kl1 = (int64_t)tile * TS + sl;
       if (kl1 < p.K_local) {
@@ -940,32 +1273,46 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
           for (int d = u; d < D; d += kSplitLanes) dst[d] = s.mu[d];
           if (u == 0) s_fi[sl] = s.cur_idx;
         } else {
+          if (tile != (int)blockIdx.x) split_noise<P>(p, robot_g, k1, s.iter, u, zn);  // (later tiles)
           const bool grp = p.n_sig_groups > 1;
           const float sc = grp ? p.sig_scale[(int)(k1 % p.n_sig_groups)] : 1.0f;
-          for (int q = u; q < D / 4; q += kSplitLanes) {
-            const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k1, s.iter, robot_g, p.rk);
-            float z[4];
-            box_muller(w.x, w.y, z[0], z[1]);
-            box_muller(w.z, w.w, z[2], z[3]);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float sg = grp ? __fmul_rn(s.sig[4 * q + i], sc) : s.sig[4 * q + i];
-              dst[4 * q + i] = __fmaf_rn(sg, z[i], s.mu[4 * q + i]);
+          for (int i = 0; i < SplitNoise<P>::NB; ++i) {
+            const int q = u + kSplitLanes * i;
+            if (q < D / 4) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const float sg = grp ? __fmul_rn(s.sig[4 * q + c], sc) : s.sig[4 * q + c];
+                dst[4 * q + c] = __fmaf_rn(sg, zn.z[i][c], s.mu[4 * q + c]);
+              }
             }
           }
-          if (u == 0) {
-            int idx = s.cur_idx;
-            if (p.gait_adapt) {
-              const U4 w = philox4x32_10_rk(0x80000000u, (uint32_t)k1, s.iter, robot_g, p.rk);
-              idx = (int)__umulhi(w.x, (uint32_t)p.n_freq);
-            }
-            s_fi[sl] = idx;
-          }
+          if (u == 0) s_fi[sl] = zn.fi >= 0 ? zn.fi : s.cur_idx;
         }
+      } else {  // past K: a valid contact-table row for the producer warps (results unused)
+        if (u == 0) s_fi[sl] = 0;
       }
       __syncthreads();
     }
-    if (valid) {
+    if (SPLIT && p.ab) {  // warps 4..15 tabulate the stance-leg forces, warps 0..3 integrate
+      float* tab = reinterpret_cast<float*>(s_fi + TS);
+      if (!sampler_thread) {
+        produce_forces<P>(p, s, s_th, s_fi, tab);
+      } else {
+        fi = s_fi[tid];
+        if (blockIdx.x == 0) SBS_TS(2);
+        SBS_CTS(1);
+        SBS_CTS(4);
+        const float Ja = rollout_ab<P>(p, fi, s, tab, tid);  // (every integrator lane: barriers)
+        SBS_CTS(5);
+        SBS_CTS(2);
+        if (blockIdx.x == 0) SBS_TS(3);
+        if (valid) {
+          J = Ja;
+          p.J[(size_t)r * p.K_local + kl] = J;
+        }
+      }
+    } else if (valid) {
       if (SPLIT) {
 #pragma unroll
         for (int d = 0; d < D; ++d) theta_set(th, d, s_th[tid * (D + 1) + d]);
@@ -976,7 +1323,11 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
         fi = draw_sample<P, false>(p, robot_g, k, s, th);
       }
       if (blockIdx.x == 0) SBS_TS(2);
+      SBS_CTS(1);
+      SBS_CTS(4);
       J = rollout<P>(p, th, fi, s);
+      SBS_CTS(5);
+      SBS_CTS(2);
       if (blockIdx.x == 0) SBS_TS(3);
       p.J[(size_t)r * p.K_local + kl] = J;
     }
@@ -993,93 +1344,147 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
         nf += __shfl_xor_sync(0xffffffffu, nf, o);
       }
       if (lane == 0 && sampler_thread) {
-        s_wm[warp] = m;
-        s_wk[warp] = mk;
-        s_wf[warp] = mf;
-        s_ws[warp] = sj;
-        s_wn[warp] = nf;
+        s_wm[par][warp] = m;
+        s_wk[par][warp] = mk;
+        s_wf[par][warp] = mf;
+        s_ws[par][warp] = sj;
+        s_wn[par][warp] = nf;
       }
       __syncthreads();
-      if (tid == 0) {
+      if (SPLIT) {
+#pragma unroll
         for (int w = 0; w < kBlock / 32; ++w) {
-          if (jk_less(s_wm[w], s_wk[w], s_run_m, s_run_k)) {
-            s_run_m = s_wm[w];
-            s_run_k = s_wk[w];
-            s_run_f = s_wf[w];
+          if (jk_less(s_wm[par][w], s_wk[par][w], h_m, h_k)) {
+            h_m = s_wm[par][w];
+            h_k = s_wk[par][w];
+            h_f = s_wf[par][w];
           }
-          s_run_sj += s_ws[w];
-          s_run_nf += s_wn[w];
+          h_sj += s_ws[par][w];
+          h_nf += s_wn[par][w];
+        }
+      } else if (tid == 0) {
+        for (int w = 0; w < kBlock / 32; ++w) {
+          if (jk_less(s_wm[par][w], s_wk[par][w], s_rm[0], s_rk[0])) {
+            s_rm[0] = s_wm[par][w];
+            s_rk[0] = s_wk[par][w];
+            s_rf[0] = s_wf[par][w];
+          }
+          s_rsj += s_ws[par][w];
+          s_rnf += s_wn[par][w];
         }
       }
-      __syncthreads();
+      par ^= 1;
       continue;
     }
     // ---- step a5 (MPPI), per tile: weights relative to the tile min, then an
     //      online-softmax merge into this CTA's running record ----
     if (lane == 0 && sampler_thread) {
-      s_wm[warp] = m;
-      s_wk[warp] = mk;
-      s_wf[warp] = mf;
+      s_wm[par][warp] = m;
+      s_wk[par][warp] = mk;
+      s_wf[par][warp] = mf;
     }
     __syncthreads();
-    if (tid == 0) {
-      float bm = s_wm[0];
-      int bk = s_wk[0], bf = s_wf[0];
-      for (int w = 1; w < kBlock / 32; ++w)
-        if (jk_less(s_wm[w], s_wk[w], bm, bk)) {
-          bm = s_wm[w];
-          bk = s_wk[w];
-          bf = s_wf[w];
-        }
-      s_tile_m = bm;
-      s_tile_k = bk;
-      s_tile_f = bf;
-    }
-    __syncthreads();
-    const float mt = s_tile_m;
+    float mt = s_wm[par][0];  // tile argmin, computed by every thread
+    int tk = s_wk[par][0], tf = s_wf[par][0];
+#pragma unroll
+    for (int w = 1; w < kBlock / 32; ++w)
+      if (jk_less(s_wm[par][w], s_wk[par][w], mt, tk)) {
+        mt = s_wm[par][w];
+        tk = s_wk[par][w];
+        tf = s_wf[par][w];
+      }
+
     const float w = fin ? __expf((mt - J) * p.inv_lambda) : 0.0f;
-    if (valid) {
+    constexpr int kQ = 4;  // SPLIT: sample quarters per reduced row
+    if (SPLIT) {           // theta is already in shared memory: rows reduced straight from s_th by 4 x NR threads
+      float* s_w = s_red + kQ * NR;  // [4][kBlock]: w, w^2, finite J, finite
+      if (sampler_thread) {
+        s_w[0 * kBlock + tid] = w;
+        s_w[1 * kBlock + tid] = w * w;
+        s_w[2 * kBlock + tid] = fin ? J : 0.0f;
+        s_w[3 * kBlock + tid] = fin ? 1.0f : 0.0f;
+      }
+      __syncthreads();
+      if (tid < kQ * NR) {
+        const int row = tid % NR, q = tid / NR, i0 = q * (kBlock / kQ);
+        const int64_t left = p.K_local - ((int64_t)tile * TS + i0);
+        const int nv = left <= 0 ? 0 : (left >= kBlock / kQ ? kBlock / kQ : (int)left);
+        float a0 = 0.f, a1 = 0.f;
+        if (row < D) {
+          const float* col = s_th + row;
+          int i = 0;
+          for (; i + 1 < nv; i += 2) {
+            a0 = fmaf(s_w[i0 + i], col[(i0 + i) * (D + 1)], a0);
+            a1 = fmaf(s_w[i0 + i + 1], col[(i0 + i + 1) * (D + 1)], a1);
+          }
+          if (i < nv) a0 = fmaf(s_w[i0 + i], col[(i0 + i) * (D + 1)], a0);
+        } else {
+          const float* rw = s_w + (row - D) * kBlock + i0;
+          for (int i = 0; i < kBlock / kQ; i += 2) {
+            a0 += rw[i];
+            a1 += rw[i + 1];
+          }
+        }
+        s_red[q * NR + row] = a0 + a1;
+      }
+      __syncthreads();
+    } else {
+      if (valid) {
 #pragma unroll
-      for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = w * theta_get(th, d);
-    } else if (sampler_thread) {
+        for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = w * theta_get(th, d);
+      } else {
 #pragma unroll
-      for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = 0.0f;
-    }
-    if (sampler_thread) {
+        for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = 0.0f;
+      }
       s_red[(D + 0) * (kBlock + 1) + tid] = w;
       s_red[(D + 1) * (kBlock + 1) + tid] = w * w;
       s_red[(D + 2) * (kBlock + 1) + tid] = fin ? J : 0.0f;
       s_red[(D + 3) * (kBlock + 1) + tid] = fin ? 1.0f : 0.0f;
+      __syncthreads();
     }
-    __syncthreads();
-    const float mr = s_run_m;
+    const float mr = SPLIT ? h_m : s_rm[par];
     const float mn = fminf(mr, mt);
     if (tid < NR) {
-      const float* rowp = &s_red[tid * (kBlock + 1)];
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      float v;
+      if (SPLIT) {
+        v = (s_red[0 * NR + tid] + s_red[1 * NR + tid]) + (s_red[2 * NR + tid] + s_red[3 * NR + tid]);
+      } else {
+        const float* rowp = &s_red[tid * (kBlock + 1)];
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll 8
-      for (int i = 0; i < kBlock; i += 4) {
-        a0 += rowp[i];
-        a1 += rowp[i + 1];
-        a2 += rowp[i + 2];
-        a3 += rowp[i + 3];
+        for (int i = 0; i < kBlock; i += 4) {
+          a0 += rowp[i];
+          a1 += rowp[i + 1];
+          a2 += rowp[i + 2];
+          a3 += rowp[i + 3];
+        }
+        v = (a0 + a1) + (a2 + a3);
       }
-      const float v = (a0 + a1) + (a2 + a3);
       const float sa = (mr < kInf) ? __expf((mn - mr) * p.inv_lambda) : 0.0f;
       const float sb = (mt < kInf) ? __expf((mn - mt) * p.inv_lambda) : 0.0f;
       if (tid < D + 1) run = fmaf(run, sa, v * sb);
       else if (tid == D + 1) run = fmaf(run, sa * sa, v * (sb * sb));
       else run += v;
     }
-    __syncthreads();
-    if (tid == 0 && jk_less(mt, s_tile_k, s_run_m, s_run_k)) {
-      s_run_m = mt;
-      s_run_k = s_tile_k;
-      s_run_f = s_tile_f;
+    if (SPLIT) {
+      if (jk_less(mt, tk, h_m, h_k)) {
+        h_m = mt;
+        h_k = tk;
+        h_f = tf;
+      }
+    } else if (tid == 0) {  // next header (the other buffer: this tile's readers may still be reading this one)
+      const bool t = jk_less(mt, tk, s_rm[par], s_rk[par]);
+      s_rm[par ^ 1] = t ? mt : s_rm[par];
+      s_rk[par ^ 1] = t ? tk : s_rk[par];
+      s_rf[par ^ 1] = t ? tf : s_rf[par];
     }
-    __syncthreads();
+    par ^= 1;
+    if (!SPLIT) __syncthreads();  // (measured: throughput mode runs faster with the CTA's warps in step)
   }
-  griddep_launch_dependents();  // (CEM: the select kernel may be scheduled; it waits for this grid)
+  // the next iteration's kernels may be scheduled.  Not for the CEM rollout: a select
+  // kernel scheduled early, next to the running rollout, was measured 1.5x slower
+  // after an L2 flush (its CTA then starts at grid completion, still PDL-ordered)
+  if (FUSED) griddep_launch_dependents();
   float* out = p.part + ((size_t)r * p.n_cta + blockIdx.x) * p.part_stride;
   if (EPI == EPI_MPPI) {
     if (tid < D) out[kPartHdr + tid] = run;
@@ -1087,16 +1492,18 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
   } else if (tid == 0) {
     out[3] = 0.f;
     out[4] = 0.f;
-    out[5] = s_run_sj;
-    out[6] = s_run_nf;
+    out[5] = SPLIT ? h_sj : s_rsj;
+    out[6] = SPLIT ? h_nf : s_rnf;
   }
   if (tid == 0) {
-    out[0] = s_run_m;
-    out[1] = __int_as_float(s_run_k);
-    out[2] = __int_as_float(s_run_f);
+    const int hp = EPI == EPI_MPPI ? par : 0;
+    out[0] = SPLIT ? h_m : s_rm[hp];
+    out[1] = __int_as_float(SPLIT ? h_k : s_rk[hp]);
+    out[2] = __int_as_float(SPLIT ? h_f : s_rf[hp]);
     out[7] = 0.0f;
   }
   if (blockIdx.x == 0) SBS_TS(4);
+  SBS_CTS(3);
   if (FUSED) {
     if (arrive_last(p.counter + r, gridDim.x)) {
       SBS_TS(5);
@@ -1430,6 +1837,7 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_cons
   else select_block(J, K, Ke, kb, el, eJ, sel_smem);
   __syncthreads();
   if (blockIdx.x == 0) SBS_TS(6);
+
   if (MODE == SEL_EMIT) {
     float* o = emit + (size_t)r * p.ex_stride + kPartHdr;
     for (int64_t e = tid; e < Ke; e += blockDim.x) {
@@ -1484,6 +1892,7 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
   load_robot(p, r, s, false);  // (not written by the select kernel: may overlap it)
   griddep_wait();              // the select kernel's elite list and diagnostics
+  if (blockIdx.x == 0) SBS_TS(11);
   const bool has_e = e < p.n_elite;
   const int64_t k = has_e ? p.elite[(size_t)r * p.n_elite + e] : 0;
   const float Je = has_e ? p.elite_J[(size_t)r * p.n_elite + e] : kInf;
@@ -1567,6 +1976,7 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   }
   write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, b.m,
                s_diag[4] > 0.f ? s_diag[3] / s_diag[4] : kInf, ne, ne, (int)((float)p.K_global - s_diag[4]), s_pre);
+  SBS_TS(12);
 }
 
 // ---------------------------------------------------------------------------
@@ -1778,7 +2188,7 @@ __global__ void __launch_bounds__(128) sbs_debug_samples_kernel(const __grid_con
 // launch with programmatic stream serialisation (PDL): the kernel may start while the
 // previous kernel on the stream drains; it waits in griddep_wait() for its inputs
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, int kind, cudaStream_t s,
                               Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -1788,6 +2198,14 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+#if defined(SBS_TIMING)  // experiments: SBS_NO_PDL=<mask> launches without the attribute (1 rollout, 2 select, 4 elite)
+  {
+    static const int mask = getenv("SBS_NO_PDL") ? atoi(getenv("SBS_NO_PDL")) : 0;
+    if (mask & kind) attr[0].val.programmaticStreamSerializationAllowed = 0;
+  }
+#else
+  (void)kind;
+#endif
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, args...);
@@ -1815,8 +2233,9 @@ constexpr size_t rollout_smem() {
 template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false>
 static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
   dim3 grid(p.n_cta, p.R);
+  const size_t smem = SPLIT ? split_smem_bytes(P, EPI == EPI_MPPI, p.H, p.ab != 0) : rollout_smem<P, EPI, FC, SPLIT>();
   return launch_pdl(sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT>, grid, dim3(SPLIT ? kBlock * kSplitLanes : kBlock),
-                    rollout_smem<P, EPI, FC, SPLIT>(), s, p);
+                    smem, 1, s, p);
 }
 
 template <int P>
@@ -1859,8 +2278,8 @@ template <int P>
 cudaError_t PEntry<P>::elite(const Params& p, cudaStream_t s) {
   dim3 grid(p.n_eblk, p.R);
   if (p.full_cov)
-    return launch_pdl(sbs_cov_kernel<P>, grid, dim3(32 * 3 * P), (size_t)cov_smem_floats(12 * P) * sizeof(float), s, p);
-  return launch_pdl(sbs_elite_kernel<P>, grid, dim3(32 * 3 * P), 0, s, p);
+    return launch_pdl(sbs_cov_kernel<P>, grid, dim3(32 * 3 * P), (size_t)cov_smem_floats(12 * P) * sizeof(float), 4, s, p);
+  return launch_pdl(sbs_elite_kernel<P>, grid, dim3(32 * 3 * P), 0, 4, s, p);
 }
 
 template <int P>
@@ -1880,7 +2299,7 @@ cudaError_t PEntry<P>::debug_samples(const Params& p, int robot, int64_t k0, int
 
 template <int P>
 cudaError_t PEntry<P>::prepare() {
-  const int big = 96 * 1024, huge = 200 * 1024;
+  const int big = 96 * 1024, huge = (int)kSplitSmemMax;
   cudaError_t e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -1922,6 +2341,9 @@ template struct PEntry<SBS_TU_P>;
 #define SBS_CAT(a, b) SBS_CAT2(a, b)
 extern "C" int SBS_CAT(sbs_debug_ts_p, SBS_TU_P)(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_sbs_ts, sizeof(g_sbs_ts));
+}
+extern "C" int SBS_CAT(sbs_debug_cta_p, SBS_TU_P)(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_sbs_cta, sizeof(g_sbs_cta));
 }
 #endif
 #endif  // SBS_TU_P
@@ -2004,8 +2426,8 @@ cudaError_t prepare_kernels(int P) {
 template <int MODE>
 static cudaError_t launch_select_t(const Params& p, int64_t K, float* emit, cudaStream_t s) {
   const size_t smem = select_smem(K);
-  if (K <= kSelSmallMax) return launch_pdl(sbs_select_kernel<MODE, true>, dim3(p.R), dim3(kSelBlock), smem, s, p, emit);
-  return launch_pdl(sbs_select_kernel<MODE, false>, dim3(p.R), dim3(kSelBlock), smem, s, p, emit);
+  if (K <= kSelSmallMax) return launch_pdl(sbs_select_kernel<MODE, true>, dim3(p.R), dim3(kSelBlock), smem, 2, s, p, emit);
+  return launch_pdl(sbs_select_kernel<MODE, false>, dim3(p.R), dim3(kSelBlock), smem, 2, s, p, emit);
 }
 
 cudaError_t launch_select(const Params& p, cudaStream_t s) { return launch_select_t<SEL_LOCAL>(p, p.K_local, nullptr, s); }

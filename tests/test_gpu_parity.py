@@ -359,6 +359,43 @@ def test_host_path_equals_device_path(B):
             assert oa[0]["iter"] == ob["iter"] and oa[0]["freq_idx"] == ob["freq_idx"]
 
 
+@pytest.mark.parametrize("mode", ["mppi", "naive", "cem"])
+@pytest.mark.parametrize("H", [12, 7, 24, 40])
+def test_latency_mode_variants_are_bitwise_equal(B, mode, H, monkeypatch):
+    """The latency-mode rollout with and without the producer / integrator warp split
+    (SBS_AB: 12 warps tabulate the stance-leg forces while 4 warps run RK4) computes the
+    same bits: costs, means, elites.  The throughput-mode rollout (one thread per sample,
+    its own instruction schedule and MPPI reduction order) agrees to rounding."""
+    base = W.config3(mode, K=3000) if mode != "mppi" else W.config2(K=3000)
+    cfg, inputs = base
+    cfg = dict(cfg, horizon=H)
+    inputs = [W.robot_input(cfg, 0, cmd=(0.4, 0.0, 0.1))]
+    res = {}
+    for tag, env in (("ab", {}), ("split", {"SBS_AB": "0"}), ("plain", {"SBS_SPLIT": "0"})):
+        for k in ("SBS_AB", "SBS_SPLIT"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        c = _ctrl(B, cfg, inputs)
+        outs = [c.step(inputs)[1][0] for _ in range(2)]
+        res[tag] = (c.debug_costs().copy(), outs, c.debug_elites(0).copy() if mode == "cem" else None)
+    np.testing.assert_array_equal(res["split"][0], res["ab"][0])
+    for oa, ob in zip(res["split"][1], res["ab"][1]):
+        for key in ("mean", "var", "u0"):
+            np.testing.assert_array_equal(oa[key], ob[key])
+    if mode == "cem":
+        np.testing.assert_array_equal(res["split"][2], res["ab"][2])
+    if H > 12:  # long horizons amplify rounding differences chaotically (divergence threshold)
+        return
+    Ja, Jp = res["ab"][0], res["plain"][0]
+    assert np.array_equal(np.isfinite(Ja), np.isfinite(Jp))
+    f = np.isfinite(Ja)
+    assert np.all(np.abs(Ja[f] - Jp[f]) <= 1e-4 * np.abs(Jp[f]) + 1e-6)
+    o_a, o_p = res["ab"][1][0], res["plain"][1][0]           # first iteration: same distribution in
+    for key in ("mean", "u0"):
+        assert np.max(np.abs(o_a[key] - o_p[key])) <= 1e-4 * max(float(np.max(np.abs(o_p[key]))), 1.0)
+
+
 def test_reference_from_device_memory(B):
     """sbs_set_reference_device (device buffer, stream-ordered) is the same reference as
     sbs_set_reference for both the host path and the device path."""
