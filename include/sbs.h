@@ -146,7 +146,7 @@ typedef struct sbs_output {
   float omega;            /* MPPI: sum of weights Omega; CEM/Naive: number of elites used */
   float ess;              /* MPPI effective sample size Omega^2 / sum w^2 */
   int32_t n_diverged;     /* rollouts with J = +inf */
-  float device_us;        /* device time of the step, CUDA events (sbs_step only; 0 otherwise) */
+  float device_us;        /* device time of the step, CUDA events (sbs_step with sbs_profile on; 0 otherwise) */
   float mean[SBS_MAX_D];  /* new mean theta2 (first D entries valid) */
   float var[SBS_MAX_D];   /* new diagonal covariance */
 } sbs_output;
@@ -182,7 +182,11 @@ int sbs_set_iter(sbs_ctx* ctx, uint32_t iter);
  * iteration counter travel inside the kernel parameters (direct launch, no
  * copy); otherwise one pinned block [iter | inputs | references] is copied up
  * by a captured CUDA graph.  The finishing kernel writes the outputs straight
- * into the context's mapped pinned memory; they are copied to `out` on return. */
+ * into the context's mapped pinned memory; they are copied to `out` on return.
+ * Completion (R = 1): the finishing CTA raises a mapped flag after its outputs
+ * (system-scope fence) and the calling thread spins on it (checking the stream
+ * for errors every 1024 polls) instead of synchronising the stream; later work
+ * on the context's stream stays stream-ordered behind the step's kernels. */
 int sbs_step(sbs_ctx* ctx, const sbs_input* in, sbs_output* out);
 
 /* Same iteration with device-resident inputs/outputs (R entries each),

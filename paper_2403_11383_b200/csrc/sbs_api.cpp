@@ -122,7 +122,11 @@ struct sbs_ctx {
   sbs_output* h_out = nullptr; // pinned, mapped: the host path's kernels write the outputs here directly
   sbs_output* h_out_dev = nullptr;  // device address of h_out (null: copied back by a D2H node)
   cudaEvent_t blk_ev = nullptr;  // last H2D of h_blk (the host rewrites it only after this completed)
+  bool blk_busy = true;          // blk_ev recorded since the last wait on it
   bool ref_dirty = false;
+  uint32_t* h_done = nullptr;    // one-robot host path: mapped completion flag (after h_out), its device address,
+  uint32_t* d_done = nullptr;    // and the value of the last step
+  uint32_t done_seq = 0;
   cudaGraphExec_t graph = nullptr;
   // closed loop (sbs_run_loop): device words {iteration counter, counter at call start, arrival counter},
   // pinned staging of the start value, and one captured iteration keyed by its arguments
@@ -149,6 +153,22 @@ struct sbs_ctx {
   nccl_comm_t comm = nullptr;
   bool external = false;  // world > 1 with an all-zero nccl_id: the caller exchanges the records
 };
+
+namespace {
+// the pinned block may be rewritten once its last upload (blk_ev) has completed;
+// a host flag skips the driver call when nothing was recorded since the last wait
+cudaError_t blk_wait(sbs_ctx* c) {
+  if (!c->blk_busy) return cudaSuccess;
+  const cudaError_t e = cudaEventSynchronize(c->blk_ev);
+  if (e == cudaSuccess) c->blk_busy = false;
+  return e;
+}
+cudaError_t blk_record(sbs_ctx* c, cudaStream_t s) {
+  c->blk_busy = true;
+  return cudaEventRecord(c->blk_ev, s);
+}
+}  // namespace
+
 
 namespace {
 
@@ -589,7 +609,7 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   c->d_in = reinterpret_cast<sbs_input*>(c->d_blk + c->blk_in_off);
   c->d_xref = reinterpret_cast<float*>(c->d_blk + c->blk_ref_off);
   CKC(cudaEventCreateWithFlags(&c->blk_ev, cudaEventDisableTiming));
-  CKC(cudaEventRecord(c->blk_ev, c->stream));
+  CKC(blk_record(c, c->stream));
   CKC(cudaMalloc(&c->d_J, (size_t)R * P.K_local * sizeof(float)));
   CKC(cudaMalloc(&c->d_part, (size_t)R * P.n_cta * P.part_stride * sizeof(float)));
   if (cfg->world > 1) {
@@ -617,10 +637,17 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaMalloc(&c->d_epart, (size_t)R * P.n_eblk * erec * sizeof(float)));
   CKC(cudaMalloc(&c->d_sdiag, (size_t)R * 8 * sizeof(float)));
   CKC(cudaMalloc(&c->d_out, R * sizeof(sbs_output)));
-  CKC(cudaHostAlloc(&c->h_out, R * sizeof(sbs_output), cudaHostAllocMapped));
+  CKC(cudaHostAlloc(&c->h_out, R * sizeof(sbs_output) + 64, cudaHostAllocMapped));  // + the completion flag
+  c->h_done = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c->h_out) + R * sizeof(sbs_output));
+  *c->h_done = 0;
   {
     const char* e = getenv("SBS_MAPPED_OUT");  // experiments: SBS_MAPPED_OUT=0 copies the outputs back instead
-    if (!e || atoi(e) != 0) CKC(cudaHostGetDevicePointer((void**)&c->h_out_dev, c->h_out, 0));
+    if (!e || atoi(e) != 0) {
+      CKC(cudaHostGetDevicePointer((void**)&c->h_out_dev, c->h_out, 0));
+      const char* f = getenv("SBS_POLL");  // experiments: SBS_POLL=0 waits with cudaStreamSynchronize instead
+      if (!f || atoi(f) != 0)
+        c->d_done = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c->h_out_dev) + R * sizeof(sbs_output));
+    }
   }
   // initial distribution: mean (0, 0, m|g_z|/4) per leg and knot, var = sigma^2, freq_idx 0
   {
@@ -693,7 +720,7 @@ int sbs_set_reference(sbs_ctx* c, int32_t robot, const float* x_ref) {
   CK(cudaSetDevice(c->cfg.device));
   // staged in pinned memory (the caller's buffer is free on return); uploaded with
   // the next step's inputs.  The block is rewritten only after its last upload.
-  CK(cudaEventSynchronize(c->blk_ev));
+  CK(blk_wait(c));
   memcpy(c->h_xref + (size_t)robot * n, x_ref, n * sizeof(float));
   c->ref_dirty = true;
   c->ref_set[robot] = 1;
@@ -704,7 +731,7 @@ int sbs_set_reference_device(sbs_ctx* c, const float* d_x_ref, void* stream) {
   if (!c || !d_x_ref) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
   CK(cudaSetDevice(c->cfg.device));
   if (c->ref_dirty) {  // host-staged references of earlier calls are superseded
-    CK(cudaEventSynchronize(c->blk_ev));
+    CK(blk_wait(c));
     c->ref_dirty = false;
   }
   CK(cudaMemcpyAsync(c->d_xref, d_x_ref, (size_t)c->P.R * c->P.H * 12 * sizeof(float), cudaMemcpyDeviceToDevice,
@@ -712,7 +739,7 @@ int sbs_set_reference_device(sbs_ctx* c, const float* d_x_ref, void* stream) {
   // keep the pinned copy in sync for later host-path steps
   CK(cudaMemcpyAsync(c->h_xref, d_x_ref, (size_t)c->P.R * c->P.H * 12 * sizeof(float), cudaMemcpyDeviceToHost,
                      (cudaStream_t)stream));
-  CK(cudaEventRecord(c->blk_ev, (cudaStream_t)stream));
+  CK(blk_record(c, (cudaStream_t)stream));
   std::fill(c->ref_set.begin(), c->ref_set.end(), 1);
   return SBS_OK;
 }
@@ -822,7 +849,31 @@ int enqueue_host_step(sbs_ctx* c, cudaStream_t s) {
 }
 }  // namespace
 
+#if defined(SBS_HOST_TIMING)  // experiments only: host-side phase times of the one-robot sbs_step
+#include <time.h>
+static double g_ht[8];
+static long g_hn;
+static inline double ht_now() {
+  timespec t;
+  clock_gettime(CLOCK_MONOTONIC, &t);
+  return t.tv_sec * 1e6 + t.tv_nsec * 1e-3;
+}
+#define HT(i) (ht[i] = ht_now())
+extern "C" int sbs_debug_host_times(double* out) {
+  for (int i = 0; i < 8; ++i) out[i] = g_hn ? g_ht[i] / g_hn : 0.0;
+  g_hn = 0;
+  for (int i = 0; i < 8; ++i) g_ht[i] = 0.0;
+  return 0;
+}
+#else
+#define HT(i) ((void)0)
+#endif
+
 int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
+#if defined(SBS_HOST_TIMING)
+  double ht[9];
+#endif
+  HT(0);
   if (!c || !in || !out) return fail(c, SBS_ERR_INVALID_ARG, "NULL argument");
   const int R = c->P.R;
   for (int r = 0; r < R; ++r) {
@@ -837,33 +888,68 @@ int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
   if (R == 1 && c->P.H * 12 <= sbs::kInlineRefFloats && c->cfg.world == 1) {
     // inputs, reference and iteration counter ride in the kernel parameters: no copy node,
     // no graph (direct launches); outputs land in mapped pinned memory
-    CK(cudaEventSynchronize(c->blk_ev));  // a reference staged by sbs_set_reference_device has landed in h_xref
+    HT(1);
+    CK(blk_wait(c));  // a reference staged by sbs_set_reference_device has landed in h_xref
+    HT(2);
     Params saved = c->P;
     c->P.inline_in = 1;
     c->P.in_inline = in[0];
     memcpy(c->P.xref_inline, c->h_xref, (size_t)c->P.H * 12 * sizeof(float));
     c->P.iter_dev = nullptr;
     c->P.out = c->h_out_dev ? c->h_out_dev : c->d_out;
-    CK(cudaEventRecord(c->ev0, s));
+    // completion: the finishing CTA raises a mapped flag after the outputs (system-scope
+    // fence) and the host polls it -- no event records, no driver synchronisation; with
+    // sbs_profile on, CUDA events time the step instead (device_us)
+    const bool timed = c->profile != 0;
+    const bool poll = c->d_done && !timed;
+    if (poll) {
+      c->P.done = c->d_done;
+      c->P.done_value = ++c->done_seq;
+    }
+    HT(3);
+    if (timed) CK(cudaEventRecord(c->ev0, s));
+    HT(4);
     const int rc = enqueue_step(c, s);
+    HT(5);
     c->P = saved;
     if (rc != SBS_OK) return rc;
     if (!c->h_out_dev) CK(cudaMemcpyAsync(c->h_out, c->d_out, sizeof(sbs_output), cudaMemcpyDeviceToHost, s));
-    CK(cudaEventRecord(c->ev1, s));
-    CK(cudaStreamSynchronize(s));
+    if (timed) CK(cudaEventRecord(c->ev1, s));
+    HT(6);
+    if (poll) {
+      const volatile uint32_t* flag = c->h_done;
+      for (uint32_t n = 1; *flag != c->done_seq; ++n) {
+        if ((n & 1023u) == 0) {  // a failed launch never raises the flag: ask the stream now and then
+          const cudaError_t e = cudaStreamQuery(s);
+          if (e != cudaErrorNotReady && e != cudaSuccess) CK(e);
+          if (e == cudaSuccess && *flag != c->done_seq) return fail(c, SBS_ERR_CUDA, "step completed without its flag");
+        }
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
+      }
+    } else {
+      CK(cudaStreamSynchronize(s));
+    }
+    HT(7);
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    if (timed) cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     c->h_out[0].device_us = ms * 1000.f;
     memcpy(out, c->h_out, sizeof(sbs_output));
     c->iter += 1;
+    HT(8);
+#if defined(SBS_HOST_TIMING)
+    for (int i = 0; i < 8; ++i) g_ht[i] += ht[i + 1] - ht[i];
+    ++g_hn;
+#endif
     return c->h_out[0].status == SBS_WARN_ALL_DIVERGED ? SBS_WARN_ALL_DIVERGED : SBS_OK;
   }
-  CK(cudaEventSynchronize(c->blk_ev));
+  CK(blk_wait(c));
   memcpy(c->h_blk, &c->iter, sizeof(uint32_t));
   memcpy(c->h_in, in, R * sizeof(sbs_input));
   c->ref_dirty = false;  // the whole block (with the reference) goes up with this step
   const bool use_graph = !c->profile && c->cfg.world == 1;
-  CK(cudaEventRecord(c->ev0, s));  // events stay outside the graph (host-synchronisable)
+  if (c->profile) CK(cudaEventRecord(c->ev0, s));  // events stay outside the graph (host-synchronisable)
   if (use_graph) {
     if (!c->graph) {
       cudaGraph_t g;
@@ -884,11 +970,11 @@ int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
     const int rc = enqueue_host_step(c, s);
     if (rc != SBS_OK) return rc;
   }
-  CK(cudaEventRecord(c->ev1, s));
-  CK(cudaEventRecord(c->blk_ev, s));
+  if (c->profile) CK(cudaEventRecord(c->ev1, s));
+  CK(blk_record(c, s));
   CK(cudaStreamSynchronize(s));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  if (c->profile) cudaEventElapsedTime(&ms, c->ev0, c->ev1);
   int status = SBS_OK;
   for (int r = 0; r < R; ++r) {
     c->h_out[r].device_us = ms * 1000.f;
@@ -907,7 +993,7 @@ int sbs_step_device(sbs_ctx* c, const sbs_input* d_in, sbs_output* d_out, void* 
   if (c->ref_dirty) {  // references staged by sbs_set_reference go up first, in stream order
     CK(cudaMemcpyAsync(c->d_xref, c->h_xref, (size_t)c->P.R * c->P.H * 12 * sizeof(float),
                        cudaMemcpyHostToDevice, (cudaStream_t)stream));
-    CK(cudaEventRecord(c->blk_ev, (cudaStream_t)stream));
+    CK(blk_record(c, (cudaStream_t)stream));
     c->ref_dirty = false;
   }
   c->P.in = d_in;
@@ -990,7 +1076,7 @@ int sbs_step_records(sbs_ctx* c, const sbs_input* d_in, float* d_rec, void* stre
   if (c->ref_dirty) {
     CK(cudaMemcpyAsync(c->d_xref, c->h_xref, (size_t)c->P.R * c->P.H * 12 * sizeof(float),
                        cudaMemcpyHostToDevice, (cudaStream_t)stream));
-    CK(cudaEventRecord(c->blk_ev, (cudaStream_t)stream));
+    CK(blk_record(c, (cudaStream_t)stream));
     c->ref_dirty = false;
   }
   c->P.in = d_in;
@@ -1036,7 +1122,7 @@ int check_loop_config(sbs_ctx* c, const sbs_loop_config* lc) {
 int upload_dirty_reference(sbs_ctx* c, cudaStream_t s) {
   if (c->ref_dirty) {  // references staged by sbs_set_reference go up first, in stream order
     CK(cudaMemcpyAsync(c->d_xref, c->h_xref, (size_t)c->P.R * c->P.H * 12 * sizeof(float), cudaMemcpyHostToDevice, s));
-    CK(cudaEventRecord(c->blk_ev, s));
+    CK(blk_record(c, s));
     c->ref_dirty = false;
   }
   return SBS_OK;
@@ -1077,11 +1163,11 @@ int sbs_run_loop(sbs_ctx* c, int32_t n_iter, sbs_input* d_in, sbs_output* d_out,
     CK(cudaMallocHost(&c->h_loopw, 2 * sizeof(uint32_t)));
   }
   // device iteration counter := iter (the step kernels read it; the advance kernel moves it)
-  CK(cudaEventSynchronize(c->blk_ev));  // h_loopw's previous upload has completed
+  CK(blk_wait(c));  // h_loopw's previous upload has completed
   c->h_loopw[0] = c->iter;
   c->h_loopw[1] = c->iter;
   CK(cudaMemcpyAsync(c->d_loopw, c->h_loopw, 2 * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-  CK(cudaEventRecord(c->blk_ev, s));
+  CK(blk_record(c, s));
   sbs::LoopArgs a = loop_args(lc, d_cmd, d_wrench, d_fallen, d_trace);
   a.loop = c->d_loopw;
   a.counter = reinterpret_cast<int*>(c->d_loopw + 2);

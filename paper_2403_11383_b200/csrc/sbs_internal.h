@@ -87,6 +87,8 @@ struct Params {
   const float* xref;          // [R][H][12]
   const sbs_input* in;        // [R]
   sbs_output* out;            // [R]
+  uint32_t* done;             // host path, one robot: mapped flag the finishing CTA sets to done_value after the outputs
+  uint32_t done_value;
   float* J;                   // [R][K_local]
   float* part;                // [R][n_cta][part_stride]
   int64_t* elite;             // [R][n_elite]

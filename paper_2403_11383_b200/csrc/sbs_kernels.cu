@@ -844,6 +844,13 @@ static __device__ void write_output(const Params& p, int r, int status, const fl
     o->device_us = 0.0f;
     p.status[r] = status;
   }
+  if (p.done) {  // host path: the outputs are in host memory before the flag (system-scope fence)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      *(volatile uint32_t*)p.done = p.done_value;
+    }
+  }
 }
 
 // Block-wide argmin over the partial headers of robot r.
