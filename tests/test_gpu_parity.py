@@ -396,6 +396,26 @@ def test_latency_mode_variants_are_bitwise_equal(B, mode, H, monkeypatch):
         assert np.max(np.abs(o_a[key] - o_p[key])) <= 1e-4 * max(float(np.max(np.abs(o_p[key]))), 1.0)
 
 
+def test_host_path_completion_flag(B, monkeypatch):
+    """sbs_step (one robot) waits on the mapped flag its finishing CTA raises; the same
+    steps waited with cudaStreamSynchronize (SBS_POLL=0) give the same outputs, for
+    every mode, and device_us is measured only with profiling on."""
+    for cfg, inputs in (W.config2(K=3000), W.config3("cem", K=3000), W.config3("naive", K=3000)):
+        res = []
+        for poll in ("1", "0"):
+            monkeypatch.setenv("SBS_POLL", poll)
+            c = _ctrl(B, cfg, inputs)
+            outs = [c.step(inputs)[1][0] for _ in range(3)]
+            assert all(o["device_us"] == 0.0 for o in outs)
+            res.append(outs)
+        for oa, ob in zip(*res):
+            for key in ("mean", "var", "u0"):
+                np.testing.assert_array_equal(oa[key], ob[key])
+            assert oa["iter"] == ob["iter"]
+        c.profile(True)
+        assert c.step(inputs)[1][0]["device_us"] > 0.0
+
+
 def test_reference_from_device_memory(B):
     """sbs_set_reference_device (device buffer, stream-ordered) is the same reference as
     sbs_set_reference for both the host path and the device path."""
