@@ -1211,7 +1211,7 @@ static __device__ void publish_to_peers(const Params& p) {
 enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
 
 
-template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false>
+template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false, bool AB = false>
 __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ? 1 : kRolloutMinBlocks)
     sbs_rollout_kernel(const __grid_constant__ Params p) {
   constexpr int D = 12 * P;
@@ -1301,7 +1301,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
       }
       __syncthreads();
     }
-    if (SPLIT && p.ab) {  // warps 4..15 tabulate the stance-leg forces, warps 0..3 integrate
+    if (SPLIT && AB) {  // warps 4..15 tabulate the stance-leg forces, warps 0..3 integrate
       float* tab = reinterpret_cast<float*>(s_fi + TS);
       if (!sampler_thread) {
         produce_forces<P>(p, s, s_th, s_fi, tab);
@@ -2240,7 +2240,12 @@ constexpr size_t rollout_smem() {
 template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false>
 static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
   dim3 grid(p.n_cta, p.R);
-  const size_t smem = SPLIT ? split_smem_bytes(P, EPI == EPI_MPPI, p.H, p.ab != 0) : rollout_smem<P, EPI, FC, SPLIT>();
+  if constexpr (SPLIT) {  // (separate instantiation: its registers are not sized for the one-thread rollout)
+    if (p.ab)
+      return launch_pdl(sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT, true>, grid, dim3(kBlock * kSplitLanes),
+                        split_smem_bytes(P, EPI == EPI_MPPI, p.H, true), 1, s, p);
+  }
+  const size_t smem = SPLIT ? split_smem_bytes(P, EPI == EPI_MPPI, p.H, false) : rollout_smem<P, EPI, FC, SPLIT>();
   return launch_pdl(sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT>, grid, dim3(SPLIT ? kBlock * kSplitLanes : kBlock),
                     smem, 1, s, p);
 }
@@ -2329,6 +2334,18 @@ cudaError_t PEntry<P>::prepare() {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, false, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, true, false, true, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, false, false, true, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, true, false, true, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, false, false, true, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_debug_samples_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
