@@ -40,7 +40,8 @@ __device__ unsigned long long g_sbs_ts[16];
       g_sbs_ts[i] = t_;                                                         \
     }                                                                           \
   } while (0)
-__device__ unsigned long long g_sbs_cta[256][6];  // per CTA: globaltimer x4, clock64 around the rollout
+__device__ unsigned long long g_sbs_cta[256][6];
+__device__ unsigned long long g_sbs_bar[4][8];  // integrator warp x chunk: cycles waiting on the chunk barrier (CTA 0)  // per CTA: globaltimer x4, clock64 around the rollout
 #define SBS_CTS(i)                                                              \
   do {                                                                          \
     if (threadIdx.x == 0 && blockIdx.x < 256 && blockIdx.y == 0) {              \
@@ -672,7 +673,17 @@ static __device__ float rollout_ab(const Params& p, int fi, const RobotSmem& s, 
   bool bad = false;
   int next_chunk = 0;
   for (int j = 0; j < p.H; ++j) {
+#if defined(SBS_TIMING)
+    if (j == ab_chunk(next_chunk)) {
+      const long long t0 = clock64();
+      named_sync(1 + next_chunk, kBlock * (1 + kAbWarpsPerSmsp));
+      if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x & 31) == 0 && next_chunk < 8)
+        g_sbs_bar[threadIdx.x >> 5][next_chunk] = (unsigned long long)(clock64() - t0);
+      ++next_chunk;
+    }
+#else
     if (j == ab_chunk(next_chunk)) named_sync(1 + next_chunk++, kBlock * (1 + kAbWarpsPerSmsp));
+#endif
     const StepForces sf = load_forces(tab, j, col);
     const float2 F = sf.F;
     const float Fz = sf.Fz, Mx = sf.Mx, My = sf.My, Mz = sf.Mz;
@@ -2365,6 +2376,9 @@ template struct PEntry<SBS_TU_P>;
 #define SBS_CAT(a, b) SBS_CAT2(a, b)
 extern "C" int SBS_CAT(sbs_debug_ts_p, SBS_TU_P)(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_sbs_ts, sizeof(g_sbs_ts));
+}
+extern "C" int SBS_CAT(sbs_debug_bar_p, SBS_TU_P)(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_sbs_bar, sizeof(g_sbs_bar));
 }
 extern "C" int SBS_CAT(sbs_debug_cta_p, SBS_TU_P)(unsigned long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_sbs_cta, sizeof(g_sbs_cta));
