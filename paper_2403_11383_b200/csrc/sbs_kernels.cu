@@ -1172,12 +1172,22 @@ __device__ __forceinline__ bool arrive_last(int* counter, int n) {
   __shared__ int s_last;
   __syncthreads();  // the CTA's record writes happen-before thread 0's fence (fences are cumulative)
   if (threadIdx.x == 0) {
+#if defined(SBS_SC_ARRIVE)
     __threadfence();
     s_last = (atomicAdd(counter, 1) == n - 1);
+#else
+    // release (the CTA's writes, ordered before by the barrier) and acquire (the other
+    // CTAs' records, for this CTA's threads after the next barrier) in one atomic
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(counter) : "memory");
+    s_last = (old == n - 1);
+#endif
   }
   __syncthreads();
   if (s_last) {
+#if defined(SBS_SC_ARRIVE)
     __threadfence();
+#endif
     if (threadIdx.x == 0) *counter = 0;  // re-arm for the next launch (stream-ordered)
   }
   return s_last;
