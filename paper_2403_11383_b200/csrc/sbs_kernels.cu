@@ -855,12 +855,9 @@ static __device__ void write_output(const Params& p, int r, int status, const fl
     o->device_us = 0.0f;
     p.status[r] = status;
   }
-  if (p.done) {  // host path: the outputs are in host memory before the flag (system-scope fence)
+  if (p.done) {  // host path: the outputs are in host memory before the flag (system-scope release)
     __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      *(volatile uint32_t*)p.done = p.done_value;
-    }
+    if (threadIdx.x == 0) asm volatile("st.release.sys.u32 [%0], %1;" ::"l"(p.done), "r"(p.done_value) : "memory");
   }
 }
 
