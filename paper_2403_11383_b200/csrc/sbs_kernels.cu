@@ -772,6 +772,7 @@ __device__ __forceinline__ bool jk_less(float ja, int ka, float jb, int kb) {
 }
 
 __device__ __forceinline__ uint32_t cost_key(float J);
+__device__ __forceinline__ float key_cost(uint32_t key);
 // (J, k) argmin of a warp, the winner's theta1 index: two integer min-reductions
 // (REDUX) over the order-preserving cost key and, among the tied lanes, the index.
 // Same result as a jk_less butterfly (k is unique per sample; only the sentinel
@@ -914,6 +915,7 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   const int nc = p.n_cta;
   const bool one_pass = nc <= 128 && nc * RL <= stage_floats;
   Best b;
+  float bmin = kInf;
   if (one_pass) {
     // one load round trip: every record, this robot's variance, input phase and iteration counter
     if (p.part_c_stride == 1) {
@@ -930,7 +932,14 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
     }
     __syncthreads();
     SBS_TS(7);
-    if (tid < 32) {  // warp 0: argmin over the staged headers, then the per-record scales
+    // every thread: the smallest record minimum (the scales' reference, no barrier); warp 0
+    // also resolves the argmin's (k, theta1) for the outputs
+    {  // per warp: lanes over the records, one integer min-reduction of the order-preserving key
+      uint32_t kmin = 0xffffffffu;
+      for (int c = tid & 31; c < nc; c += 32) kmin = min(kmin, cost_key(stage[c * RL]));
+      bmin = key_cost(__reduce_min_sync(0xffffffffu, kmin));
+    }
+    if (tid < 32) {
       float m = kInf;
       int mk = 0x7fffffff, mf = 0;
       for (int c = tid; c < nc; c += 32) {
@@ -943,23 +952,17 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
         }
       }
       warp_argmin(m, mk, mf);
-      for (int c = tid; c < nc; c += 32) {
-        const float mc = stage[c * RL];
-        s_sc[c] = (mc < kInf) ? __expf((m - mc) * p.inv_lambda) : 0.0f;
-      }
       if (tid == 0) {
         s_bm[0] = m;
         s_bk[0] = mk;
         s_bf[0] = mf;
       }
     }
-    __syncthreads();
-    b = Best{s_bm[0], s_bk[0], s_bf[0]};
   } else {
     b = merge_argmin(p, r);
   }
   SBS_TS(8);
-  const float beta = b.m;
+  const float beta = one_pass ? bmin : b.m;  // (one pass: b is read after the row sums' barrier)
   const int CH = one_pass ? nc : min(128, max(1, stage_floats / RL));
   float acc = 0.f;  // thread tid < NR owns row tid: 0..D-1 V, D S, D+1 S2, D+2 sumJ, D+3 nfin
   for (int c0 = 0; c0 < nc; c0 += CH) {
@@ -972,7 +975,7 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
       }
       __syncthreads();
     }
-    if (one_pass) {  // scales already in s_sc (warp 0); (row, record-chunk) per thread, then chunk sums
+    if (one_pass) {  // (row, record-chunk) per thread, each computing its records' scales, then chunk sums
       const int nch = max(1, min((int)blockDim.x / NR, 16));  // record chunks
       const int per = (n + nch - 1) / nch;
       float* part = s_part;                                    // [nch][NR]
@@ -983,15 +986,19 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
         const int c_end = min(n, (ch + 1) * per);
         float a0 = 0.f, a1 = 0.f;
         int c = ch * per;
+        auto scale = [&](int cc) {
+          const float mc = stage[cc * RL];
+          return (mc < kInf) ? __expf((beta - mc) * p.inv_lambda) : 0.0f;
+        };
         for (; c + 1 < c_end; c += 2) {
-          float s0 = s_sc[c], s1 = s_sc[c + 1];
+          float s0 = scale(c), s1 = scale(c + 1);
           if (kind == 1) { s0 *= s0; s1 *= s1; }
           if (kind == 2) { s0 = 1.f; s1 = 1.f; }
           a0 = fmaf(stage[c * RL + col], s0, a0);
           a1 = fmaf(stage[(c + 1) * RL + col], s1, a1);
         }
         if (c < c_end) {
-          float s0 = kind == 2 ? 1.f : s_sc[c];
+          float s0 = kind == 2 ? 1.f : scale(c);
           if (kind == 1) s0 *= s0;
           a0 = fmaf(stage[c * RL + col], s0, a0);
         }
@@ -1033,20 +1040,21 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   }
   if (!one_pass && tid < NR) s_row[0][tid] = acc;
   __syncthreads();
+  if (one_pass) b = Best{s_bm[0], s_bk[0], s_bf[0]};  // (warp 0's argmin, ordered by the barriers above)
   SBS_TS(9);
   if (EMIT) {  // this rank's merged record, relative to its own beta
     float* o = emit + (size_t)r * p.part_stride;
     if (tid < D) o[kPartHdr + tid] = s_row[0][tid];
     else if (tid < NR) o[3 + tid - D] = s_row[0][tid];
     if (tid == 0) {
-      o[0] = beta;
+      o[0] = b.m;
       o[1] = __int_as_float(b.k);
       o[2] = __int_as_float(b.f);
       o[7] = 0.0f;
     }
     return;
   }
-  const bool all_div = !(beta < kInf);
+  const bool all_div = !(b.m < kInf);
   const float S = s_row[0][D], S2 = s_row[0][D + 1], sumJ = s_row[0][D + 2], nfin = s_row[0][D + 3];
   float* mean = p.mean + (size_t)r * D;
   const float* var = p.var + (size_t)r * D;
@@ -1059,7 +1067,7 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   for (int d = tid; d < D; d += blockDim.x) mean[d] = s_mean[d];
   if (tid == 0) p.fidx[r] = fi;
   SBS_TS(10);
-  write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, beta,
+  write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, b.m,
                nfin > 0.f ? sumJ / nfin : kInf, S, all_div ? 0.f : S * S / S2, (int)((float)p.K_global - nfin),
                one_pass ? s_pre : nullptr);
 }
