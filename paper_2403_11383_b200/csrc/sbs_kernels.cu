@@ -160,6 +160,11 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
                "l"(__cvta_generic_to_global(src))
                : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(__cvta_generic_to_global(src))
+               : "memory");
+}
 static __device__ void load_robot_issue(const Params& p, int r, RobotSmem& s, float* mraw) {
   const int D = p.D;
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
@@ -1075,14 +1080,23 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
 // merges robot r's records (the rollout's CTA records, or the gathered rank
 // records) into d: sdiag layout (J_min, k_best, theta1_best, sum J, n finite),
 // or, with part_layout, a rank record header [m, k, f, 0, 0, sum J, n finite, 0]
-static __device__ void merge_diag(const Params& p, int r, float* d, bool part_layout) {
+// (hdr: the records' 8-float headers already staged in shared memory, or null: read from L2)
+static __device__ void merge_diag(const Params& p, int r, float* d, bool part_layout, const float* hdr = nullptr) {
   if (threadIdx.x >= 32) return;  // one warp, one load round trip; the other warps go on (no block barrier)
   float m = kInf, sj = 0.f, nf = 0.f;
   int mk = 0x7fffffff, mf = 0;
   for (int c = threadIdx.x; c < p.n_cta; c += 32) {
-    const float* pc = part_rec(p, r, c);
-    const float mc = __ldcg(pc), sc = __ldcg(pc + 5), nc = __ldcg(pc + 6);
-    const int kc = __float_as_int(__ldcg(pc + 1)), fc = __float_as_int(__ldcg(pc + 2));
+    float mc, sc, nc;
+    int kc, fc;
+    if (hdr) {
+      const float* pc = hdr + 8 * c;
+      mc = pc[0], sc = pc[5], nc = pc[6];
+      kc = __float_as_int(pc[1]), fc = __float_as_int(pc[2]);
+    } else {
+      const float* pc = part_rec(p, r, c);
+      mc = __ldcg(pc), sc = __ldcg(pc + 5), nc = __ldcg(pc + 6);
+      kc = __float_as_int(__ldcg(pc + 1)), fc = __float_as_int(__ldcg(pc + 2));
+    }
     if (jk_less(mc, kc, m, mk)) {
       m = mc;
       mk = kc;
@@ -1708,6 +1722,7 @@ static __device__ void select_block(const float* J, int64_t K, int64_t K_e, int6
 constexpr int kSelSmallMax = 16384;
 constexpr int kSelKPT = kSelSmallMax / kSelBlock;
 constexpr int kSelSmallSmemBytes = 32768 * 4;
+constexpr int kSelHdrMax = 256;  // rollout records whose headers the select kernel stages (world = 1)
 
 // exclusive block scan of v over kSelBlock threads; returns the total in *tot
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_w, uint32_t* tot) {
@@ -1851,7 +1866,18 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_cons
   const int64_t Ke = p.n_elite;
   float* hdr = MODE == SEL_EMIT ? emit + (size_t)r * p.ex_stride : p.sdiag + (size_t)r * 8;
   if (blockIdx.x == 0) SBS_TS(0);
-  merge_diag(p, r, hdr, MODE == SEL_EMIT);
+  // world = 1: the rollout records' headers arrive by cp.async while the selection runs
+  // (their diagnostics are merged at the end, off the selection's critical path)
+  __shared__ __align__(16) float s_hdr[kSelHdrMax * 8];
+  const bool staged = MODE == SEL_LOCAL && SMALL && p.n_cta <= kSelHdrMax && p.part_c_stride == 1;
+  if (staged) {
+    for (int c = tid; c < p.n_cta; c += blockDim.x) {
+      cp_async16(&s_hdr[8 * c], part_rec(p, r, c));
+      cp_async16(&s_hdr[8 * c + 4], part_rec(p, r, c) + 4);
+    }
+  } else {
+    merge_diag(p, r, hdr, MODE == SEL_EMIT);
+  }
   if (blockIdx.x == 0) SBS_TS(1);
   const float* J = p.J + (size_t)r * p.K_local;
   int64_t K = p.K_local, kb = p.k_begin;
@@ -1868,7 +1894,9 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_kernel(const __grid_cons
   float* eJ = p.elite_J + (size_t)r * Ke;
   if (SMALL) select_block_small(J, (int)K, (int)Ke, kb, el, eJ, sel_smem, true);
   else select_block(J, K, Ke, kb, el, eJ, sel_smem);
+  if (staged) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if (staged) merge_diag(p, r, hdr, false, s_hdr);
   if (blockIdx.x == 0) SBS_TS(6);
 
   if (MODE == SEL_EMIT) {
