@@ -35,11 +35,11 @@ for fl in (False, True):
         b = (C.c_uint64 * 16)(); L.sbs_debug_ts_common(b)
         t0 = a[0]
         row = [(a[4] - t0), (b[0] - t0), (b[6] - t0), (a[11] - t0), (a[12] - t0), e0.elapsed_time(e1) * 1e3] + \
-              [(b[i] - b[0]) for i in range(1, 7)]
+              [(b[i] - b[0]) for i in range(1, 9)]
         if it >= 5:
             acc.append(np.array(row, dtype=np.float64))
     m = np.median(np.array(acc), axis=0)
     m[:5] /= 1e3
     m[6:] /= 1e3
     print(f"{sys.argv[1] if len(sys.argv) > 1 else ''} {'flushed' if fl else 'warm'}: rollout CTA0 start 0 | CTA0 record {m[0]:.2f} | "
-          f"select released {m[1]:.2f} end {m[2]:.2f} (merge {m[6]:.2f} keys {m[7]:.2f} pass1 {m[8]:.2f} pass2 {m[9]:.2f} scans {m[10]:.2f}) | elite released {m[3]:.2f} end {m[4]:.2f} | events {m[5]:.2f} us")
+          f"select released {m[1]:.2f} end {m[2]:.2f} (merge {m[6]:.2f} keys {m[7]:.2f} pass1 {m[8]:.2f} pass2 {m[9]:.2f} scans {m[10]:.2f} writes {m[12]:.2f} synced {m[13]:.2f} end {m[11]:.2f}) | elite released {m[3]:.2f} end {m[4]:.2f} | events {m[5]:.2f} us")
