@@ -1766,11 +1766,13 @@ static __device__ void digit16_pass(const uint32_t (&key)[kSelKPT], int nk, uint
   if (!zeroed) zero_hist16(hist);
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < kSelKPT; ++i)
-    if (i < nk && (key[i] & pmask) == pref) {
+  for (int i = 0; i < kSelKPT; ++i) {
+    if (i >= nk) break;
+    if ((key[i] & pmask) == pref) {
       const uint32_t d = (key[i] >> sh) & 0xFFFFu;
       atomicAdd(&hist[d >> 1], 1u << ((d & 1u) << 4));
     }
+  }
   __syncthreads();
   // thread t owns digits [64 t, 64 t + 64)
   uint32_t loc = 0;
@@ -1780,23 +1782,27 @@ static __device__ void digit16_pass(const uint32_t (&key)[kSelKPT], int nk, uint
   }
   uint32_t tot;
   const uint32_t base = block_excl_scan(loc, s_w, &tot);
-  if (base < want && want <= base + loc) {
-    uint32_t cum = base;
-    for (int w = 0; w < 32; ++w) {
-      const uint32_t h = hist[tid * 32 + w];
-      const uint32_t c0 = h & 0xFFFFu, c1 = h >> 16;
-      if (cum + c0 >= want) {
-        s_res[0] = (uint32_t)(tid * 64 + 2 * w);
-        s_res[1] = cum;
-        break;
-      }
-      cum += c0;
-      if (cum + c1 >= want) {
-        s_res[0] = (uint32_t)(tid * 64 + 2 * w + 1);
-        s_res[1] = cum;
-        break;
-      }
-      cum += c1;
+  // the warp holding the digit range that contains rank `want` resolves the digit: its
+  // lanes take one word (two digits) each of the owner's range, then a warp scan
+  const uint32_t owner = __ballot_sync(0xffffffffu, base < want && want <= base + loc);
+  if (owner) {
+    const int ol = __ffs(owner) - 1, lane = tid & 31;
+    const int t = (tid & ~31) + ol;
+    const uint32_t obase = __shfl_sync(0xffffffffu, base, ol);
+    const uint32_t h = hist[t * 32 + lane];
+    const uint32_t c0 = h & 0xFFFFu, c1 = h >> 16;
+    uint32_t incl = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const uint32_t cum = obase + incl - (c0 + c1);  // count below this word's first digit
+    const bool hit0 = cum + c0 >= want, hit1 = cum + c0 + c1 >= want;
+    const uint32_t first = __ballot_sync(0xffffffffu, hit1);
+    if (lane == __ffs(first) - 1) {
+      s_res[0] = (uint32_t)(t * 64 + 2 * lane + (hit0 ? 0 : 1));
+      s_res[1] = hit0 ? cum : cum + c0;
     }
   }
   __syncthreads();
@@ -1823,11 +1829,11 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
   const uint32_t n_eq = (uint32_t)K_e - below_hi - s_res[1];  // ties at T to take, lowest indices first
   uint32_t lt = 0, eq = 0;
 #pragma unroll
-  for (int i = 0; i < kSelKPT; ++i)
-    if (i < nk) {
-      lt += key[i] < T;
-      eq += key[i] == T;
-    }
+  for (int i = 0; i < kSelKPT; ++i) {
+    if (i >= nk) break;
+    lt += key[i] < T;
+    eq += key[i] == T;
+  }
   uint32_t t1, t2;
   const uint32_t lt_before = block_excl_scan(lt, s_w, &t1);
   uint32_t eq_before = block_excl_scan(eq, s_w, &t2);
@@ -1839,20 +1845,23 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
   int64_t* s_el = reinterpret_cast<int64_t*>(hist);
   float* s_eJ = reinterpret_cast<float*>(s_el + K_e);
 #pragma unroll
-  for (int i = 0; i < kSelKPT; ++i)
-    if (i < nk) {
-      const bool take = key[i] < T || (key[i] == T && eq_before++ < n_eq);
-      if (take) {
-        const float Jv = key_cost(key[i]);  // (J itself up to NaN -> +inf, -0 -> +0)
-        if (stage) {
-          s_eJ[pos] = Jv;
-          s_el[pos++] = k_begin + k0 + i;
-        } else {
-          if (eJ) eJ[pos] = Jv;
-          elite[pos++] = k_begin + k0 + i;
-        }
+  for (int i = 0; i < kSelKPT; ++i) {
+    if (i >= nk) break;
+    const bool is_eq = key[i] == T;
+    const bool take = key[i] < T || (is_eq && eq_before < n_eq);  // ties: lowest indices first
+    eq_before += is_eq ? 1u : 0u;
+    if (take) {
+      const float Jv = key_cost(key[i]);  // (J itself up to NaN -> +inf, -0 -> +0)
+      if (stage) {
+        s_eJ[pos] = Jv;
+        s_el[pos] = k_begin + k0 + i;
+      } else {
+        if (eJ) eJ[pos] = Jv;
+        elite[pos] = k_begin + k0 + i;
       }
     }
+    pos += take ? 1u : 0u;
+  }
   if (stage) {
     __syncthreads();
     for (int e = tid; e < K_e; e += blockDim.x) {
