@@ -1834,9 +1834,10 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
     lt += key[i] < T;
     eq += key[i] == T;
   }
-  uint32_t t1, t2;
-  const uint32_t lt_before = block_excl_scan(lt, s_w, &t1);
-  uint32_t eq_before = block_excl_scan(eq, s_w, &t2);
+  uint32_t t1;  // one scan of both counts, packed (each total <= K <= 16384 < 2^16)
+  const uint32_t both = block_excl_scan(lt | (eq << 16), s_w, &t1);
+  const uint32_t lt_before = both & 0xFFFFu;
+  uint32_t eq_before = both >> 16;
   uint32_t pos = lt_before + min(eq_before, n_eq);
   if (blockIdx.x == 0) SBS_TS(5);
   // the compacted list goes through shared memory (the histogram is free now) so that
