@@ -254,10 +254,14 @@ def test_config3_elites(B, orc, mode):
 
 def test_select_same_J_bitwise(B, orc):
     rng = np.random.default_rng(21)
-    for K, Ke in [(1, 1), (64, 1), (64, 64), (1000, 100), (10000, 1000), (50000, 3), (70001, 7000)]:
-        for kind in ("ties", "uniform"):
+    # (16384, 12000): the compacted list exceeds the shared-memory staging (direct writes)
+    for K, Ke in [(1, 1), (64, 1), (64, 64), (1000, 100), (10000, 1000), (16384, 10000), (16384, 12000),
+                  (12000, 11999), (50000, 3), (70001, 7000)]:
+        for kind in ("ties", "uniform", "signed"):
             if kind == "ties":
                 J = rng.integers(0, 25, K).astype(np.float32)
+            elif kind == "signed":
+                J = rng.normal(0.0, 5.0, K).astype(np.float32)
             else:
                 J = rng.uniform(0, 10, K).astype(np.float32)
             J[rng.integers(0, K, max(1, K // 50))] = np.inf
