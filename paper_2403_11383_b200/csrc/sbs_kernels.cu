@@ -918,33 +918,15 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   __shared__ int s_bk[32], s_bf[32];
   __shared__ float s_part[16 * (SBS_MAX_D + 4)];
   const int nc = p.n_cta;
-  const int RS = RL | 1;  // one pass: records staged at an odd stride (lanes over records: no bank conflicts)
-  const bool one_pass = nc <= 128 && nc * RS <= stage_floats;
+  const bool one_pass = nc <= 128 && nc * RL <= stage_floats;
   Best b;
   float bmin = kInf;
   if (one_pass) {
     // one load round trip: every record, this robot's variance, input phase and iteration counter
-    {
-      const int q4 = RL >> 2;  // float4 per record (RL % 4 == 0)
-      for (int i0 = tid; i0 < nc * q4; i0 += 4 * blockDim.x) {
-        float4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + u * blockDim.x;
-          if (i < nc * q4) v[u] = __ldcg(reinterpret_cast<const float4*>(part_rec(p, r, i / q4)) + i % q4);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + u * blockDim.x;
-          if (i < nc * q4) {
-            float* d = stage + (i / q4) * RS + 4 * (i % q4);
-            d[0] = v[u].x;
-            d[1] = v[u].y;
-            d[2] = v[u].z;
-            d[3] = v[u].w;
-          }
-        }
-      }
+    if (p.part_c_stride == 1) {
+      stage_copy(stage, part_rec(p, r, 0), nc * RL);  // records of a robot are contiguous
+    } else {
+      for (int c = 0; c < nc; ++c) stage_copy(stage + c * RL, part_rec(p, r, c), RL);
     }
     if (!EMIT) {
       for (int d = tid; d < D; d += blockDim.x) s_var[d] = p.var[(size_t)r * D + d];
@@ -959,14 +941,14 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
     // also resolves the argmin's (k, theta1) for the outputs
     {  // per warp: lanes over the records, one integer min-reduction of the order-preserving key
       uint32_t kmin = 0xffffffffu;
-      for (int c = tid & 31; c < nc; c += 32) kmin = min(kmin, cost_key(stage[c * RS]));
+      for (int c = tid & 31; c < nc; c += 32) kmin = min(kmin, cost_key(stage[c * RL]));
       bmin = key_cost(__reduce_min_sync(0xffffffffu, kmin));
     }
     if (tid < 32) {
       float m = kInf;
       int mk = 0x7fffffff, mf = 0;
       for (int c = tid; c < nc; c += 32) {
-        const float* h = stage + c * RS;
+        const float* h = stage + c * RL;
         const int kc = __float_as_int(h[1]);
         if (jk_less(h[0], kc, m, mk)) {
           m = h[0];
@@ -998,27 +980,40 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
       }
       __syncthreads();
     }
-    if (one_pass) {  // warp per row: lanes over the records (scales computed once per lane), butterfly sums
-      const int lane = tid & 31, nw = (int)blockDim.x >> 5;
-      float sc[4];  // nc <= 128: records lane, lane + 32, lane + 64, lane + 96
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = lane + 32 * u;
-        const float mc = c < n ? stage[c * RS] : kInf;
-        sc[u] = (mc < kInf) ? __expf((beta - mc) * p.inv_lambda) : 0.0f;
-      }
-      for (int row = tid >> 5; row < NR; row += nw) {
+    if (one_pass) {  // (row, record-chunk) per thread, each computing its records' scales, then chunk sums
+      const int nch = max(1, min((int)blockDim.x / NR, 16));  // record chunks
+      const int per = (n + nch - 1) / nch;
+      float* part = s_part;                                    // [nch][NR]
+      if (tid < nch * NR) {
+        const int row = tid % NR, ch = tid / NR;
         const int col = row < D ? kPartHdr + row : 3 + (row - D);
         const int kind = row < D + 1 ? 0 : (row == D + 1 ? 1 : 2);
-        float a = 0.f;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int c = lane + 32 * u;
-          if (c < n) a = fmaf(stage[c * RS + col], kind == 0 ? sc[u] : (kind == 1 ? sc[u] * sc[u] : 1.0f), a);
+        const int c_end = min(n, (ch + 1) * per);
+        float a0 = 0.f, a1 = 0.f;
+        int c = ch * per;
+        auto scale = [&](int cc) {
+          const float mc = stage[cc * RL];
+          return (mc < kInf) ? __expf((beta - mc) * p.inv_lambda) : 0.0f;
+        };
+        for (; c + 1 < c_end; c += 2) {
+          float s0 = scale(c), s1 = scale(c + 1);
+          if (kind == 1) { s0 *= s0; s1 *= s1; }
+          if (kind == 2) { s0 = 1.f; s1 = 1.f; }
+          a0 = fmaf(stage[c * RL + col], s0, a0);
+          a1 = fmaf(stage[(c + 1) * RL + col], s1, a1);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if (lane == 0) s_row[0][row] = a;
+        if (c < c_end) {
+          float s0 = kind == 2 ? 1.f : scale(c);
+          if (kind == 1) s0 *= s0;
+          a0 = fmaf(stage[c * RL + col], s0, a0);
+        }
+        part[ch * NR + row] = a0 + a1;
+      }
+      __syncthreads();
+      if (tid < NR) {
+        float a = 0.f;
+        for (int ch = 0; ch < nch; ++ch) a += part[ch * NR + tid];
+        s_row[0][tid] = a;
       }
       break;  // single chunk
     }
