@@ -250,8 +250,7 @@ __device__ __forceinline__ void split_noise(const Params& p, uint32_t robot_g, i
     const int q = u + kSplitLanes * i;
     if (q < 3 * P) {
       const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k, iter, robot_g, p.rk);
-      box_muller(w.x, w.y, n.z[i][0], n.z[i][1]);
-      box_muller(w.z, w.w, n.z[i][2], n.z[i][3]);
+      box_muller_x2(w, n.z[i]);
     }
   }
   n.fi = -1;
@@ -300,8 +299,7 @@ __device__ __forceinline__ int draw_sample(const Params& p, uint32_t robot_g, in
   for (int q = 0; q < D / 4; ++q) {
     const U4 w = philox4x32_10_rk((uint32_t)q, kk, s.iter, robot_g, p.rk);
     float z[4];
-    box_muller(w.x, w.y, z[0], z[1]);
-    box_muller(w.z, w.w, z[2], z[3]);
+    box_muller_x2(w, z);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float sg = grp ? __fmul_rn(s.sig[4 * q + i], sc) : s.sig[4 * q + i];
@@ -328,8 +326,7 @@ __device__ __forceinline__ void sample_block(const Params& p, uint32_t robot_g, 
   }
   const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k, s.iter, robot_g, p.rk);
   float z[4];
-  box_muller(w.x, w.y, z[0], z[1]);
-  box_muller(w.z, w.w, z[2], z[3]);
+  box_muller_x2(w, z);
   const bool grp = p.n_sig_groups > 1;
   const float sc = grp ? p.sig_scale[(int)(k % p.n_sig_groups)] : 1.0f;
 #pragma unroll
@@ -359,8 +356,7 @@ __device__ __forceinline__ int draw_sample_fc(const Params& p, uint32_t robot_g,
   for (int q = 0; q < D / 4; ++q) {
     const U4 w = philox4x32_10_rk((uint32_t)q, kk, s.iter, robot_g, p.rk);
     float z[4];
-    box_muller(w.x, w.y, z[0], z[1]);
-    box_muller(w.z, w.w, z[2], z[3]);
+    box_muller_x2(w, z);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int j = 4 * q + u;
@@ -397,8 +393,7 @@ __device__ __forceinline__ void noise_block(const Params& p, uint32_t robot_g, i
     return;
   }
   const U4 w = philox4x32_10_rk((uint32_t)q, (uint32_t)k, s.iter, robot_g, p.rk);
-  box_muller(w.x, w.y, z[0], z[1]);
-  box_muller(w.z, w.w, z[2], z[3]);
+  box_muller_x2(w, z);
 }
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
