@@ -1473,7 +1473,11 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
     } else {
       if (valid) {
 #pragma unroll
-        for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = w * theta_get(th, d);
+        for (int d = 0; d < D; d += 2) {  // w theta, two coordinates per packed multiply
+          const float2 v = __fmul2_rn(make_float2(w, w), make_float2(theta_get(th, d), theta_get(th, d + 1)));
+          s_red[d * (kBlock + 1) + tid] = v.x;
+          s_red[(d + 1) * (kBlock + 1) + tid] = v.y;
+        }
       } else {
 #pragma unroll
         for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = 0.0f;
