@@ -63,10 +63,12 @@ def full(rep, out, K, H):
             cyc = t * g["sm__cycles_elapsed.avg.per_second"] * (1e9 if u[h.index("sm__cycles_elapsed.avg.per_second")] == "Ghz" else 1e6)
             rate = (2 * g[KEYS[-3]] + g[KEYS[-2]] + g[KEYS[-1]])
             flop = rate * cyc
+            scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            dram = sum(g[k] * scale.get(u[h.index(k)], 1.0) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
             f.write(f"\nDerived (scalar FFMA/FMUL/FADD counters only; packed FFMA2/FADD2/FMUL2 are not counted): FP32 FLOP = {flop:.4e}; per sample-step = {flop/(K*H):.1f}; "
                     f"instructions per sample = {g['inst_executed']*32/K:.0f}; "
                     f"FP32 FLOP/cycle/SM = {rate/148:.1f} of 256 ({rate/148/256:.1%}); "
-                    f"DRAM bytes per launch = {g['dram__bytes_read.sum'] + g['dram__bytes_write.sum']:.4g}\n\n")
+                    f"DRAM bytes per launch = {dram:.4g}\n\n")
             st = sorted(((k[len(STALLS):].replace('_per_issue_active.ratio', ''), float(row[i] or 0))
                          for i, k in enumerate(h) if k.startswith(STALLS) and k.endswith("per_issue_active.ratio")),
                         key=lambda x: -x[1])
