@@ -155,3 +155,56 @@ def test_divergence_is_infinite(orc):
     x = x0.copy()
     x[10] = 200.0                                # pitch rate drives pitch past pi/2 - 1e-3
     assert orc.rollout(cfg, x, 0, feet, feet, xref, theta, 0) == math.inf
+
+
+@pytest.mark.parametrize("fz", [20.0, M * G / 2, 120.0, 150.0])
+def test_two_leg_trot_thrust_closed_form(orc, fz):
+    """u^r = -m g_z / max(1, n_stance) with n_stance = 2 (L12, "(u - u^r)^T R
+    (u - u^r)"), and swing legs carry neither force nor effort (P:277 delta_i, P:249
+    mask).  Trot (offsets 0, 1/2, 1/2, 0), D_f = 0.5, phi0 = 0, 1.3 Hz, H = 12: the
+    FL/RR phase reaches 12 * 0.026 = 0.312 < 0.5 of a cycle, so FL and RR stay in
+    stance and FR, RL in swing for the whole horizon.  FL and RR hips are mirror
+    images through the CoM, so vertical forces of equal size give zero net torque at
+    any height and the body rises or falls straight with a = 2 f_z / m - g (RK4 is
+    exact for constant acceleration).  With R_z = 1e-3 the effort term is of the
+    same order as the tracking terms, so 'm g / 4 always' or 'count swing legs'
+    changes J by > 1e-3 relative."""
+    cfg = _cfg(duty_factor=0.5, phase_offset=[0.0, 0.5, 0.5, 0.0], R=[1e-3] * 12)
+    H, P, dt = cfg["horizon"], cfg["knots"], cfg["dt"]
+    assert H == 12
+    d = orc.contact_sequence(cfg, 0, 1.3).reshape(H, 4)
+    np.testing.assert_array_equal(d, np.tile([1, 0, 0, 1], (H, 1)))
+    x0, feet, xref = _hover_inputs(H)
+    theta = np.tile([0, 0, fz], 4 * P)
+    J = orc.rollout(cfg, x0, 0, feet, feet, xref, theta, 0)
+    a = 2 * fz / M - G
+    Qz, Qvz, Rz = cfg["Q"][2], cfg["Q"][5], cfg["R"][2]
+    want = sum(Qz * (0.5 * a * (j * dt) ** 2) ** 2 + Qvz * (a * j * dt) ** 2 + 2 * Rz * (fz - M * G / 2) ** 2
+               for j in range(H))
+    assert J == pytest.approx(want, rel=1e-10, abs=1e-14)
+    wrong_mg4 = sum(Qz * (0.5 * a * (j * dt) ** 2) ** 2 + Qvz * (a * j * dt) ** 2 + 2 * Rz * (fz - M * G / 4) ** 2
+                    for j in range(H))
+    assert abs(wrong_mg4 - want) > 1e-3 * want    # the pin separates the readings
+
+
+@pytest.mark.parametrize("fz_raw,fz_clamped", [(200.0, 180.0), (260.0, 180.0), (0.0, 5.0), (-40.0, 5.0)])
+def test_cone_penalty_enters_cost(orc, fz_raw, fz_clamped):
+    """L9 / P:294: the stance force is the cone projection of the raw spline output
+    (f_z clamped to [fz_min, fz_max]) and J gains w_fc * (squared violation of the raw
+    output) per stance leg and step.  D_f = 1, f_z knots outside the bounds, no
+    horizontal force: the motion is the vertical-thrust closed form at the clamped
+    force, and the penalty adds w_fc * H * 4 * (f_z - bound)^2."""
+    cfg = _cfg(w_fc=1e-3)
+    H, P, dt = cfg["horizon"], cfg["knots"], cfg["dt"]
+    x0, feet, xref = _hover_inputs(H)
+    theta = np.tile([0, 0, fz_raw], 4 * P)
+    J = orc.rollout(cfg, x0, 0, feet, feet, xref, theta, 0)
+    a = 4 * fz_clamped / M - G
+    Qz, Qvz, Rz = cfg["Q"][2], cfg["Q"][5], cfg["R"][2]
+    thrust = sum(Qz * (0.5 * a * (j * dt) ** 2) ** 2 + Qvz * (a * j * dt) ** 2
+                 + 4 * Rz * (fz_clamped - M * G / 4) ** 2 for j in range(H))
+    pen = cfg["w_fc"] * H * 4 * (fz_raw - fz_clamped) ** 2
+    assert J == pytest.approx(thrust + pen, rel=1e-10)
+    # the penalty weight enters linearly: w_fc = 0 leaves the thrust closed form
+    J0 = orc.rollout(_cfg(w_fc=0.0), x0, 0, feet, feet, xref, theta, 0)
+    assert J0 == pytest.approx(thrust, rel=1e-10)

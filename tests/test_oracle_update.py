@@ -100,3 +100,25 @@ def test_cem_moments(orc):
     rc, mu, var, e, dg = orc.cem_update(J, th, K, np.zeros(D), 1, np.ones(D))
     np.testing.assert_allclose(mu, th.mean(0), atol=1e-12)
     np.testing.assert_allclose(var, th.var(0), atol=1e-12)
+
+
+@pytest.mark.parametrize("K,Ke,n_inf", [(50, 20, 40), (64, 64, 10), (200, 30, 185), (10, 10, 9)])
+def test_cem_fewer_finite_than_elites(orc, K, Ke, n_inf):
+    """Alg. 1 refits on the elite set; L17: a diverged rollout (J = +inf,
+    L26) never enters the moments.  With fewer finite costs than K_e the elite list
+    still holds K_e indices in (J, k) order (+inf last), and mean / variance are the
+    population moments of the finite samples only (numpy on that subset)."""
+    rng = np.random.default_rng(K * 7 + n_inf)
+    D = 9
+    J = rng.uniform(0, 5, K)
+    J[rng.permutation(K)[:n_inf]] = math.inf
+    th = rng.normal(size=(K, D)) * 3 + 1
+    floor = np.full(D, 1e-3)
+    rc, mu, var, e, dg = orc.cem_update(J, th, Ke, floor, 1, np.ones(D))
+    fin = np.flatnonzero(np.isfinite(J))
+    assert rc == 0 and dg.n_diverged == n_inf
+    np.testing.assert_array_equal(e, np.argsort(J, kind="stable")[:Ke])
+    sel = fin[np.argsort(J[fin], kind="stable")][:Ke]
+    np.testing.assert_allclose(mu, th[sel].mean(0), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(var, np.maximum(th[sel].var(0), floor), rtol=0, atol=1e-12)
+    assert dg.omega == len(sel)
