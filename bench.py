@@ -34,10 +34,13 @@ sys.path.insert(0, ROOT)
 
 K_PER_GPU = 10000
 H = 12
-# Algorithmic FP32 FLOPs per sample-step of the rollout kernel:
-# FP32 adds/muls/FMAs (FMA = 2) of the round-1 kernel formulation, counted by ncu
-# (sm__sass_thread_inst_executed_op_{fadd,fmul,ffma}_pred_on) at config 2, frozen.
-ALG_FLOP_PER_SAMPLE_STEP = 794.0
+# Algorithmic FLOPs per sample-step, frozen from the oracle's
+# op-counting mode over the config-2 workload (scripts/op_count.py, 256 samples;
+# tests/test_oracle_opcount.py re-derives them): the rollout + cost (a2-a4) alone,
+# and the whole fused kernel (+ sampling a1: binary32 Box-Muller and theta2, + MPPI a5).
+ALG_FLOP_ROLLOUT = 9343.0 / 12.0          # 778.58
+ALG_FLOP_FUSED = 886.1419270833334        # rollout 778.58 + sampling 95.16 + MPPI 12.40
+ALG_FLOP_PER_SAMPLE_STEP = ALG_FLOP_FUSED
 # per-kernel CUDA events (for the roofline's kernel time) bracket every PROFILE_EVERY-th
 # timed step, so their own cost stays out of the headline per-iteration time
 PROFILE_EVERY = 10

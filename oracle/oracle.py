@@ -16,6 +16,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sbs_oracle.c")
 _HDR = os.path.join(_HERE, "sbs_oracle.h")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_CNT_SRC = os.path.join(_HERE, "opcount.cpp")
+_CNT_LIB = os.path.join(_HERE, "libopcount.so")
 
 MAX_KNOTS = 8
 MAX_D = 12 * MAX_KNOTS
@@ -32,6 +34,13 @@ def build_oracle(force: bool = False) -> str:
         subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math",
                                "-Wall", "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
+    stale = force or not os.path.exists(_CNT_LIB) or max(
+        os.path.getmtime(_SRC), os.path.getmtime(_HDR), os.path.getmtime(_CNT_SRC)) > os.path.getmtime(_CNT_LIB)
+    if stale:  # op-counting mode (opcount.cpp): the same source with counting scalars
+        tmp = _CNT_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", "-O1", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-Wall",
+                               "-Wno-class-memaccess", "-fPIC", "-shared", "-o", tmp, _CNT_SRC])
+        os.replace(tmp, _CNT_LIB)
     return _LIB
 
 
@@ -304,6 +313,57 @@ class Oracle:
                                  _dp(_f64(xref, H * 12)), _dp(_f64(theta, 12 * cfg["knots"])),
                                  int(fidx), _dp(tr) if traj else None)
         return (J, tr) if traj else J
+
+    def _count_lib(self):
+        if not hasattr(self, "_cnt"):
+            self._cnt = C.CDLL(_CNT_LIB)
+            self._cnt.orc_count_rollout.argtypes = [
+                C.POINTER(OrcConfig), C.POINTER(C.c_double), C.c_uint32, C.POINTER(C.c_double),
+                C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32,
+                C.POINTER(C.c_uint64)]
+            self._cnt.orc_count_rollout.restype = C.c_double
+            self._cnt.orc_count_sample.argtypes = [
+                C.POINTER(OrcConfig), C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32, C.c_uint32,
+                C.c_uint32, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+            self._cnt.orc_count_mppi.argtypes = [C.c_int64, C.c_int32, C.POINTER(C.c_double),
+                                                 C.POINTER(C.c_double), C.c_double, C.POINTER(C.c_double),
+                                                 C.POINTER(C.c_uint64)]
+            self._cnt.orc_count_mppi.restype = C.c_int
+        return self._cnt
+
+    def count_rollout(self, cfg, x0, phase0, feet_cur, feet_next, xref, theta, fidx):
+        """Op-counting mode (opcount.cpp): (J, FLOPs, transcendentals, compares) of one
+        orc_rollout call, counted on the sample-dependent values."""
+        L = self._count_lib()
+        c = make_config(cfg)
+        H = cfg["horizon"]
+        n = (C.c_uint64 * 3)()
+        J = L.orc_count_rollout(C.byref(c), _dp(_f64(x0, 12)), int(phase0) & 0xFFFFFFFF,
+                                        _dp(_f64(feet_cur, 12)), _dp(_f64(feet_next, 12)),
+                                        _dp(_f64(xref, H * 12)), _dp(_f64(theta, 12 * cfg["knots"])),
+                                        int(fidx), n)
+        return J, int(n[0]), int(n[1]), int(n[2])
+
+    def count_sample(self, cfg, mu_shift, var, cur_idx, it, robot, k):
+        """Op-counting mode of orc_sample: (theta2, FLOPs, transcendentals, compares)."""
+        L = self._count_lib()
+        c = make_config(cfg)
+        th = np.zeros(12 * cfg["knots"])
+        n = (C.c_uint64 * 3)()
+        L.orc_count_sample(C.byref(c), _dp(_f64(mu_shift)), _dp(_f64(var)), int(cur_idx), int(it) & 0xFFFFFFFF,
+                           int(robot), int(k), _dp(th), n)
+        return th, int(n[0]), int(n[1]), int(n[2])
+
+    def count_mppi(self, J, theta, lam):
+        """Op-counting mode of orc_mppi: (mu_new, FLOPs, transcendentals, compares)."""
+        L = self._count_lib()
+        J = _f64(J)
+        th = _f64(theta)
+        D = th.shape[1]
+        mu = np.zeros(D)
+        n = (C.c_uint64 * 3)()
+        L.orc_count_mppi(len(J), D, _dp(J), _dp(th), float(lam), _dp(mu), n)
+        return mu, int(n[0]), int(n[1]), int(n[2])
 
     # ---- updates ---------------------------------------------------------
     def mppi(self, J, theta, lam):

@@ -256,8 +256,10 @@ void orc_spline_step(const orc_config* c, const double* theta, int32_t j, double
  * constraints"; L9): clamp f_z to [fz_min, fz_max], then |f_x|,|f_y| to
  * mu f_z (inner pyramid); pen = squared violation of the raw output.
  * ==================================================================== */
-static double clampd(double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); }
-static double pos(double x) { return x > 0.0 ? x : 0.0; }
+/* written with fmin/fmax (same values as the comparison forms for every non-NaN x) so
+ * that the op-counting mode (opcount.cpp) sees a clamped result as sample-dependent */
+static double clampd(double x, double lo, double hi) { return fmin(fmax(x, lo), hi); }
+static double pos(double x) { return fmax(x, 0.0); }
 
 void orc_cone(const orc_config* c, const double raw[3], double out[3], double* pen) {
   double fz = clampd(raw[2], c->fz_min, c->fz_max);

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsbs.so")
 SOURCES = ["sbs_kernels.cu", "sbs_loop.cu", "sbs_api.cpp"]
-HEADERS = ["sbs_internal.h", "sbs_noise.cuh"]
+HEADERS = ["sbs_internal.h", "sbs_noise.cuh", "sbs_robot_model.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-diag-suppress", "177,550", "-Xcompiler", "-fPIC,-O2,-Wall", "-cudart", "static",

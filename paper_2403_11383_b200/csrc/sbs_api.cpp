@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "sbs_internal.h"
+#include "sbs_robot_model.h"
 
 using sbs::Params;
 
@@ -188,6 +189,22 @@ int cuda_fail(sbs_ctx* c, cudaError_t e, const char* where) {
     cudaError_t e_ = (call);                              \
     if (e_ != cudaSuccess) return cuda_fail(c, e_, #call); \
   } while (0)
+
+// the context's model / cost constants equal the compiled-in robot model bit for bit
+// (then the rollout may take them as immediate operands: sbs_robot_model.h)
+bool same_bits(float a, float b) { return memcmp(&a, &b, sizeof a) == 0; }
+bool model_matches(const sbs::Params& P) {
+  namespace m = sbs::model;
+  if (P.P != m::kKnots || !P.diag_inertia || P.full_cov) return false;
+  bool ok = same_bits(P.dt, m::kDt) && same_bits(P.inv_mass, m::kInvMass) && same_bits(P.g[0], 0.0f) &&
+            same_bits(P.g[1], 0.0f) && same_bits(P.g[2], m::kGz) && same_bits(P.mu, m::kMu) &&
+            same_bits(P.fz_min, m::kFzMin) && same_bits(P.fz_max, m::kFzMax) && same_bits(P.w_fc, m::kWfc);
+  ok = ok && same_bits(P.I[0], m::kI0) && same_bits(P.I[4], m::kI1) && same_bits(P.I[8], m::kI2);
+  ok = ok && same_bits(P.Iinv[0], m::kIinv0) && same_bits(P.Iinv[4], m::kIinv1) && same_bits(P.Iinv[8], m::kIinv2);
+  for (int i = 0; i < 12; ++i) ok = ok && same_bits(P.Q[i], m::Q(i)) && same_bits(P.Rw[i], m::kR);
+  for (int n = 0; n <= 4; ++n) ok = ok && same_bits(P.urz[n], m::urz(n));
+  return ok;
+}
 
 bool finite_all(const float* v, int n) {
   for (int i = 0; i < n; ++i)
@@ -564,6 +581,9 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
     P.rk[r][1] = P.seed_hi + (uint32_t)r * 0xBB67AE85u;
   }
   P.robot_offset = cfg->robot_offset;
+  // ---- compiled-in robot model (sbs_robot_model.h): every constant bit-identical ----
+  P.model = model_matches(P) ? 1 : 0;
+  if (const char* e = getenv("SBS_MODEL")) P.model = P.model && atoi(e) != 0;  // experiments / tests: SBS_MODEL=0 disables
   // ---- sharding and launch geometry ----
   P.R = R;
   P.K_global = cfg->n_samples;
@@ -582,7 +602,7 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
     bool ab = split && sbs::split_smem_bytes(Pk, cfg->mode == SBS_MPPI, P.H, true) <= sbs::kSplitSmemMax;
     if (const char* e = getenv("SBS_AB")) ab = ab && atoi(e) != 0;  // experiments: SBS_AB=0 disables
     P.ab = ab ? 1 : 0;
-    const int occ = sbs::rollout_occupancy(Pk, cfg->mode, cfg->full_cov != 0, split);
+    const int occ = sbs::rollout_occupancy(Pk, cfg->mode, cfg->full_cov != 0, split, P.model != 0);
     const int64_t slots = (int64_t)occ * c->sm_count;
     P.n_cta = (int)std::max<int64_t>(1, std::min<int64_t>(P.n_tiles, slots / R));
   }

@@ -60,6 +60,7 @@ struct Params {
   int split;                  // latency mode: kSplitTile samples per tile, sampler split over 4 lanes
   int ab;                     // latency mode: 12 producer warps tabulate the stance-leg forces for the 4 integrator warps
   int full_cov;               // f3 (L42): CEM with a full covariance C = L L^T
+  int model;                  // 1: the constants equal the compiled-in robot model (sbs_robot_model.h)
   float* Lmat;                // [R][D][D] lower Cholesky factor (row-major), full_cov only
   int n_sig_groups;           // multiple Gaussians (L41): sample k uses sig_scale[k mod n_sig_groups]
   float sig_scale[8];
@@ -142,7 +143,7 @@ cudaError_t launch_elite(const Params& p, cudaStream_t s);
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                  int* fidx, cudaStream_t s);
 cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s);
-int rollout_occupancy(int P, int mode, bool fc = false, bool split = false);
+int rollout_occupancy(int P, int mode, bool fc = false, bool split = false, bool model = false);
 // kernel attributes (dynamic shared memory limits), once per process and P, never inside a capture
 cudaError_t prepare_kernels(int P);  // resident CTAs per SM of the rollout kernel
 

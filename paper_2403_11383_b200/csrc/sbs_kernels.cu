@@ -26,8 +26,11 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "sbs_internal.h"
 #include "sbs_noise.cuh"
+#include "sbs_robot_model.h"
 
 namespace sbs {
 #if defined(SBS_TIMING)  // experiments only: phase timestamps (%globaltimer) of CTA 0 / the last CTA
@@ -401,9 +404,61 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return _
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 
+// Model and cost constants of the rollout.  DynC reads them from the parameter
+// block (any robot); ModelC is the compiled-in robot of sbs_robot_model.h, whose
+// values the compiler folds into immediate operands (sbs_create selects it only
+// when the parameter block holds exactly these values).
+struct DynC {
+  static constexpr bool kStatic = false;
+  __device__ static __forceinline__ float dt(const Params& p) { return p.dt; }
+  __device__ static __forceinline__ float inv_mass(const Params& p) { return p.inv_mass; }
+  __device__ static __forceinline__ float g(const Params& p, int i) { return p.g[i]; }
+  __device__ static __forceinline__ bool diag(const Params& p) { return p.diag_inertia != 0; }
+  __device__ static __forceinline__ float I(const Params& p, int i) { return p.I[i]; }
+  __device__ static __forceinline__ float Iinv(const Params& p, int i) { return p.Iinv[i]; }
+  __device__ static __forceinline__ float Q(const Params& p, int i) { return p.Q[i]; }
+  __device__ static __forceinline__ float Rw(const Params& p, int i) { return p.Rw[i]; }
+  __device__ static __forceinline__ float urz(const Params& p, int n) { return p.urz[n]; }
+  __device__ static __forceinline__ float mu(const Params& p) { return p.mu; }
+  __device__ static __forceinline__ float fz_min(const Params& p) { return p.fz_min; }
+  __device__ static __forceinline__ float fz_max(const Params& p) { return p.fz_max; }
+  __device__ static __forceinline__ float w_fc(const Params& p) { return p.w_fc; }
+};
+struct ModelC {
+  static constexpr bool kStatic = true;
+  __device__ static __forceinline__ constexpr float dt(const Params&) { return model::kDt; }
+  __device__ static __forceinline__ constexpr float inv_mass(const Params&) { return model::kInvMass; }
+  __device__ static __forceinline__ constexpr float g(const Params&, int i) { return i == 2 ? model::kGz : 0.0f; }
+  __device__ static __forceinline__ constexpr bool diag(const Params&) { return true; }
+  __device__ static __forceinline__ constexpr float I(const Params&, int i) {
+    return i == 0 ? model::kI0 : (i == 4 ? model::kI1 : (i == 8 ? model::kI2 : 0.0f));
+  }
+  __device__ static __forceinline__ constexpr float Iinv(const Params&, int i) {
+    return i == 0 ? model::kIinv0 : (i == 4 ? model::kIinv1 : (i == 8 ? model::kIinv2 : 0.0f));
+  }
+  __device__ static __forceinline__ constexpr float Q(const Params&, int i) { return model::Q(i); }
+  __device__ static __forceinline__ constexpr float Rw(const Params&, int) { return model::kR; }
+  __device__ static __forceinline__ float urz(const Params&, int n) {  // n = stance-leg count 0..4
+    return n <= 1 ? model::urz(1) : (n == 2 ? model::urz(2) : (n == 3 ? model::urz(3) : model::urz(4)));
+  }
+  __device__ static __forceinline__ constexpr float mu(const Params&) { return model::kMu; }
+  __device__ static __forceinline__ constexpr float fz_min(const Params&) { return model::kFzMin; }
+  __device__ static __forceinline__ constexpr float fz_max(const Params&) { return model::kFzMax; }
+  __device__ static __forceinline__ constexpr float w_fc(const Params&) { return model::kWfc; }
+};
+
+// 1 / x for the Euler-rate map (|x| = cos(pitch) >= sin(1e-3) on every scored state, L26):
+// MUFU reciprocal, flush-to-zero variant (no denormal range fix-up is needed here)
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // Eq. 1 angular part at one RK4 stage (L24): given the world torque tau,
 //   w' = I^-1 (R^T tau - w x I w),  Phi' = E'^-1(Phi) w.
 // Angular state in three pairs: A = (roll, pitch), B = (yaw, w_x), C = (w_y, w_z).
+template <class KC>
 __device__ __forceinline__ void ang_deriv(const Params& p, float2 A, float2 B, float2 C, float tx, float ty, float tz,
                                           float2& dA, float2& dB, float2& dC) {
   float sr, cr, sp, cp, sy, cy;
@@ -417,14 +472,14 @@ __device__ __forceinline__ void ang_deriv(const Params& p, float2 A, float2 B, f
   const float by = fmaf(cr, t1y, sr * t2z), bz = fmaf(cr, t2z, -sr * t1y);
   float dwx;
   float2 dwyz;
-  if (p.diag_inertia) {
-    const float Lx = p.I[0] * wx;
-    const float2 Lyz = fmul2(f2(p.I[4], p.I[8]), C);
+  if (KC::diag(p)) {
+    const float Lx = KC::I(p, 0) * wx;
+    const float2 Lyz = fmul2(f2(KC::I(p, 4), KC::I(p, 8)), C);
     // r = b - w x L = b + L x w
     const float rx = bx + fmaf(Lyz.x, wz, -Lyz.y * wy);
     const float2 ryz = fadd2(f2(by, bz), f2(fmaf(Lyz.y, wx, -Lx * wz), fmaf(Lx, wy, -Lyz.x * wx)));
-    dwx = p.Iinv[0] * rx;
-    dwyz = fmul2(f2(p.Iinv[4], p.Iinv[8]), ryz);
+    dwx = KC::Iinv(p, 0) * rx;
+    dwyz = fmul2(f2(KC::Iinv(p, 4), KC::Iinv(p, 8)), ryz);
   } else {
     const float Lx = fmaf(p.I[0], wx, fmaf(p.I[1], wy, p.I[2] * wz));
     const float Ly = fmaf(p.I[3], wx, fmaf(p.I[4], wy, p.I[5] * wz));
@@ -436,7 +491,7 @@ __device__ __forceinline__ void ang_deriv(const Params& p, float2 A, float2 B, f
     dwyz = f2(fmaf(p.Iinv[3], rx, fmaf(p.Iinv[4], ry, p.Iinv[5] * rz)),
               fmaf(p.Iinv[6], rx, fmaf(p.Iinv[7], ry, p.Iinv[8] * rz)));
   }
-  const float rc = __fdividef(1.0f, cp);
+  const float rc = rcp_approx(cp);
   const float a = fmaf(sr, wy, cr * wz);
   dA = f2(fmaf(sp * rc, a, wx), fmaf(cr, wy, -sr * wz));
   dB = f2(a * rc, dwx);
@@ -454,10 +509,10 @@ struct StepForces {
 };
 constexpr int kStepForceFloats = 10;
 
-template <int P>
+template <int P, class KC = DynC>
 __device__ __forceinline__ StepForces step_forces(const Params& p, const Theta<P>& th, uint32_t fl, int j,
                                                   const RobotSmem& s) {
-  const float urz = p.urz[__popc(fl & 0xFu)];
+  const float urz = KC::urz(p, __popc(fl & 0xFu));
   float Wj[P];
 #pragma unroll
   for (int q = 0; q < P; ++q) Wj[q] = p.W[j][q];
@@ -476,16 +531,16 @@ __device__ __forceinline__ StepForces step_forces(const Params& p, const Theta<P
         g = ffma2(f2(Wj[q], Wj[q]), th.xy[q][leg], g);
         gz = fmaf(Wj[q], th.z[q][leg], gz);
       }
-      const float fzc = fminf(fmaxf(gz, p.fz_min), p.fz_max);
-      const float l = p.mu * fzc;
-      const float vzv = fmaxf(p.fz_min - gz, 0.0f) + fmaxf(gz - p.fz_max, 0.0f);
+      const float fzc = fminf(fmaxf(gz, KC::fz_min(p)), KC::fz_max(p));
+      const float l = KC::mu(p) * fzc;
+      const float vzv = fmaxf(KC::fz_min(p) - gz, 0.0f) + fmaxf(gz - KC::fz_max(p), 0.0f);
       const float vxv = fmaxf(fabsf(g.x) - l, 0.0f), vyv = fmaxf(fabsf(g.y) - l, 0.0f);
       o.pen += fmaf(vzv, vzv, fmaf(vxv, vxv, vyv * vyv));
       const float2 c = f2(fminf(fmaxf(g.x, -l), l), fminf(fmaxf(g.y, -l), l));
       // effort (u - u^r)^T R (u - u^r), u^r = (0, 0, m|g|/n_stance) (L12)
-      o.effxy = ffma2(fmul2(f2(p.Rw[3 * leg], p.Rw[3 * leg + 1]), c), c, o.effxy);
+      o.effxy = ffma2(fmul2(f2(KC::Rw(p, 3 * leg), KC::Rw(p, 3 * leg + 1)), c), c, o.effxy);
       const float ez = fzc - urz;
-      o.effz = fmaf(p.Rw[3 * leg + 2] * ez, ez, o.effz);
+      o.effz = fmaf(KC::Rw(p, 3 * leg + 2) * ez, ez, o.effz);
       // net force and moment about the origin; feet switch at touchdown (L23)
       o.F = fadd2(o.F, c);
       o.Fz += fzc;
@@ -539,24 +594,24 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 // steps a2-a4: Rollout(theta_k, x0), Alg. 2 with policy pi.
 // Per-leg work sits behind the stance bit: with a fixed gait every lane of a warp
 // shares the contact schedule, so swing legs cost nothing.
-template <int P>
+template <int P, class KC = DynC>
 static __device__ float rollout(const Params& p, const Theta<P>& th, int fi, const RobotSmem& s) {
   float2 pxy = f2(s.x0[0], s.x0[1]), vxy = f2(s.x0[3], s.x0[4]);
   float pz = s.x0[2], vz = s.x0[5];
   float2 A = f2(s.x0[6], s.x0[7]), Bq = f2(s.x0[8], s.x0[9]), C = f2(s.x0[10], s.x0[11]);
-  const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt * (1.0f / 6.0f);
-  const float dt2h = 0.5f * p.dt * p.dt, dt2q = 0.25f * p.dt * p.dt;
+  const float dt = KC::dt(p), hdt = 0.5f * dt, dt6 = dt * (1.0f / 6.0f);
+  const float dt2h = 0.5f * dt * dt, dt2q = 0.25f * dt * dt;
   const float2 dt_2 = f2(dt, dt), hdt_2 = f2(hdt, hdt), dt6_2 = f2(dt6, dt6), two_2 = f2(2.f, 2.f);
   const float2 dt2h_2 = f2(dt2h, dt2h), dt2q_2 = f2(dt2q, dt2q);
-  const float2 Qp = f2(p.Q[0], p.Q[1]), Qv = f2(p.Q[3], p.Q[4]), Qz = f2(p.Q[2], p.Q[5]);
-  const float2 QA = f2(p.Q[6], p.Q[7]), QB = f2(p.Q[8], p.Q[9]), QC = f2(p.Q[10], p.Q[11]);
-  const float2 im_2 = f2(p.inv_mass, p.inv_mass), gxy = f2(p.g[0], p.g[1]);
+  const float2 Qp = f2(KC::Q(p, 0), KC::Q(p, 1)), Qv = f2(KC::Q(p, 3), KC::Q(p, 4)), Qz = f2(KC::Q(p, 2), KC::Q(p, 5));
+  const float2 QA = f2(KC::Q(p, 6), KC::Q(p, 7)), QB = f2(KC::Q(p, 8), KC::Q(p, 9)), QC = f2(KC::Q(p, 10), KC::Q(p, 11));
+  const float2 im_2 = f2(KC::inv_mass(p), KC::inv_mass(p)), gxy = f2(KC::g(p, 0), KC::g(p, 1));
   const uint8_t* ct = s.ctab[fi];
   float J = 0.0f;
   bool bad = false;
   for (int j = 0; j < p.H; ++j) {
     const uint32_t fl = ct[j];
-    const float urz = p.urz[__popc(fl & 0xFu)];
+    const float urz = KC::urz(p, __popc(fl & 0xFu));
     float Wj[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) Wj[q] = p.W[j][q];
@@ -574,16 +629,16 @@ static __device__ float rollout(const Params& p, const Theta<P>& th, int fi, con
           g = ffma2(f2(Wj[q], Wj[q]), th.xy[q][leg], g);
           gz = fmaf(Wj[q], th.z[q][leg], gz);
         }
-        const float fzc = fminf(fmaxf(gz, p.fz_min), p.fz_max);
-        const float l = p.mu * fzc;
-        const float vzv = fmaxf(p.fz_min - gz, 0.0f) + fmaxf(gz - p.fz_max, 0.0f);
+        const float fzc = fminf(fmaxf(gz, KC::fz_min(p)), KC::fz_max(p));
+        const float l = KC::mu(p) * fzc;
+        const float vzv = fmaxf(KC::fz_min(p) - gz, 0.0f) + fmaxf(gz - KC::fz_max(p), 0.0f);
         const float vxv = fmaxf(fabsf(g.x) - l, 0.0f), vyv = fmaxf(fabsf(g.y) - l, 0.0f);
         pen += fmaf(vzv, vzv, fmaf(vxv, vxv, vyv * vyv));
         const float2 c = f2(fminf(fmaxf(g.x, -l), l), fminf(fmaxf(g.y, -l), l));
         // effort (u - u^r)^T R (u - u^r), u^r = (0, 0, m|g|/n_stance) (L12)
-        effxy = ffma2(fmul2(f2(p.Rw[3 * leg], p.Rw[3 * leg + 1]), c), c, effxy);
+        effxy = ffma2(fmul2(f2(KC::Rw(p, 3 * leg), KC::Rw(p, 3 * leg + 1)), c), c, effxy);
         const float ez = fzc - urz;
-        effz = fmaf(p.Rw[3 * leg + 2] * ez, ez, effz);
+        effz = fmaf(KC::Rw(p, 3 * leg + 2) * ez, ez, effz);
         // net force and moment about the origin; feet switch at touchdown (L23)
         F = fadd2(F, c);
         Fz += fzc;
@@ -610,31 +665,31 @@ static __device__ float rollout(const Params& p, const Theta<P>& th, int fi, con
     acc = ffma2(fmul2(QB, e4), e4, acc);
     acc = ffma2(fmul2(QC, e5), e5, acc);
     acc = fadd2(acc, effxy);
-    J += (acc.x + acc.y) + fmaf(p.w_fc, pen, effz);
+    J += (acc.x + acc.y) + fmaf(KC::w_fc(p), pen, effz);
     // --- x_{j+1}: v' = F/m + g is constant over the step, so RK4 on (p, v) is
     //     exact and the stage positions are closed-form; tau = M - p_stage x F ---
     const float2 axy = ffma2(F, im_2, gxy);
-    const float az = fmaf(Fz, p.inv_mass, p.g[2]);
+    const float az = fmaf(Fz, KC::inv_mass(p), KC::g(p, 2));
     float2 k1A, k1B, k1C, k2A, k2B, k2C, k3A, k3B, k3C, k4A, k4B, k4C;
-    ang_deriv(p, A, Bq, C, Mx - fmaf(pxy.y, Fz, -pz * F.y), My - fmaf(pz, F.x, -pxy.x * Fz),
+    ang_deriv<KC>(p, A, Bq, C, Mx - fmaf(pxy.y, Fz, -pz * F.y), My - fmaf(pz, F.x, -pxy.x * Fz),
               Mz - fmaf(pxy.x, F.y, -pxy.y * F.x), k1A, k1B, k1C);
     {
       const float2 q = ffma2(hdt_2, vxy, pxy);
       const float qz = fmaf(hdt, vz, pz);
-      ang_deriv(p, ffma2(hdt_2, k1A, A), ffma2(hdt_2, k1B, Bq), ffma2(hdt_2, k1C, C),
+      ang_deriv<KC>(p, ffma2(hdt_2, k1A, A), ffma2(hdt_2, k1B, Bq), ffma2(hdt_2, k1C, C),
                 Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
                 k2A, k2B, k2C);
     }
     {
       const float2 q = ffma2(dt2q_2, axy, ffma2(hdt_2, vxy, pxy));
       const float qz = fmaf(dt2q, az, fmaf(hdt, vz, pz));
-      ang_deriv(p, ffma2(hdt_2, k2A, A), ffma2(hdt_2, k2B, Bq), ffma2(hdt_2, k2C, C),
+      ang_deriv<KC>(p, ffma2(hdt_2, k2A, A), ffma2(hdt_2, k2B, Bq), ffma2(hdt_2, k2C, C),
                 Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
                 k3A, k3B, k3C);
     }
     const float2 n = ffma2(dt2h_2, axy, ffma2(dt_2, vxy, pxy));
     const float nz = fmaf(dt2h, az, fmaf(dt, vz, pz));
-    ang_deriv(p, ffma2(dt_2, k3A, A), ffma2(dt_2, k3B, Bq), ffma2(dt_2, k3C, C), Mx - fmaf(n.y, Fz, -nz * F.y),
+    ang_deriv<KC>(p, ffma2(dt_2, k3A, A), ffma2(dt_2, k3B, Bq), ffma2(dt_2, k3C, C), Mx - fmaf(n.y, Fz, -nz * F.y),
               My - fmaf(nz, F.x, -n.x * Fz), Mz - fmaf(n.x, F.y, -n.y * F.x), k4A, k4B, k4C);
     A = ffma2(dt6_2, ffma2(two_2, fadd2(k2A, k3A), fadd2(k1A, k4A)), A);
     Bq = ffma2(dt6_2, ffma2(two_2, fadd2(k2B, k3B), fadd2(k1B, k4B)), Bq);
@@ -657,18 +712,18 @@ static __device__ float rollout(const Params& p, const Theta<P>& th, int fi, con
 // Latency mode, integrator warps: rollout() with the stance-leg quantities of every
 // step read from the producer warps' table (step_forces: the same arithmetic, the
 // same bits), waiting on the chunk barriers.
-template <int P>
+template <int P, class KC = DynC>
 static __device__ float rollout_ab(const Params& p, int fi, const RobotSmem& s, const float* tab, int col) {
   float2 pxy = f2(s.x0[0], s.x0[1]), vxy = f2(s.x0[3], s.x0[4]);
   float pz = s.x0[2], vz = s.x0[5];
   float2 A = f2(s.x0[6], s.x0[7]), Bq = f2(s.x0[8], s.x0[9]), C = f2(s.x0[10], s.x0[11]);
-  const float dt = p.dt, hdt = 0.5f * p.dt, dt6 = p.dt * (1.0f / 6.0f);
-  const float dt2h = 0.5f * p.dt * p.dt, dt2q = 0.25f * p.dt * p.dt;
+  const float dt = KC::dt(p), hdt = 0.5f * dt, dt6 = dt * (1.0f / 6.0f);
+  const float dt2h = 0.5f * dt * dt, dt2q = 0.25f * dt * dt;
   const float2 dt_2 = f2(dt, dt), hdt_2 = f2(hdt, hdt), dt6_2 = f2(dt6, dt6), two_2 = f2(2.f, 2.f);
   const float2 dt2h_2 = f2(dt2h, dt2h), dt2q_2 = f2(dt2q, dt2q);
-  const float2 Qp = f2(p.Q[0], p.Q[1]), Qv = f2(p.Q[3], p.Q[4]), Qz = f2(p.Q[2], p.Q[5]);
-  const float2 QA = f2(p.Q[6], p.Q[7]), QB = f2(p.Q[8], p.Q[9]), QC = f2(p.Q[10], p.Q[11]);
-  const float2 im_2 = f2(p.inv_mass, p.inv_mass), gxy = f2(p.g[0], p.g[1]);
+  const float2 Qp = f2(KC::Q(p, 0), KC::Q(p, 1)), Qv = f2(KC::Q(p, 3), KC::Q(p, 4)), Qz = f2(KC::Q(p, 2), KC::Q(p, 5));
+  const float2 QA = f2(KC::Q(p, 6), KC::Q(p, 7)), QB = f2(KC::Q(p, 8), KC::Q(p, 9)), QC = f2(KC::Q(p, 10), KC::Q(p, 11));
+  const float2 im_2 = f2(KC::inv_mass(p), KC::inv_mass(p)), gxy = f2(KC::g(p, 0), KC::g(p, 1));
   float J = 0.0f;
   bool bad = false;
   int next_chunk = 0;
@@ -703,31 +758,31 @@ static __device__ float rollout_ab(const Params& p, int fi, const RobotSmem& s, 
     acc = ffma2(fmul2(QB, e4), e4, acc);
     acc = ffma2(fmul2(QC, e5), e5, acc);
     acc = fadd2(acc, sf.effxy);
-    J += (acc.x + acc.y) + fmaf(p.w_fc, sf.pen, sf.effz);
+    J += (acc.x + acc.y) + fmaf(KC::w_fc(p), sf.pen, sf.effz);
     // --- x_{j+1}: v' = F/m + g is constant over the step, so RK4 on (p, v) is
     //     exact and the stage positions are closed-form; tau = M - p_stage x F ---
     const float2 axy = ffma2(F, im_2, gxy);
-    const float az = fmaf(Fz, p.inv_mass, p.g[2]);
+    const float az = fmaf(Fz, KC::inv_mass(p), KC::g(p, 2));
     float2 k1A, k1B, k1C, k2A, k2B, k2C, k3A, k3B, k3C, k4A, k4B, k4C;
-    ang_deriv(p, A, Bq, C, Mx - fmaf(pxy.y, Fz, -pz * F.y), My - fmaf(pz, F.x, -pxy.x * Fz),
+    ang_deriv<KC>(p, A, Bq, C, Mx - fmaf(pxy.y, Fz, -pz * F.y), My - fmaf(pz, F.x, -pxy.x * Fz),
               Mz - fmaf(pxy.x, F.y, -pxy.y * F.x), k1A, k1B, k1C);
     {
       const float2 q = ffma2(hdt_2, vxy, pxy);
       const float qz = fmaf(hdt, vz, pz);
-      ang_deriv(p, ffma2(hdt_2, k1A, A), ffma2(hdt_2, k1B, Bq), ffma2(hdt_2, k1C, C),
+      ang_deriv<KC>(p, ffma2(hdt_2, k1A, A), ffma2(hdt_2, k1B, Bq), ffma2(hdt_2, k1C, C),
                 Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
                 k2A, k2B, k2C);
     }
     {
       const float2 q = ffma2(dt2q_2, axy, ffma2(hdt_2, vxy, pxy));
       const float qz = fmaf(dt2q, az, fmaf(hdt, vz, pz));
-      ang_deriv(p, ffma2(hdt_2, k2A, A), ffma2(hdt_2, k2B, Bq), ffma2(hdt_2, k2C, C),
+      ang_deriv<KC>(p, ffma2(hdt_2, k2A, A), ffma2(hdt_2, k2B, Bq), ffma2(hdt_2, k2C, C),
                 Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
                 k3A, k3B, k3C);
     }
     const float2 n = ffma2(dt2h_2, axy, ffma2(dt_2, vxy, pxy));
     const float nz = fmaf(dt2h, az, fmaf(dt, vz, pz));
-    ang_deriv(p, ffma2(dt_2, k3A, A), ffma2(dt_2, k3B, Bq), ffma2(dt_2, k3C, C), Mx - fmaf(n.y, Fz, -nz * F.y),
+    ang_deriv<KC>(p, ffma2(dt_2, k3A, A), ffma2(dt_2, k3B, Bq), ffma2(dt_2, k3C, C), Mx - fmaf(n.y, Fz, -nz * F.y),
               My - fmaf(nz, F.x, -n.x * Fz), Mz - fmaf(n.x, F.y, -n.y * F.x), k4A, k4B, k4C);
     A = ffma2(dt6_2, ffma2(two_2, fadd2(k2A, k3A), fadd2(k1A, k4A)), A);
     Bq = ffma2(dt6_2, ffma2(two_2, fadd2(k2B, k3B), fadd2(k1B, k4B)), Bq);
@@ -749,7 +804,7 @@ static __device__ float rollout_ab(const Params& p, int fi, const RobotSmem& s, 
 
 // Latency mode, producer warps: the stance-leg table of the integrator warp on the same
 // SM sub-partition (warp w: integrator warp w % 4, step class w / 4 - 1), chunk by chunk.
-template <int P>
+template <int P, class KC = DynC>
 __device__ __forceinline__ void produce_forces(const Params& p, const RobotSmem& s, const float* s_th, const int* s_fi,
                                                float* tab) {
   constexpr int D = 12 * P;
@@ -761,7 +816,7 @@ __device__ __forceinline__ void produce_forces(const Params& p, const RobotSmem&
   const uint8_t* ct = s.ctab[s_fi[col]];
   for (int c = 0; ab_chunk(c) < p.H; ++c) {
     const int j1 = min(ab_chunk(c + 1), p.H);
-    for (int j = ab_chunk(c) + cls; j < j1; j += kAbWarpsPerSmsp) store_forces(tab, j, col, step_forces<P>(p, th, ct[j], j, s));
+    for (int j = ab_chunk(c) + cls; j < j1; j += kAbWarpsPerSmsp) store_forces(tab, j, col, step_forces<P, KC>(p, th, ct[j], j, s));
     named_arrive(1 + c, kBlock * (1 + kAbWarpsPerSmsp));
   }
 }
@@ -1246,9 +1301,10 @@ static __device__ void publish_to_peers(const Params& p) {
 enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
 
 
-template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false, bool AB = false>
+template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false, bool AB = false, bool MODEL = false>
 __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ? 1 : kRolloutMinBlocks)
     sbs_rollout_kernel(const __grid_constant__ Params p) {
+  using KC = typename std::conditional<MODEL, ModelC, DynC>::type;  // compiled-in robot model, or the parameter block
   constexpr int D = 12 * P;
   constexpr int NR = D + 4;  // reduced rows (MPPI): w theta[D], w, w^2, J (finite), 1 (finite)
   constexpr int TS = kBlock;  // samples per tile
@@ -1339,13 +1395,13 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
     if (SPLIT && AB) {  // warps 4..15 tabulate the stance-leg forces, warps 0..3 integrate
       float* tab = reinterpret_cast<float*>(s_fi + TS);
       if (!sampler_thread) {
-        produce_forces<P>(p, s, s_th, s_fi, tab);
+        produce_forces<P, KC>(p, s, s_th, s_fi, tab);
       } else {
         fi = s_fi[tid];
         if (blockIdx.x == 0) SBS_TS(2);
         SBS_CTS(1);
         SBS_CTS(4);
-        const float Ja = rollout_ab<P>(p, fi, s, tab, tid);  // (every integrator lane: barriers)
+        const float Ja = rollout_ab<P, KC>(p, fi, s, tab, tid);  // (every integrator lane: barriers)
         SBS_CTS(5);
         SBS_CTS(2);
         if (blockIdx.x == 0) SBS_TS(3);
@@ -1367,7 +1423,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
       if (blockIdx.x == 0) SBS_TS(2);
       SBS_CTS(1);
       SBS_CTS(4);
-      J = rollout<P>(p, th, fi, s);
+      J = rollout<P, KC>(p, th, fi, s);
       SBS_CTS(5);
       SBS_CTS(2);
       if (blockIdx.x == 0) SBS_TS(3);
@@ -2304,7 +2360,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
 template <int P>
 struct PEntry {
   static cudaError_t rollout(const Params& p, int mode, bool fused, cudaStream_t s);
-  static int occupancy(int mode, bool fc, bool split);
+  static int occupancy(int mode, bool fc, bool split, bool model);
   static cudaError_t elite(const Params& p, cudaStream_t s);
   static cudaError_t naive_finalize(const Params& p, cudaStream_t s);
   static cudaError_t debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
@@ -2320,17 +2376,29 @@ constexpr size_t rollout_smem() {
          (SPLIT ? (size_t)kBlock * (D + 2) * sizeof(float) : 0);
 }
 
-template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false>
-static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
+// the compiled-in robot model (sbs_robot_model.h) is instantiated for its knot count only
+template <int P>
+constexpr bool kHasModel = (P == model::kKnots);
+
+template <int P, int EPI, bool FUSED, bool FC, bool SPLIT, bool MODEL>
+static cudaError_t launch_rollout_m(const Params& p, cudaStream_t s) {
   dim3 grid(p.n_cta, p.R);
   if constexpr (SPLIT) {  // (separate instantiation: its registers are not sized for the one-thread rollout)
     if (p.ab)
-      return launch_pdl(sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT, true>, grid, dim3(kBlock * kSplitLanes),
+      return launch_pdl(sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT, true, MODEL>, grid, dim3(kBlock * kSplitLanes),
                         split_smem_bytes(P, EPI == EPI_MPPI, p.H, true), 1, s, p);
   }
   const size_t smem = SPLIT ? split_smem_bytes(P, EPI == EPI_MPPI, p.H, false) : rollout_smem<P, EPI, FC, SPLIT>();
-  return launch_pdl(sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT>, grid, dim3(SPLIT ? kBlock * kSplitLanes : kBlock),
-                    smem, 1, s, p);
+  return launch_pdl(sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT, false, MODEL>, grid,
+                    dim3(SPLIT ? kBlock * kSplitLanes : kBlock), smem, 1, s, p);
+}
+
+template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false>
+static cudaError_t launch_rollout_t(const Params& p, cudaStream_t s) {
+  if constexpr (kHasModel<P> && !FC) {
+    if (p.model) return launch_rollout_m<P, EPI, FUSED, FC, SPLIT, true>(p, s);
+  }
+  return launch_rollout_m<P, EPI, FUSED, FC, SPLIT, false>(p, s);
 }
 
 template <int P>
@@ -2349,20 +2417,24 @@ cudaError_t PEntry<P>::rollout(const Params& p, int mode, bool fused, cudaStream
 }
 
 template <int P>
-int PEntry<P>::occupancy(int mode, bool fc, bool split) {
+int PEntry<P>::occupancy(int mode, bool fc, bool split, bool model) {
   size_t smem;
   const void* f;
+  constexpr bool M = kHasModel<P>;
+  model = model && M && !fc;
   if (mode == SBS_MPPI) {
     smem = split ? rollout_smem<P, EPI_MPPI, false, true>() : rollout_smem<P, EPI_MPPI, false, false>();
     f = split ? (const void*)sbs_rollout_kernel<P, EPI_MPPI, true, false, true>
-              : (const void*)sbs_rollout_kernel<P, EPI_MPPI, true>;
+              : (model ? (const void*)sbs_rollout_kernel<P, EPI_MPPI, true, false, false, false, M>
+                       : (const void*)sbs_rollout_kernel<P, EPI_MPPI, true>);
   } else if (fc) {
     smem = rollout_smem<P, EPI_ARGMIN, true, false>();
     f = (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false, true>;
   } else {
     smem = split ? rollout_smem<P, EPI_ARGMIN, false, true>() : rollout_smem<P, EPI_ARGMIN, false, false>();
     f = split ? (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false, false, true>
-              : (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false>;
+              : (model ? (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false, false, false, false, M>
+                       : (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false>);
   }
   int n = 0;  // (dynamic shared memory limits: prepare(), which sbs_create runs first)
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, f, split && !fc ? kBlock * kSplitLanes : kBlock, smem) != cudaSuccess) return 1;
@@ -2432,6 +2504,37 @@ cudaError_t PEntry<P>::prepare() {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_debug_samples_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if constexpr (kHasModel<P>) {  // the compiled-in robot model's instantiations
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, true, false, false, false, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, false, false, false, false, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, true, false, false, false, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, false, false, false, false, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    for (int ab = 0; ab < 2 && e == cudaSuccess; ++ab) {
+      e = cudaFuncSetAttribute(ab ? (const void*)sbs_rollout_kernel<P, EPI_MPPI, true, false, true, true, true>
+                                  : (const void*)sbs_rollout_kernel<P, EPI_MPPI, true, false, true, false, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ab ? (const void*)sbs_rollout_kernel<P, EPI_MPPI, false, false, true, true, true>
+                                    : (const void*)sbs_rollout_kernel<P, EPI_MPPI, false, false, true, false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ab ? (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, true, false, true, true, true>
+                                    : (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, true, false, true, false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ab ? (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false, false, true, true, true>
+                                    : (const void*)sbs_rollout_kernel<P, EPI_ARGMIN, false, false, true, false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
+    }
+  }
   // load every remaining kernel of this P now: with CUDA's lazy module loading the first
   // launch of a kernel can wait for the device, which must never happen behind a stream
   // that waits on a peer's flag (peer-memory exchange)
@@ -2476,8 +2579,8 @@ cudaError_t launch_rollout(const Params& p, int mode, bool fused, cudaStream_t s
   return cudaErrorInvalidValue;
 }
 
-int rollout_occupancy(int P, int mode, bool fc, bool split) {
-  SBS_DISPATCH_P(P, occupancy(mode, fc, split));
+int rollout_occupancy(int P, int mode, bool fc, bool split, bool model) {
+  SBS_DISPATCH_P(P, occupancy(mode, fc, split, model));
   return 1;
 }
 
