@@ -31,22 +31,27 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in _inputs())
 
 
-def _units():
+def _units(only_p=None):
     """(source, extra defines, object suffix): the kernels file once per knot count and once
-    for the common kernels, plus the host runtime -- compiled in parallel."""
-    units = [("sbs_kernels.cu", [f"SBS_TU_P={p}"], f"p{p}") for p in range(2, 9)]
+    for the common kernels, plus the host runtime -- compiled in parallel.  only_p: one knot
+    count (experiment builds)."""
+    units = [("sbs_kernels.cu", [f"SBS_TU_P={p}"], f"p{p}") for p in range(2, 9) if only_p in (None, p)]
     units.append(("sbs_kernels.cu", ["SBS_TU_COMMON"], "common"))
     units.append(("sbs_loop.cu", [], "loop"))
     units.append(("sbs_api.cpp", [], "api"))
     return units
 
 
-def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
-    """Compile csrc/ into `out` (default: the in-tree libsbs.so)."""
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=(), only_p=None) -> str:
+    """Compile csrc/ into `out` (default: the in-tree libsbs.so).  Experiment builds (another
+    `out`) may add `defines` and restrict the knot count with `only_p`."""
     if out == LIB and not force and not stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
     tag = "" if out == LIB else "." + os.path.basename(out)
+    if only_p is not None:
+        assert out != LIB, "the in-tree library carries every knot count"
+        defines = (*defines, f"SBS_ONLY_P={only_p}")
 
     def compile_unit(u):
         src, defs, suffix = u
@@ -59,7 +64,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
         return obj
 
     with ThreadPoolExecutor(max_workers=min(10, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(compile_unit, _units()))
+        objs = list(ex.map(compile_unit, _units(only_p)))
     tmp = out + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, out)

@@ -201,6 +201,7 @@ bool model_matches(const sbs::Params& P) {
             same_bits(P.fz_min, m::kFzMin) && same_bits(P.fz_max, m::kFzMax) && same_bits(P.w_fc, m::kWfc);
   ok = ok && same_bits(P.I[0], m::kI0) && same_bits(P.I[4], m::kI1) && same_bits(P.I[8], m::kI2);
   ok = ok && same_bits(P.Iinv[0], m::kIinv0) && same_bits(P.Iinv[4], m::kIinv1) && same_bits(P.Iinv[8], m::kIinv2);
+  ok = ok && same_bits(P.gyr[0], m::kGyr0) && same_bits(P.gyr[1], m::kGyr1) && same_bits(P.gyr[2], m::kGyr2);
   for (int i = 0; i < 12; ++i) ok = ok && same_bits(P.Q[i], m::Q(i)) && same_bits(P.Rw[i], m::kR);
   for (int n = 0; n <= 4; ++n) ok = ok && same_bits(P.urz[n], m::urz(n));
   return ok;
@@ -522,6 +523,9 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
       P.Iinv[i] = (float)inv[i];
     }
     P.diag_inertia = (A[1] == 0 && A[2] == 0 && A[5] == 0) ? 1 : 0;
+    P.gyr[0] = P.Iinv[0] * (P.I[4] - P.I[8]);
+    P.gyr[1] = P.Iinv[4] * (P.I[8] - P.I[0]);
+    P.gyr[2] = P.Iinv[8] * (P.I[0] - P.I[4]);
   }
   P.mu = cfg->mu;
   P.fz_min = cfg->fz_min;
@@ -537,6 +541,17 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.w_fc = cfg->w_fc;
   P.inv_lambda = (float)(1.0 / (double)cfg->lambda);
   for (int n = 0; n <= 4; ++n) P.urz[n] = (float)(-(double)cfg->mass * (double)cfg->gravity[2] / (double)std::max(1, n));
+  {  // packed operand pairs (Params::pk), binary32 as the kernel would form them
+    const float dt = cfg->dt, hdt = 0.5f * dt, dt6 = dt * (1.0f / 6.0f), dt2h = 0.5f * dt * dt,
+                dt2q = 0.25f * dt * dt;
+    const float v[6] = {dt, hdt, dt6, 2.0f, dt2h, dt2q};
+    for (int i = 0; i < 6; ++i) P.pk[i] = make_float2(v[i], v[i]);
+    P.pk[6] = make_float2(P.inv_mass, P.inv_mass);
+    P.pk[7] = make_float2(cfg->gravity[0], cfg->gravity[1]);
+    const int qi[6][2] = {{0, 1}, {3, 4}, {2, 5}, {6, 7}, {8, 9}, {10, 11}};
+    for (int i = 0; i < 6; ++i) P.pk[8 + i] = make_float2(cfg->Q[qi[i][0]], cfg->Q[qi[i][1]]);
+    for (int i = 0; i < 4; ++i) P.pk[14 + i] = make_float2(cfg->R[3 * i], cfg->R[3 * i + 1]);
+  }
   // ---- gait: Q0.32 tables (L22) ----
   for (int f = 0; f < SBS_MAX_FREQ; ++f) {
     P.inc[f] = f < cfg->n_freq ? q32_inc((double)cfg->freq_hz[f], (double)cfg->dt) : 0u;

@@ -17,11 +17,11 @@ constexpr int kEPartStride = 2 * SBS_MAX_D + 4;  // CEM elite-moment record [S1[
 // full-covariance CEM elite record [S1[D], n, lower triangle of S2 (D (D + 1) / 2)], 16-byte multiple
 __host__ __device__ constexpr int fc_record_floats(int D) { return ((D + 1 + D * (D + 1) / 2) + 3) / 4 * 4; }
 // latency-mode shared memory: MPPI reduction rows, theta / theta1 of the tile, and (ab)
-// the producer warps' stance-leg table [H][10][kBlock]
+// the producer warps' stance-leg table [H][7][kBlock]
 constexpr size_t kSplitSmemMax = 200 * 1024;
 __host__ __device__ constexpr size_t split_smem_bytes(int P, bool mppi, int H, bool ab) {
   return (mppi ? (size_t)(12 * P + 4) * (kBlock + 1) * 4 : 0) + (size_t)kBlock * (12 * P + 2) * 4 +
-         (ab ? (size_t)10 * H * kBlock * 4 : 0);
+         (ab ? (size_t)7 * H * kBlock * 4 : 0);
 }
 #ifndef SBS_ROLLOUT_MIN_BLOCKS
 #define SBS_ROLLOUT_MIN_BLOCKS 4
@@ -35,6 +35,7 @@ struct Params {
   float g[3];
   float I[9], Iinv[9];
   int diag_inertia;
+  float gyr[3];               // diagonal I: I^-1_x (I_y - I_z), I^-1_y (I_z - I_x), I^-1_z (I_x - I_y) (binary32)
   float mu, fz_min, fz_max;
   float dt;
   float duty;                 // duty factor D_f (closed-loop T_st = D_f / f_s)
@@ -42,6 +43,12 @@ struct Params {
   float Q[12], Rw[12];
   float rho, f_nominal, w_fc, inv_lambda;
   float urz[5];               // u^r_z = -m g_z / max(1, n_stance)   (L12)
+  // loop-invariant operand pairs of the rollout's packed FP32x2 arithmetic, formed on the
+  // host (same binary32 operations as the scalar forms) so that the kernel reads them as
+  // uniform-register pairs: dt, dt/2, dt/6, 2, dt^2/2, dt^2/4, (1/m, 1/m), (g_x, g_y),
+  // then the cost weights (Q_px, Q_py), (Q_vx, Q_vy), (Q_pz, Q_vz), (Q_roll, Q_pitch),
+  // (Q_yaw, Q_wx), (Q_wy, Q_wz), then (R_x, R_y) of legs 0..3
+  float2 pk[18];
   // --- gait ---
   uint32_t inc[SBS_MAX_FREQ]; // Q0.32 phase increment per step for each frequency option
   float freq_hz[SBS_MAX_FREQ];

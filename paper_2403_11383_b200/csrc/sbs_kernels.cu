@@ -28,6 +28,18 @@
 
 #include <type_traits>
 
+// experiment switches of the throughput rollout
+#ifndef SBS_TSM
+#define SBS_TSM 0
+#endif
+#ifndef SBS_TS_UNROLL
+#define SBS_TS_UNROLL 12
+#endif
+constexpr int kTsUnroll = SBS_TS_UNROLL;
+#ifndef SBS_TSM_MIN_BLOCKS
+#define SBS_TSM_MIN_BLOCKS 6
+#endif
+
 #include "sbs_internal.h"
 #include "sbs_noise.cuh"
 #include "sbs_robot_model.h"
@@ -269,6 +281,41 @@ template <int P>
 struct Theta {
   float2 xy[P][4];
   float z[P][4];
+  // Gamma_j of one leg (O8): the knots weighted by the step's Catmull-Rom row
+  __device__ __forceinline__ void spline(int leg, const float (&Wj)[P], float2& g, float& gz) const {
+    g = __fmul2_rn(make_float2(Wj[0], Wj[0]), xy[0][leg]);
+    gz = Wj[0] * z[0][leg];
+#pragma unroll
+    for (int q = 1; q < P; ++q) {
+      g = __ffma2_rn(make_float2(Wj[q], Wj[q]), xy[q][leg], g);
+      gz = fmaf(Wj[q], z[q][leg], gz);
+    }
+  }
+};
+
+// theta2 of one sample in the shared-memory tile (throughput mode, P = 4): a row of
+// kTsStride floats, leg-major -- leg i at [12 i, 12 i + 12) as (x0, y0, x1, y1),
+// (x2, y2, x3, y3), (z0, z1, z2, z3): three 16-byte loads per stance leg and step.
+// The stride (52 words) keeps the 16-byte loads of 8 consecutive samples on distinct banks.
+constexpr int kTsStride = 52;
+__host__ __device__ constexpr int ts_slot(int d) {  // element d = (p*4 + leg)*3 + axis
+  return 12 * ((d % 12) / 3) + ((d % 12) % 3 < 2 ? 2 * (d / 12) + (d % 12) % 3 : 8 + d / 12);
+}
+struct ThetaRow4 {
+  const float* row;
+  __device__ __forceinline__ void spline(int leg, const float (&Wj)[4], float2& g, float& gz) const {
+    const float4 a = *reinterpret_cast<const float4*>(row + 12 * leg);
+    const float4 b = *reinterpret_cast<const float4*>(row + 12 * leg + 4);
+    const float4 z = *reinterpret_cast<const float4*>(row + 12 * leg + 8);
+    g = __fmul2_rn(make_float2(Wj[0], Wj[0]), make_float2(a.x, a.y));
+    gz = Wj[0] * z.x;
+    g = __ffma2_rn(make_float2(Wj[1], Wj[1]), make_float2(a.z, a.w), g);
+    gz = fmaf(Wj[1], z.y, gz);
+    g = __ffma2_rn(make_float2(Wj[2], Wj[2]), make_float2(b.x, b.y), g);
+    gz = fmaf(Wj[2], z.z, gz);
+    g = __ffma2_rn(make_float2(Wj[3], Wj[3]), make_float2(b.z, b.w), g);
+    gz = fmaf(Wj[3], z.w, gz);
+  }
 };
 template <int P>
 __device__ __forceinline__ void theta_set(Theta<P>& t, int d, float v) {  // d is a compile-time constant here
@@ -314,6 +361,40 @@ __device__ __forceinline__ int draw_sample(const Params& p, uint32_t robot_g, in
   if (p.gait_adapt) {
     const U4 w = philox4x32_10_rk(0x80000000u, kk, s.iter, robot_g, p.rk);
     idx = (int)__umulhi(w.x, (uint32_t)p.n_freq);  // (w * n) >> 32
+  }
+  return idx;
+}
+
+// step a1 into the shared-memory tile row (throughput mode, P = 4): the same draws and
+// rounding as draw_sample, stored at ts_slot(d)
+template <int P>
+__device__ __forceinline__ int draw_sample_ts(const Params& p, uint32_t robot_g, int64_t k, const RobotSmem& s,
+                                              float* row) {
+  static_assert(P == 4, "leg-major tile rows are laid out for P = 4");
+  constexpr int D = 12 * P;
+  if (p.elite_preserve && k == 0) {  // L21
+#pragma unroll
+    for (int d = 0; d < D; ++d) row[ts_slot(d)] = s.mu[d];
+    return s.cur_idx;
+  }
+  const uint32_t kk = (uint32_t)k;
+  const bool grp = p.n_sig_groups > 1;
+  const float sc = grp ? p.sig_scale[(int)(k % p.n_sig_groups)] : 1.0f;
+#pragma unroll kTsUnroll
+  for (int q = 0; q < D / 4; ++q) {
+    const U4 w = philox4x32_10_rk((uint32_t)q, kk, s.iter, robot_g, p.rk);
+    float z[4];
+    box_muller_x2(w, z);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float sg = grp ? __fmul_rn(s.sig[4 * q + i], sc) : s.sig[4 * q + i];
+      row[ts_slot(4 * q + i)] = __fmaf_rn(sg, z[i], s.mu[4 * q + i]);
+    }
+  }
+  int idx = s.cur_idx;
+  if (p.gait_adapt) {
+    const U4 w = philox4x32_10_rk(0x80000000u, kk, s.iter, robot_g, p.rk);
+    idx = (int)__umulhi(w.x, (uint32_t)p.n_freq);
   }
   return idx;
 }
@@ -416,6 +497,7 @@ struct DynC {
   __device__ static __forceinline__ bool diag(const Params& p) { return p.diag_inertia != 0; }
   __device__ static __forceinline__ float I(const Params& p, int i) { return p.I[i]; }
   __device__ static __forceinline__ float Iinv(const Params& p, int i) { return p.Iinv[i]; }
+  __device__ static __forceinline__ float gyr(const Params& p, int i) { return p.gyr[i]; }
   __device__ static __forceinline__ float Q(const Params& p, int i) { return p.Q[i]; }
   __device__ static __forceinline__ float Rw(const Params& p, int i) { return p.Rw[i]; }
   __device__ static __forceinline__ float urz(const Params& p, int n) { return p.urz[n]; }
@@ -436,6 +518,9 @@ struct ModelC {
   __device__ static __forceinline__ constexpr float Iinv(const Params&, int i) {
     return i == 0 ? model::kIinv0 : (i == 4 ? model::kIinv1 : (i == 8 ? model::kIinv2 : 0.0f));
   }
+  __device__ static __forceinline__ constexpr float gyr(const Params&, int i) {
+    return i == 0 ? model::kGyr0 : (i == 1 ? model::kGyr1 : model::kGyr2);
+  }
   __device__ static __forceinline__ constexpr float Q(const Params&, int i) { return model::Q(i); }
   __device__ static __forceinline__ constexpr float Rw(const Params&, int) { return model::kR; }
   __device__ static __forceinline__ float urz(const Params&, int n) {  // n = stance-leg count 0..4
@@ -452,6 +537,13 @@ struct ModelC {
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// NaN-propagating maximum (max.NaN): a NaN component keeps the divergence test failing
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
   return r;
 }
 
@@ -473,13 +565,10 @@ __device__ __forceinline__ void ang_deriv(const Params& p, float2 A, float2 B, f
   float dwx;
   float2 dwyz;
   if (KC::diag(p)) {
-    const float Lx = KC::I(p, 0) * wx;
-    const float2 Lyz = fmul2(f2(KC::I(p, 4), KC::I(p, 8)), C);
-    // r = b - w x L = b + L x w
-    const float rx = bx + fmaf(Lyz.x, wz, -Lyz.y * wy);
-    const float2 ryz = fadd2(f2(by, bz), f2(fmaf(Lyz.y, wx, -Lx * wz), fmaf(Lx, wy, -Lyz.x * wx)));
-    dwx = KC::Iinv(p, 0) * rx;
-    dwyz = fmul2(f2(KC::Iinv(p, 4), KC::Iinv(p, 8)), ryz);
+    // diagonal I: (w x I w)_x = (I_z - I_y) w_y w_z (cyclic), so
+    // w'_x = I^-1_x b_x + G_x w_y w_z with G_x = I^-1_x (I_y - I_z) (cyclic; Params::gyr)
+    dwx = fmaf(KC::gyr(p, 0), wy * wz, KC::Iinv(p, 0) * bx);
+    dwyz = f2(fmaf(KC::gyr(p, 1), wz * wx, KC::Iinv(p, 4) * by), fmaf(KC::gyr(p, 2), wx * wy, KC::Iinv(p, 8) * bz));
   } else {
     const float Lx = fmaf(p.I[0], wx, fmaf(p.I[1], wy, p.I[2] * wz));
     const float Ly = fmaf(p.I[3], wx, fmaf(p.I[4], wy, p.I[5] * wz));
@@ -491,66 +580,72 @@ __device__ __forceinline__ void ang_deriv(const Params& p, float2 A, float2 B, f
     dwyz = f2(fmaf(p.Iinv[3], rx, fmaf(p.Iinv[4], ry, p.Iinv[5] * rz)),
               fmaf(p.Iinv[6], rx, fmaf(p.Iinv[7], ry, p.Iinv[8] * rz)));
   }
-  const float rc = rcp_approx(cp);
-  const float a = fmaf(sr, wy, cr * wz);
-  dA = f2(fmaf(sp * rc, a, wx), fmaf(cr, wy, -sr * wz));
-  dB = f2(a * rc, dwx);
+  // E'^-1 w: yaw rate (sr wy + cr wz) / cos(pitch); roll rate wx + sin(pitch) * yaw rate
+  const float yd = fmaf(sr, wy, cr * wz) * rcp_approx(cp);
+  dA = f2(fmaf(sp, yd, wx), fmaf(cr, wy, -sr * wz));
+  dB = f2(yd, dwx);
   dC = dwyz;
 }
 
 // Stance-leg quantities of one horizon step j (state-independent): the spline forces
-// Gamma_j = sigma(theta2, t_j) (O8), their cone projection and penalty (O9), the
-// effort terms and the net force / moment about the origin.  Per-leg work sits behind
-// the stance bit: with a fixed gait every lane of a warp shares the contact schedule,
-// so swing legs cost nothing.
+// Gamma_j = sigma(theta2, t_j) (O8), their cone projection and penalty (O9), the effort
+// (L12) and the net force / moment about the origin.  Per-leg work sits behind the
+// stance bit: with a fixed gait every lane of a warp shares the contact schedule, so
+// swing legs cost nothing.
 struct StepForces {
-  float2 F, effxy;
-  float Fz, Mx, My, Mz, pen, effz;
+  float2 F;
+  float Fz, Mx, My, Mz;
+  float ju;  // control part of the stage cost: (u - u^r)^T R (u - u^r) + w_fc pen
 };
-constexpr int kStepForceFloats = 10;
+constexpr int kStepForceFloats = 7;
 
-template <int P, class KC = DynC>
-__device__ __forceinline__ StepForces step_forces(const Params& p, const Theta<P>& th, uint32_t fl, int j,
+template <int P, class KC = DynC, class TH = Theta<P>>
+__device__ __forceinline__ StepForces step_forces(const Params& p, const TH& th, uint32_t fl, const float (&Wj)[P],
                                                   const RobotSmem& s) {
   const float urz = KC::urz(p, __popc(fl & 0xFu));
-  float Wj[P];
-#pragma unroll
-  for (int q = 0; q < P; ++q) Wj[q] = p.W[j][q];
   // accumulators start at -0 (the additive identity), so the first add is not a real op
   StepForces o;
   o.F = f2(-0.f, -0.f);
-  o.effxy = f2(-0.f, -0.f);
-  o.Fz = -0.f, o.Mx = -0.f, o.My = -0.f, o.Mz = -0.f, o.pen = -0.f, o.effz = -0.f;
+  o.Fz = -0.f, o.Mx = -0.f, o.My = -0.f, o.Mz = -0.f;
+  float2 pen = f2(-0.f, -0.f), eff = f2(-0.f, -0.f);
+  float penz = -0.f, effz = -0.f;
 #pragma unroll
   for (int leg = 0; leg < 4; ++leg) {
     if (fl & (1u << leg)) {
-      float2 g = fmul2(f2(Wj[0], Wj[0]), th.xy[0][leg]);
-      float gz = Wj[0] * th.z[0][leg];
-#pragma unroll
-      for (int q = 1; q < P; ++q) {
-        g = ffma2(f2(Wj[q], Wj[q]), th.xy[q][leg], g);
-        gz = fmaf(Wj[q], th.z[q][leg], gz);
-      }
+      float2 g;
+      float gz;
+      th.spline(leg, Wj, g, gz);
       const float fzc = fminf(fmaxf(gz, KC::fz_min(p)), KC::fz_max(p));
       const float l = KC::mu(p) * fzc;
-      const float vzv = fmaxf(KC::fz_min(p) - gz, 0.0f) + fmaxf(gz - KC::fz_max(p), 0.0f);
-      const float vxv = fmaxf(fabsf(g.x) - l, 0.0f), vyv = fmaxf(fabsf(g.y) - l, 0.0f);
-      o.pen += fmaf(vzv, vzv, fmaf(vxv, vxv, vyv * vyv));
       const float2 c = f2(fminf(fmaxf(g.x, -l), l), fminf(fmaxf(g.y, -l), l));
+      // squared violation of the raw output = squared distance to its projection
+      // (max(0, |g| - l) = |g - c| and max(0, fz_min - g) + max(0, g - fz_max) = |g - fzc|)
+      const float2 dv = fadd2(g, f2(-c.x, -c.y));
+      const float dz = gz - fzc;
+      pen = ffma2(dv, dv, pen);
+      penz = fmaf(dz, dz, penz);
       // effort (u - u^r)^T R (u - u^r), u^r = (0, 0, m|g|/n_stance) (L12)
-      o.effxy = ffma2(fmul2(f2(KC::Rw(p, 3 * leg), KC::Rw(p, 3 * leg + 1)), c), c, o.effxy);
       const float ez = fzc - urz;
-      o.effz = fmaf(KC::Rw(p, 3 * leg + 2) * ez, ez, o.effz);
+      if constexpr (KC::kStatic) {  // one weight for every component: applied once per step
+        eff = ffma2(c, c, eff);
+        effz = fmaf(ez, ez, effz);
+      } else {
+        eff = ffma2(p.pk[14 + leg], fmul2(c, c), eff);  // R (c c), the weight pair uniform
+        effz = fmaf(KC::Rw(p, 3 * leg + 2) * ez, ez, effz);
+      }
       // net force and moment about the origin; feet switch at touchdown (L23)
       o.F = fadd2(o.F, c);
       o.Fz += fzc;
       const int fo = ((fl >> (4 + leg)) & 1u) * 12 + 3 * leg;  // feet_next after touchdown
       const float fx = s.feet[fo], fy = s.feet[fo + 1], fzz = s.feet[fo + 2];
-      o.Mx += fmaf(fy, fzc, -fzz * c.y);
-      o.My += fmaf(fzz, c.x, -fx * fzc);
-      o.Mz += fmaf(fx, c.y, -fy * c.x);
+      o.Mx = fmaf(fy, fzc, fmaf(-fzz, c.y, o.Mx));
+      o.My = fmaf(fzz, c.x, fmaf(-fx, fzc, o.My));
+      o.Mz = fmaf(fx, c.y, fmaf(-fy, c.x, o.Mz));
     }
   }
+  const float pen_s = (pen.x + pen.y) + penz;
+  const float eff_s = (eff.x + eff.y) + effz;
+  o.ju = fmaf(KC::w_fc(p), pen_s, KC::kStatic ? KC::Rw(p, 0) * eff_s : eff_s);
   return o;
 }
 
@@ -564,10 +659,7 @@ __device__ __forceinline__ void store_forces(float* tab, int j, int col, const S
   t[3 * kBlock] = f.Mx;
   t[4 * kBlock] = f.My;
   t[5 * kBlock] = f.Mz;
-  t[6 * kBlock] = f.effxy.x;
-  t[7 * kBlock] = f.effxy.y;
-  t[8 * kBlock] = f.pen;
-  t[9 * kBlock] = f.effz;
+  t[6 * kBlock] = f.ju;
 }
 __device__ __forceinline__ StepForces load_forces(const float* tab, int j, int col) {
   const float* t = tab + (size_t)j * kStepForceFloats * kBlock + col;
@@ -577,9 +669,7 @@ __device__ __forceinline__ StepForces load_forces(const float* tab, int j, int c
   f.Mx = t[3 * kBlock];
   f.My = t[4 * kBlock];
   f.Mz = t[5 * kBlock];
-  f.effxy = f2(t[6 * kBlock], t[7 * kBlock]);
-  f.pen = t[8 * kBlock];
-  f.effz = t[9 * kBlock];
+  f.ju = t[6 * kBlock];
   return f;
 }
 
@@ -591,118 +681,98 @@ constexpr int kAbWarpsPerSmsp = 3;  // producer warps per integrator warp (the C
 __device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// steps a2-a4: Rollout(theta_k, x0), Alg. 2 with policy pi.
-// Per-leg work sits behind the stance bit: with a fixed gait every lane of a warp
-// shares the contact schedule, so swing legs cost nothing.
-template <int P, class KC = DynC>
-static __device__ float rollout(const Params& p, const Theta<P>& th, int fi, const RobotSmem& s) {
+// State part of the stage cost r(u_j, x_j, x^r_j): (x - x^r)^T Q (x - x^r),
+// yaw error wrapped, packed pairs in the kernel's state order.
+__device__ __forceinline__ float state_cost(const Params& p, const float* xr, float2 pxy, float2 vxy, float pz, float vz,
+                                            float2 A, float2 Bq, float2 C) {
+  const float2 e0 = fadd2(pxy, f2(-xr[0], -xr[1]));
+  const float2 e1 = fadd2(vxy, f2(-xr[2], -xr[3]));
+  const float2 e2 = fadd2(f2(pz, vz), f2(-xr[4], -xr[5]));
+  const float2 e3 = fadd2(A, f2(-xr[6], -xr[7]));
+  float2 e4 = fadd2(Bq, f2(-xr[8], -xr[9]));
+  e4.x = fmaf(-kTwoPi, rintf(e4.x * kInvTwoPi), e4.x);  // yaw wrapped to [-pi, pi]
+  const float2 e5 = fadd2(C, f2(-xr[10], -xr[11]));
+  // Q (e e): the weight pair is the uniform operand of each packed multiply-add (Params::pk)
+  float2 acc = fmul2(p.pk[8], fmul2(e0, e0));
+  acc = ffma2(p.pk[9], fmul2(e1, e1), acc);
+  acc = ffma2(p.pk[10], fmul2(e2, e2), acc);
+  acc = ffma2(p.pk[11], fmul2(e3, e3), acc);
+  acc = ffma2(p.pk[12], fmul2(e4, e4), acc);
+  acc = ffma2(p.pk[13], fmul2(e5, e5), acc);
+  return acc.x + acc.y;
+}
+
+// x_{j+1} = f(x_j, u_j), Eq. 1 with classic RK4.  v' = F/m + g is
+// constant over the step, so RK4 on (p, v) is exact and the stage positions q are
+// closed-form; each stage's torque about the CoM is tau = M - q x F (M, F about the
+// origin, step_forces), and only the 6 angular states run the RK4 recurrence.
+template <class KC>
+__device__ __forceinline__ void srbd_step(const Params& p, const StepForces& sf, float2& pxy, float2& vxy, float& pz,
+                                          float& vz, float2& A, float2& Bq, float2& C) {
+  const float dt = KC::dt(p), hdt = 0.5f * dt;
+  const float dt2h = 0.5f * dt * dt, dt2q = 0.25f * dt * dt;
+  // packed operand pairs from the parameter block (uniform registers; Params::pk)
+  const float2 dt_2 = p.pk[0], hdt_2 = p.pk[1], dt6_2 = p.pk[2], two_2 = p.pk[3];
+  const float2 dt2h_2 = p.pk[4], dt2q_2 = p.pk[5], im_2 = p.pk[6], gxy = p.pk[7];
+  const float2 F = sf.F;
+  const float Fz = sf.Fz;
+  // tau = M - q x F at the stage position (q, qz)
+  auto tq = [&](float2 q, float qz, float& tx, float& ty, float& tz) {
+    tx = fmaf(qz, F.y, fmaf(-q.y, Fz, sf.Mx));
+    ty = fmaf(q.x, Fz, fmaf(-qz, F.x, sf.My));
+    tz = fmaf(q.y, F.x, fmaf(-q.x, F.y, sf.Mz));
+  };
+  const float2 axy = ffma2(F, im_2, gxy);
+  const float az = fmaf(Fz, KC::inv_mass(p), KC::g(p, 2));
+  float2 k1A, k1B, k1C, k2A, k2B, k2C, k3A, k3B, k3C, k4A, k4B, k4C;
+  float tx, ty, tz;
+  tq(pxy, pz, tx, ty, tz);
+  ang_deriv<KC>(p, A, Bq, C, tx, ty, tz, k1A, k1B, k1C);
+  tq(ffma2(hdt_2, vxy, pxy), fmaf(hdt, vz, pz), tx, ty, tz);
+  ang_deriv<KC>(p, ffma2(hdt_2, k1A, A), ffma2(hdt_2, k1B, Bq), ffma2(hdt_2, k1C, C), tx, ty, tz, k2A, k2B, k2C);
+  tq(ffma2(dt2q_2, axy, ffma2(hdt_2, vxy, pxy)), fmaf(dt2q, az, fmaf(hdt, vz, pz)), tx, ty, tz);
+  ang_deriv<KC>(p, ffma2(hdt_2, k2A, A), ffma2(hdt_2, k2B, Bq), ffma2(hdt_2, k2C, C), tx, ty, tz, k3A, k3B, k3C);
+  const float2 n = ffma2(dt2h_2, axy, ffma2(dt_2, vxy, pxy));
+  const float nz = fmaf(dt2h, az, fmaf(dt, vz, pz));
+  tq(n, nz, tx, ty, tz);
+  ang_deriv<KC>(p, ffma2(dt_2, k3A, A), ffma2(dt_2, k3B, Bq), ffma2(dt_2, k3C, C), tx, ty, tz, k4A, k4B, k4C);
+  A = ffma2(dt6_2, ffma2(two_2, fadd2(k2A, k3A), fadd2(k1A, k4A)), A);
+  Bq = ffma2(dt6_2, ffma2(two_2, fadd2(k2B, k3B), fadd2(k1B, k4B)), Bq);
+  C = ffma2(dt6_2, ffma2(two_2, fadd2(k2C, k3C), fadd2(k1C, k4C)), C);
+  pxy = n;
+  pz = nz;
+  vxy = ffma2(dt_2, axy, vxy);
+  vz = fmaf(dt, az, vz);
+}
+
+// divergence of x_{j+1} (L26): a component beyond 1e6, a NaN (max.NaN keeps it) or
+// |pitch| >= pi/2 - 1e-3
+__device__ __forceinline__ bool diverged(float2 pxy, float2 vxy, float pz, float vz, float2 A, float2 Bq, float2 C) {
+  const float big = fmax_nan(fmax_nan(fmax_nan(fabsf(pxy.x), fabsf(pxy.y)), fmax_nan(fabsf(pz), fabsf(vxy.x))),
+                             fmax_nan(fmax_nan(fabsf(vxy.y), fabsf(vz)), fmax_nan(fabsf(A.x), fabsf(Bq.x))));
+  const float big2 = fmax_nan(fmax_nan(fabsf(Bq.y), fabsf(C.x)), fabsf(C.y));
+  return !(fmax_nan(big, big2) <= 1e6f) || !(fabsf(A.y) < kPitchMax);
+}
+
+// steps a2-a4: Rollout(theta_k, x0), Alg. 2 with policy pi:
+//   for j: u_j = pi(theta, t_j); J += r(u_j, x_j, x^r_j); x_{j+1} = f(x_j, u_j)
+// then J += rho (f - f_n)^2; a diverged rollout costs +inf (L26).
+template <int P, class KC = DynC, class TH = Theta<P>>
+static __device__ float rollout(const Params& p, const TH& th, int fi, const RobotSmem& s) {
   float2 pxy = f2(s.x0[0], s.x0[1]), vxy = f2(s.x0[3], s.x0[4]);
   float pz = s.x0[2], vz = s.x0[5];
   float2 A = f2(s.x0[6], s.x0[7]), Bq = f2(s.x0[8], s.x0[9]), C = f2(s.x0[10], s.x0[11]);
-  const float dt = KC::dt(p), hdt = 0.5f * dt, dt6 = dt * (1.0f / 6.0f);
-  const float dt2h = 0.5f * dt * dt, dt2q = 0.25f * dt * dt;
-  const float2 dt_2 = f2(dt, dt), hdt_2 = f2(hdt, hdt), dt6_2 = f2(dt6, dt6), two_2 = f2(2.f, 2.f);
-  const float2 dt2h_2 = f2(dt2h, dt2h), dt2q_2 = f2(dt2q, dt2q);
-  const float2 Qp = f2(KC::Q(p, 0), KC::Q(p, 1)), Qv = f2(KC::Q(p, 3), KC::Q(p, 4)), Qz = f2(KC::Q(p, 2), KC::Q(p, 5));
-  const float2 QA = f2(KC::Q(p, 6), KC::Q(p, 7)), QB = f2(KC::Q(p, 8), KC::Q(p, 9)), QC = f2(KC::Q(p, 10), KC::Q(p, 11));
-  const float2 im_2 = f2(KC::inv_mass(p), KC::inv_mass(p)), gxy = f2(KC::g(p, 0), KC::g(p, 1));
   const uint8_t* ct = s.ctab[fi];
   float J = 0.0f;
   bool bad = false;
   for (int j = 0; j < p.H; ++j) {
-    const uint32_t fl = ct[j];
-    const float urz = KC::urz(p, __popc(fl & 0xFu));
     float Wj[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) Wj[q] = p.W[j][q];
-    // accumulators start at -0 (the additive identity), so the first add is not a real op
-    float2 F = f2(-0.f, -0.f), effxy = f2(-0.f, -0.f);
-    float Fz = -0.f, Mx = -0.f, My = -0.f, Mz = -0.f, pen = -0.f, effz = -0.f;
-#pragma unroll
-    for (int leg = 0; leg < 4; ++leg) {
-      if (fl & (1u << leg)) {
-        // --- Gamma_j = sigma(theta2, t_j) for this stance leg, cone, penalty (O8-O9) ---
-        float2 g = fmul2(f2(Wj[0], Wj[0]), th.xy[0][leg]);
-        float gz = Wj[0] * th.z[0][leg];
-#pragma unroll
-        for (int q = 1; q < P; ++q) {
-          g = ffma2(f2(Wj[q], Wj[q]), th.xy[q][leg], g);
-          gz = fmaf(Wj[q], th.z[q][leg], gz);
-        }
-        const float fzc = fminf(fmaxf(gz, KC::fz_min(p)), KC::fz_max(p));
-        const float l = KC::mu(p) * fzc;
-        const float vzv = fmaxf(KC::fz_min(p) - gz, 0.0f) + fmaxf(gz - KC::fz_max(p), 0.0f);
-        const float vxv = fmaxf(fabsf(g.x) - l, 0.0f), vyv = fmaxf(fabsf(g.y) - l, 0.0f);
-        pen += fmaf(vzv, vzv, fmaf(vxv, vxv, vyv * vyv));
-        const float2 c = f2(fminf(fmaxf(g.x, -l), l), fminf(fmaxf(g.y, -l), l));
-        // effort (u - u^r)^T R (u - u^r), u^r = (0, 0, m|g|/n_stance) (L12)
-        effxy = ffma2(fmul2(f2(KC::Rw(p, 3 * leg), KC::Rw(p, 3 * leg + 1)), c), c, effxy);
-        const float ez = fzc - urz;
-        effz = fmaf(KC::Rw(p, 3 * leg + 2) * ez, ez, effz);
-        // net force and moment about the origin; feet switch at touchdown (L23)
-        F = fadd2(F, c);
-        Fz += fzc;
-        const int fo = ((fl >> (4 + leg)) & 1u) * 12 + 3 * leg;  // feet_next after touchdown
-        const float fx = s.feet[fo], fy = s.feet[fo + 1], fzz = s.feet[fo + 2];
-        Mx += fmaf(fy, fzc, -fzz * c.y);
-        My += fmaf(fzz, c.x, -fx * fzc);
-        Mz += fmaf(fx, c.y, -fy * c.x);
-      }
-    }
-    // --- stage cost r(u_j, x_j, x^r_j), packed pairs ---
-    const float* xr = &s.xref[12 * j];
-    const float2 e0 = fadd2(pxy, f2(-xr[0], -xr[1]));
-    const float2 e1 = fadd2(vxy, f2(-xr[2], -xr[3]));
-    const float2 e2 = fadd2(f2(pz, vz), f2(-xr[4], -xr[5]));
-    const float2 e3 = fadd2(A, f2(-xr[6], -xr[7]));
-    float2 e4 = fadd2(Bq, f2(-xr[8], -xr[9]));
-    e4.x = fmaf(-kTwoPi, rintf(e4.x * kInvTwoPi), e4.x);  // yaw wrapped to [-pi, pi]
-    const float2 e5 = fadd2(C, f2(-xr[10], -xr[11]));
-    float2 acc = fmul2(fmul2(Qp, e0), e0);
-    acc = ffma2(fmul2(Qv, e1), e1, acc);
-    acc = ffma2(fmul2(Qz, e2), e2, acc);
-    acc = ffma2(fmul2(QA, e3), e3, acc);
-    acc = ffma2(fmul2(QB, e4), e4, acc);
-    acc = ffma2(fmul2(QC, e5), e5, acc);
-    acc = fadd2(acc, effxy);
-    J += (acc.x + acc.y) + fmaf(KC::w_fc(p), pen, effz);
-    // --- x_{j+1}: v' = F/m + g is constant over the step, so RK4 on (p, v) is
-    //     exact and the stage positions are closed-form; tau = M - p_stage x F ---
-    const float2 axy = ffma2(F, im_2, gxy);
-    const float az = fmaf(Fz, KC::inv_mass(p), KC::g(p, 2));
-    float2 k1A, k1B, k1C, k2A, k2B, k2C, k3A, k3B, k3C, k4A, k4B, k4C;
-    ang_deriv<KC>(p, A, Bq, C, Mx - fmaf(pxy.y, Fz, -pz * F.y), My - fmaf(pz, F.x, -pxy.x * Fz),
-              Mz - fmaf(pxy.x, F.y, -pxy.y * F.x), k1A, k1B, k1C);
-    {
-      const float2 q = ffma2(hdt_2, vxy, pxy);
-      const float qz = fmaf(hdt, vz, pz);
-      ang_deriv<KC>(p, ffma2(hdt_2, k1A, A), ffma2(hdt_2, k1B, Bq), ffma2(hdt_2, k1C, C),
-                Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
-                k2A, k2B, k2C);
-    }
-    {
-      const float2 q = ffma2(dt2q_2, axy, ffma2(hdt_2, vxy, pxy));
-      const float qz = fmaf(dt2q, az, fmaf(hdt, vz, pz));
-      ang_deriv<KC>(p, ffma2(hdt_2, k2A, A), ffma2(hdt_2, k2B, Bq), ffma2(hdt_2, k2C, C),
-                Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
-                k3A, k3B, k3C);
-    }
-    const float2 n = ffma2(dt2h_2, axy, ffma2(dt_2, vxy, pxy));
-    const float nz = fmaf(dt2h, az, fmaf(dt, vz, pz));
-    ang_deriv<KC>(p, ffma2(dt_2, k3A, A), ffma2(dt_2, k3B, Bq), ffma2(dt_2, k3C, C), Mx - fmaf(n.y, Fz, -nz * F.y),
-              My - fmaf(nz, F.x, -n.x * Fz), Mz - fmaf(n.x, F.y, -n.y * F.x), k4A, k4B, k4C);
-    A = ffma2(dt6_2, ffma2(two_2, fadd2(k2A, k3A), fadd2(k1A, k4A)), A);
-    Bq = ffma2(dt6_2, ffma2(two_2, fadd2(k2B, k3B), fadd2(k1B, k4B)), Bq);
-    C = ffma2(dt6_2, ffma2(two_2, fadd2(k2C, k3C), fadd2(k1C, k4C)), C);
-    pxy = n;
-    pz = nz;
-    vxy = ffma2(dt_2, axy, vxy);
-    vz = fmaf(dt, az, vz);
-    // --- divergence of x_{j+1} (L26); NaN fails every <= test ---
-    const float big = fmaxf(fmaxf(fmaxf(fabsf(pxy.x), fabsf(pxy.y)), fmaxf(fabsf(pz), fabsf(vxy.x))),
-                            fmaxf(fmaxf(fabsf(vxy.y), fabsf(vz)), fmaxf(fabsf(A.x), fabsf(Bq.x))));
-    const float big2 = fmaxf(fmaxf(fabsf(Bq.y), fabsf(C.x)), fabsf(C.y));
-    bad = bad || !(big <= 1e6f) || !(big2 <= 1e6f) || !(fabsf(A.y) < kPitchMax);
+    const StepForces sf = step_forces<P, KC>(p, th, ct[j], Wj, s);
+    J += state_cost(p, &s.xref[12 * j], pxy, vxy, pz, vz, A, Bq, C) + sf.ju;
+    srbd_step<KC>(p, sf, pxy, vxy, pz, vz, A, Bq, C);
+    bad = bad || diverged(pxy, vxy, pz, vz, A, Bq, C);
   }
   const float df = p.freq_hz[fi] - p.f_nominal;
   J = fmaf(p.rho * df, df, J);  // P:350, once per rollout (L14)
@@ -717,13 +787,6 @@ static __device__ float rollout_ab(const Params& p, int fi, const RobotSmem& s, 
   float2 pxy = f2(s.x0[0], s.x0[1]), vxy = f2(s.x0[3], s.x0[4]);
   float pz = s.x0[2], vz = s.x0[5];
   float2 A = f2(s.x0[6], s.x0[7]), Bq = f2(s.x0[8], s.x0[9]), C = f2(s.x0[10], s.x0[11]);
-  const float dt = KC::dt(p), hdt = 0.5f * dt, dt6 = dt * (1.0f / 6.0f);
-  const float dt2h = 0.5f * dt * dt, dt2q = 0.25f * dt * dt;
-  const float2 dt_2 = f2(dt, dt), hdt_2 = f2(hdt, hdt), dt6_2 = f2(dt6, dt6), two_2 = f2(2.f, 2.f);
-  const float2 dt2h_2 = f2(dt2h, dt2h), dt2q_2 = f2(dt2q, dt2q);
-  const float2 Qp = f2(KC::Q(p, 0), KC::Q(p, 1)), Qv = f2(KC::Q(p, 3), KC::Q(p, 4)), Qz = f2(KC::Q(p, 2), KC::Q(p, 5));
-  const float2 QA = f2(KC::Q(p, 6), KC::Q(p, 7)), QB = f2(KC::Q(p, 8), KC::Q(p, 9)), QC = f2(KC::Q(p, 10), KC::Q(p, 11));
-  const float2 im_2 = f2(KC::inv_mass(p), KC::inv_mass(p)), gxy = f2(KC::g(p, 0), KC::g(p, 1));
   float J = 0.0f;
   bool bad = false;
   int next_chunk = 0;
@@ -740,62 +803,9 @@ static __device__ float rollout_ab(const Params& p, int fi, const RobotSmem& s, 
     if (j == ab_chunk(next_chunk)) named_sync(1 + next_chunk++, kBlock * (1 + kAbWarpsPerSmsp));
 #endif
     const StepForces sf = load_forces(tab, j, col);
-    const float2 F = sf.F;
-    const float Fz = sf.Fz, Mx = sf.Mx, My = sf.My, Mz = sf.Mz;
-    // --- stage cost r(u_j, x_j, x^r_j), packed pairs ---
-    const float* xr = &s.xref[12 * j];
-    const float2 e0 = fadd2(pxy, f2(-xr[0], -xr[1]));
-    const float2 e1 = fadd2(vxy, f2(-xr[2], -xr[3]));
-    const float2 e2 = fadd2(f2(pz, vz), f2(-xr[4], -xr[5]));
-    const float2 e3 = fadd2(A, f2(-xr[6], -xr[7]));
-    float2 e4 = fadd2(Bq, f2(-xr[8], -xr[9]));
-    e4.x = fmaf(-kTwoPi, rintf(e4.x * kInvTwoPi), e4.x);  // yaw wrapped to [-pi, pi]
-    const float2 e5 = fadd2(C, f2(-xr[10], -xr[11]));
-    float2 acc = fmul2(fmul2(Qp, e0), e0);
-    acc = ffma2(fmul2(Qv, e1), e1, acc);
-    acc = ffma2(fmul2(Qz, e2), e2, acc);
-    acc = ffma2(fmul2(QA, e3), e3, acc);
-    acc = ffma2(fmul2(QB, e4), e4, acc);
-    acc = ffma2(fmul2(QC, e5), e5, acc);
-    acc = fadd2(acc, sf.effxy);
-    J += (acc.x + acc.y) + fmaf(KC::w_fc(p), sf.pen, sf.effz);
-    // --- x_{j+1}: v' = F/m + g is constant over the step, so RK4 on (p, v) is
-    //     exact and the stage positions are closed-form; tau = M - p_stage x F ---
-    const float2 axy = ffma2(F, im_2, gxy);
-    const float az = fmaf(Fz, KC::inv_mass(p), KC::g(p, 2));
-    float2 k1A, k1B, k1C, k2A, k2B, k2C, k3A, k3B, k3C, k4A, k4B, k4C;
-    ang_deriv<KC>(p, A, Bq, C, Mx - fmaf(pxy.y, Fz, -pz * F.y), My - fmaf(pz, F.x, -pxy.x * Fz),
-              Mz - fmaf(pxy.x, F.y, -pxy.y * F.x), k1A, k1B, k1C);
-    {
-      const float2 q = ffma2(hdt_2, vxy, pxy);
-      const float qz = fmaf(hdt, vz, pz);
-      ang_deriv<KC>(p, ffma2(hdt_2, k1A, A), ffma2(hdt_2, k1B, Bq), ffma2(hdt_2, k1C, C),
-                Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
-                k2A, k2B, k2C);
-    }
-    {
-      const float2 q = ffma2(dt2q_2, axy, ffma2(hdt_2, vxy, pxy));
-      const float qz = fmaf(dt2q, az, fmaf(hdt, vz, pz));
-      ang_deriv<KC>(p, ffma2(hdt_2, k2A, A), ffma2(hdt_2, k2B, Bq), ffma2(hdt_2, k2C, C),
-                Mx - fmaf(q.y, Fz, -qz * F.y), My - fmaf(qz, F.x, -q.x * Fz), Mz - fmaf(q.x, F.y, -q.y * F.x),
-                k3A, k3B, k3C);
-    }
-    const float2 n = ffma2(dt2h_2, axy, ffma2(dt_2, vxy, pxy));
-    const float nz = fmaf(dt2h, az, fmaf(dt, vz, pz));
-    ang_deriv<KC>(p, ffma2(dt_2, k3A, A), ffma2(dt_2, k3B, Bq), ffma2(dt_2, k3C, C), Mx - fmaf(n.y, Fz, -nz * F.y),
-              My - fmaf(nz, F.x, -n.x * Fz), Mz - fmaf(n.x, F.y, -n.y * F.x), k4A, k4B, k4C);
-    A = ffma2(dt6_2, ffma2(two_2, fadd2(k2A, k3A), fadd2(k1A, k4A)), A);
-    Bq = ffma2(dt6_2, ffma2(two_2, fadd2(k2B, k3B), fadd2(k1B, k4B)), Bq);
-    C = ffma2(dt6_2, ffma2(two_2, fadd2(k2C, k3C), fadd2(k1C, k4C)), C);
-    pxy = n;
-    pz = nz;
-    vxy = ffma2(dt_2, axy, vxy);
-    vz = fmaf(dt, az, vz);
-    // --- divergence of x_{j+1} (L26); NaN fails every <= test ---
-    const float big = fmaxf(fmaxf(fmaxf(fabsf(pxy.x), fabsf(pxy.y)), fmaxf(fabsf(pz), fabsf(vxy.x))),
-                            fmaxf(fmaxf(fabsf(vxy.y), fabsf(vz)), fmaxf(fabsf(A.x), fabsf(Bq.x))));
-    const float big2 = fmaxf(fmaxf(fabsf(Bq.y), fabsf(C.x)), fabsf(C.y));
-    bad = bad || !(big <= 1e6f) || !(big2 <= 1e6f) || !(fabsf(A.y) < kPitchMax);
+    J += state_cost(p, &s.xref[12 * j], pxy, vxy, pz, vz, A, Bq, C) + sf.ju;
+    srbd_step<KC>(p, sf, pxy, vxy, pz, vz, A, Bq, C);
+    bad = bad || diverged(pxy, vxy, pz, vz, A, Bq, C);
   }
   const float df = p.freq_hz[fi] - p.f_nominal;
   J = fmaf(p.rho * df, df, J);  // P:350, once per rollout (L14)
@@ -816,7 +826,12 @@ __device__ __forceinline__ void produce_forces(const Params& p, const RobotSmem&
   const uint8_t* ct = s.ctab[s_fi[col]];
   for (int c = 0; ab_chunk(c) < p.H; ++c) {
     const int j1 = min(ab_chunk(c + 1), p.H);
-    for (int j = ab_chunk(c) + cls; j < j1; j += kAbWarpsPerSmsp) store_forces(tab, j, col, step_forces<P, KC>(p, th, ct[j], j, s));
+    for (int j = ab_chunk(c) + cls; j < j1; j += kAbWarpsPerSmsp) {
+      float Wj[P];
+#pragma unroll
+      for (int q = 0; q < P; ++q) Wj[q] = p.W[j][q];
+      store_forces(tab, j, col, step_forces<P, KC>(p, th, ct[j], Wj, s));
+    }
     named_arrive(1 + c, kBlock * (1 + kAbWarpsPerSmsp));
   }
 }
@@ -1301,16 +1316,23 @@ static __device__ void publish_to_peers(const Params& p) {
 enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
 
 
+// throughput mode with the theta tile in shared memory (P = 4): no theta registers
+template <int P, bool FC, bool SPLIT>
+constexpr bool rollout_tsm() { return SBS_TSM && P == 4 && !FC && !SPLIT; }
+template <int P, bool FC, bool SPLIT>
+constexpr int rollout_min_blocks() { return SPLIT ? 1 : (rollout_tsm<P, FC, SPLIT>() ? SBS_TSM_MIN_BLOCKS : kRolloutMinBlocks); }
+
 template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false, bool AB = false, bool MODEL = false>
-__global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ? 1 : kRolloutMinBlocks)
+__global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, (rollout_min_blocks<P, FC, SPLIT>()))
     sbs_rollout_kernel(const __grid_constant__ Params p) {
   using KC = typename std::conditional<MODEL, ModelC, DynC>::type;  // compiled-in robot model, or the parameter block
+  constexpr bool TSM = rollout_tsm<P, FC, SPLIT>();
   constexpr int D = 12 * P;
   constexpr int NR = D + 4;  // reduced rows (MPPI): w theta[D], w, w^2, J (finite), 1 (finite)
   constexpr int TS = kBlock;  // samples per tile
   __shared__ RobotSmem s;
   extern __shared__ float s_red[];  // [NR][kBlock + 1] (MPPI) or L^T [D][D] (FC); SPLIT: + theta [TS][D + 1], fidx [TS]
-  float* s_th = s_red + (EPI == EPI_MPPI ? NR * (kBlock + 1) : 0);
+  float* s_th = TSM ? s_red : s_red + (EPI == EPI_MPPI ? NR * (kBlock + 1) : 0);  // TSM: [kBlock][kTsStride]
   int* s_fi = reinterpret_cast<int*>(s_th + TS * (D + 1));
   const bool sampler_thread = !SPLIT || threadIdx.x < kBlock;  // holds a sample in phase 2 / the epilogue
   __shared__ float s_wm[2][kBlock / 32], s_ws[2][kBlock / 32], s_wn[2][kBlock / 32];  // per warp, by tile parity
@@ -1417,13 +1439,16 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
         fi = s_fi[tid];
       } else if (FC) {
         fi = draw_sample_fc<P, false>(p, robot_g, k, s, s_red, th);
+      } else if constexpr (TSM) {
+        fi = draw_sample_ts<P>(p, robot_g, k, s, s_th + tid * kTsStride);
       } else {
         fi = draw_sample<P, false>(p, robot_g, k, s, th);
       }
       if (blockIdx.x == 0) SBS_TS(2);
       SBS_CTS(1);
       SBS_CTS(4);
-      J = rollout<P, KC>(p, th, fi, s);
+      if constexpr (TSM) J = rollout<P, KC, ThetaRow4>(p, ThetaRow4{s_th + tid * kTsStride}, fi, s);
+      else J = rollout<P, KC>(p, th, fi, s);
       SBS_CTS(5);
       SBS_CTS(2);
       if (blockIdx.x == 0) SBS_TS(3);
@@ -1526,6 +1551,13 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
         s_red[q * NR + row] = a0 + a1;
       }
       __syncthreads();
+    } else if constexpr (TSM) {  // theta is in the tile: only the weight rows are staged
+      float* s_w = s_th + kBlock * kTsStride;  // [4][kBlock]: w, w^2, finite J, finite
+      s_w[0 * kBlock + tid] = w;
+      s_w[1 * kBlock + tid] = w * w;
+      s_w[2 * kBlock + tid] = fin ? J : 0.0f;
+      s_w[3 * kBlock + tid] = fin ? 1.0f : 0.0f;
+      __syncthreads();
     } else {
       if (valid) {
 #pragma unroll
@@ -1550,6 +1582,28 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
       float v;
       if (SPLIT) {
         v = (s_red[0 * NR + tid] + s_red[1 * NR + tid]) + (s_red[2 * NR + tid] + s_red[3 * NR + tid]);
+      } else if (TSM) {  // row tid of the tile: w theta[d] from the theta rows, or a weight row
+        const float* s_w = s_th + kBlock * kTsStride;
+        float a0 = 0.f, a1 = 0.f;
+        if (tid < D) {
+          const int64_t left = p.K_local - (int64_t)tile * TS;
+          const int nv = left >= kBlock ? kBlock : (int)left;
+          const float* col = s_th + ts_slot(tid);
+          int i = 0;
+          for (; i + 1 < nv; i += 2) {
+            a0 = fmaf(s_w[i], col[i * kTsStride], a0);
+            a1 = fmaf(s_w[i + 1], col[(i + 1) * kTsStride], a1);
+          }
+          if (i < nv) a0 = fmaf(s_w[i], col[i * kTsStride], a0);
+        } else {
+          const float* rw = s_w + (tid - D) * kBlock;
+#pragma unroll 8
+          for (int i = 0; i < kBlock; i += 2) {
+            a0 += rw[i];
+            a1 += rw[i + 1];
+          }
+        }
+        v = a0 + a1;
       } else {
         const float* rowp = &s_red[tid * (kBlock + 1)];
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
@@ -2372,6 +2426,7 @@ struct PEntry {
 template <int P, int EPI, bool FC, bool SPLIT>
 constexpr size_t rollout_smem() {
   constexpr int D = 12 * P;
+  if (rollout_tsm<P, FC, SPLIT>()) return (size_t)kBlock * kTsStride * sizeof(float) + (EPI == EPI_MPPI ? 4 * kBlock * sizeof(float) : 0);
   return (EPI == EPI_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : (FC ? (size_t)D * D * sizeof(float) : 0)) +
          (SPLIT ? (size_t)kBlock * (D + 2) * sizeof(float) : 0);
 }
@@ -2562,6 +2617,10 @@ extern "C" int SBS_CAT(sbs_debug_cta_p, SBS_TU_P)(unsigned long long* out) {
 #endif  // SBS_TU_P
 
 #if defined(SBS_TU_COMMON)
+#if defined(SBS_ONLY_P)  // experiment builds with one knot count (build.py only_p=...)
+#define SBS_DISPATCH_P(P_, CALL) \
+  if ((P_) == SBS_ONLY_P) return PEntry<SBS_ONLY_P>::CALL;
+#else
 #define SBS_DISPATCH_P(P_, CALL)                 \
   switch (P_) {                                  \
     case 2: return PEntry<2>::CALL;              \
@@ -2573,6 +2632,7 @@ extern "C" int SBS_CAT(sbs_debug_cta_p, SBS_TU_P)(unsigned long long* out) {
     case 8: return PEntry<8>::CALL;              \
     default: break;                              \
   }
+#endif
 
 cudaError_t launch_rollout(const Params& p, int mode, bool fused, cudaStream_t s) {
   SBS_DISPATCH_P(p.P, rollout(p, mode, fused, s));

@@ -34,6 +34,11 @@ constexpr float kInvMass = (float)(1.0 / (double)kMass);
 constexpr float kIinv0 = (float)(((double)kI1 * (double)kI2) / kDet);
 constexpr float kIinv1 = (float)(((double)kI0 * (double)kI2) / kDet);
 constexpr float kIinv2 = (float)(((double)kI0 * (double)kI1) / kDet);
+// gyroscopic coefficients of the diagonal-inertia Euler equations, binary32 as sbs_create
+// forms them: G_x = I^-1_x (I_y - I_z), G_y = I^-1_y (I_z - I_x), G_z = I^-1_z (I_x - I_y)
+constexpr float kGyr0 = kIinv0 * (kI1 - kI2);
+constexpr float kGyr1 = kIinv1 * (kI2 - kI0);
+constexpr float kGyr2 = kIinv2 * (kI0 - kI1);
 __host__ __device__ constexpr float urz(int n) {  // u^r_z = -m g_z / max(1, n) (L12)
   return (float)(-(double)kMass * (double)kGz / (double)(n > 1 ? n : 1));
 }
