@@ -9,6 +9,7 @@
 namespace sbs {
 
 constexpr int kBlock = 128;         // samples per tile = threads per rollout CTA
+constexpr int kRedStride = kBlock + 4;  // floats per row of the MPPI tile reduction (16-byte rows)
 constexpr int kMaxWorld = 8;               // ranks of one node (peer-memory exchange)
 constexpr int kInlineRefFloats = 16 * 12;  // host path, R = 1, H <= 16: inputs and reference ride in the kernel parameters
 constexpr int kSplitLanes = 4;      // latency-mode (SPLIT) rollout: lanes per sample in the sampler phase
@@ -20,7 +21,7 @@ __host__ __device__ constexpr int fc_record_floats(int D) { return ((D + 1 + D *
 // the producer warps' stance-leg table [H][7][kBlock]
 constexpr size_t kSplitSmemMax = 200 * 1024;
 __host__ __device__ constexpr size_t split_smem_bytes(int P, bool mppi, int H, bool ab) {
-  return (mppi ? (size_t)(12 * P + 4) * (kBlock + 1) * 4 : 0) + (size_t)kBlock * (12 * P + 2) * 4 +
+  return (mppi ? (size_t)(12 * P + 4) * kRedStride * 4 : 0) + (size_t)kBlock * (12 * P + 2) * 4 +
          (ab ? (size_t)7 * H * kBlock * 4 : 0);
 }
 #ifndef SBS_ROLLOUT_MIN_BLOCKS

@@ -28,17 +28,6 @@
 
 #include <type_traits>
 
-// experiment switches of the throughput rollout
-#ifndef SBS_TSM
-#define SBS_TSM 0
-#endif
-#ifndef SBS_TS_UNROLL
-#define SBS_TS_UNROLL 12
-#endif
-constexpr int kTsUnroll = SBS_TS_UNROLL;
-#ifndef SBS_TSM_MIN_BLOCKS
-#define SBS_TSM_MIN_BLOCKS 6
-#endif
 
 #include "sbs_internal.h"
 #include "sbs_noise.cuh"
@@ -86,7 +75,7 @@ struct RobotSmem {
   float mu[SBS_MAX_D];
   float sig[SBS_MAX_D];
   float x0[12];
-  float feet[24];  // [0, 12): feet_cur, [12, 24): feet_next
+  float4 feet[2][4];  // [0]: feet_cur, [1]: feet_next, per leg (x, y, z, 0): one 16-byte load per stance leg
   float xref[SBS_MAX_HORIZON * 12];  // per step, kernel order (px,py, vx,vy, pz,vz, roll,pitch, yaw,wx, wy,wz)
   uint8_t ctab[SBS_MAX_FREQ][SBS_MAX_HORIZON];  // bits 0-3: stance of leg i at step j; bits 4-7: leg i touched down
   uint32_t phase0;
@@ -139,8 +128,8 @@ static __device__ void load_robot(const Params& p, int r, RobotSmem& s, bool rol
   if (!rollout_inputs) return;  // sampling only (elite regeneration, debug draws)
   for (int a = threadIdx.x; a < 12; a += blockDim.x) {
     s.x0[a] = in->x0[a];
-    s.feet[a] = in->feet_cur[a];
-    s.feet[12 + a] = in->feet_next[a];
+    reinterpret_cast<float*>(&s.feet[0][a / 3])[a % 3] = in->feet_cur[a];
+    reinterpret_cast<float*>(&s.feet[1][a / 3])[a % 3] = in->feet_next[a];
   }
   const float* xr = robot_xref(p, r);
   for (int a = threadIdx.x; a < p.H * 12; a += blockDim.x) {
@@ -191,8 +180,8 @@ static __device__ void load_robot_issue(const Params& p, int r, RobotSmem& s, fl
   const sbs_input* in = p.in + r;
   for (int a = threadIdx.x; a < 12; a += blockDim.x) {
     cp_async4(&s.x0[a], &in->x0[a]);
-    cp_async4(&s.feet[a], &in->feet_cur[a]);
-    cp_async4(&s.feet[12 + a], &in->feet_next[a]);
+    cp_async4(reinterpret_cast<float*>(&s.feet[0][a / 3]) + a % 3, &in->feet_cur[a]);
+    cp_async4(reinterpret_cast<float*>(&s.feet[1][a / 3]) + a % 3, &in->feet_next[a]);
   }
   const float* xr = p.xref + (size_t)r * p.H * 12;
   for (int a = threadIdx.x; a < p.H * 12; a += blockDim.x) {
@@ -206,8 +195,8 @@ static __device__ void load_robot_commit(const Params& p, RobotSmem& s, const fl
     const sbs_input* in = &p.in_inline;
     for (int a = threadIdx.x; a < 12; a += blockDim.x) {
       s.x0[a] = in->x0[a];
-      s.feet[a] = in->feet_cur[a];
-      s.feet[12 + a] = in->feet_next[a];
+      reinterpret_cast<float*>(&s.feet[0][a / 3])[a % 3] = in->feet_cur[a];
+      reinterpret_cast<float*>(&s.feet[1][a / 3])[a % 3] = in->feet_next[a];
     }
     for (int a = threadIdx.x; a < p.H * 12; a += blockDim.x) {
       const int j = a / 12, c = a - 12 * j;
@@ -293,30 +282,7 @@ struct Theta {
   }
 };
 
-// theta2 of one sample in the shared-memory tile (throughput mode, P = 4): a row of
-// kTsStride floats, leg-major -- leg i at [12 i, 12 i + 12) as (x0, y0, x1, y1),
-// (x2, y2, x3, y3), (z0, z1, z2, z3): three 16-byte loads per stance leg and step.
-// The stride (52 words) keeps the 16-byte loads of 8 consecutive samples on distinct banks.
-constexpr int kTsStride = 52;
-__host__ __device__ constexpr int ts_slot(int d) {  // element d = (p*4 + leg)*3 + axis
-  return 12 * ((d % 12) / 3) + ((d % 12) % 3 < 2 ? 2 * (d / 12) + (d % 12) % 3 : 8 + d / 12);
-}
-struct ThetaRow4 {
-  const float* row;
-  __device__ __forceinline__ void spline(int leg, const float (&Wj)[4], float2& g, float& gz) const {
-    const float4 a = *reinterpret_cast<const float4*>(row + 12 * leg);
-    const float4 b = *reinterpret_cast<const float4*>(row + 12 * leg + 4);
-    const float4 z = *reinterpret_cast<const float4*>(row + 12 * leg + 8);
-    g = __fmul2_rn(make_float2(Wj[0], Wj[0]), make_float2(a.x, a.y));
-    gz = Wj[0] * z.x;
-    g = __ffma2_rn(make_float2(Wj[1], Wj[1]), make_float2(a.z, a.w), g);
-    gz = fmaf(Wj[1], z.y, gz);
-    g = __ffma2_rn(make_float2(Wj[2], Wj[2]), make_float2(b.x, b.y), g);
-    gz = fmaf(Wj[2], z.z, gz);
-    g = __ffma2_rn(make_float2(Wj[3], Wj[3]), make_float2(b.z, b.w), g);
-    gz = fmaf(Wj[3], z.w, gz);
-  }
-};
+
 template <int P>
 __device__ __forceinline__ void theta_set(Theta<P>& t, int d, float v) {  // d is a compile-time constant here
   const int pk = d / 12, c = d % 12, leg = c / 3, ax = c % 3;
@@ -361,40 +327,6 @@ __device__ __forceinline__ int draw_sample(const Params& p, uint32_t robot_g, in
   if (p.gait_adapt) {
     const U4 w = philox4x32_10_rk(0x80000000u, kk, s.iter, robot_g, p.rk);
     idx = (int)__umulhi(w.x, (uint32_t)p.n_freq);  // (w * n) >> 32
-  }
-  return idx;
-}
-
-// step a1 into the shared-memory tile row (throughput mode, P = 4): the same draws and
-// rounding as draw_sample, stored at ts_slot(d)
-template <int P>
-__device__ __forceinline__ int draw_sample_ts(const Params& p, uint32_t robot_g, int64_t k, const RobotSmem& s,
-                                              float* row) {
-  static_assert(P == 4, "leg-major tile rows are laid out for P = 4");
-  constexpr int D = 12 * P;
-  if (p.elite_preserve && k == 0) {  // L21
-#pragma unroll
-    for (int d = 0; d < D; ++d) row[ts_slot(d)] = s.mu[d];
-    return s.cur_idx;
-  }
-  const uint32_t kk = (uint32_t)k;
-  const bool grp = p.n_sig_groups > 1;
-  const float sc = grp ? p.sig_scale[(int)(k % p.n_sig_groups)] : 1.0f;
-#pragma unroll kTsUnroll
-  for (int q = 0; q < D / 4; ++q) {
-    const U4 w = philox4x32_10_rk((uint32_t)q, kk, s.iter, robot_g, p.rk);
-    float z[4];
-    box_muller_x2(w, z);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float sg = grp ? __fmul_rn(s.sig[4 * q + i], sc) : s.sig[4 * q + i];
-      row[ts_slot(4 * q + i)] = __fmaf_rn(sg, z[i], s.mu[4 * q + i]);
-    }
-  }
-  int idx = s.cur_idx;
-  if (p.gait_adapt) {
-    const U4 w = philox4x32_10_rk(0x80000000u, kk, s.iter, robot_g, p.rk);
-    idx = (int)__umulhi(w.x, (uint32_t)p.n_freq);
   }
   return idx;
 }
@@ -636,8 +568,8 @@ __device__ __forceinline__ StepForces step_forces(const Params& p, const TH& th,
       // net force and moment about the origin; feet switch at touchdown (L23)
       o.F = fadd2(o.F, c);
       o.Fz += fzc;
-      const int fo = ((fl >> (4 + leg)) & 1u) * 12 + 3 * leg;  // feet_next after touchdown
-      const float fx = s.feet[fo], fy = s.feet[fo + 1], fzz = s.feet[fo + 2];
+      const float4 ft = s.feet[(fl >> (4 + leg)) & 1u][leg];  // feet_next after touchdown
+      const float fx = ft.x, fy = ft.y, fzz = ft.z;
       o.Mx = fmaf(fy, fzc, fmaf(-fzz, c.y, o.Mx));
       o.My = fmaf(fzz, c.x, fmaf(-fx, fzc, o.My));
       o.Mz = fmaf(fx, c.y, fmaf(-fy, c.x, o.Mz));
@@ -1316,23 +1248,16 @@ static __device__ void publish_to_peers(const Params& p) {
 enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
 
 
-// throughput mode with the theta tile in shared memory (P = 4): no theta registers
-template <int P, bool FC, bool SPLIT>
-constexpr bool rollout_tsm() { return SBS_TSM && P == 4 && !FC && !SPLIT; }
-template <int P, bool FC, bool SPLIT>
-constexpr int rollout_min_blocks() { return SPLIT ? 1 : (rollout_tsm<P, FC, SPLIT>() ? SBS_TSM_MIN_BLOCKS : kRolloutMinBlocks); }
-
 template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false, bool AB = false, bool MODEL = false>
-__global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, (rollout_min_blocks<P, FC, SPLIT>()))
+__global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ? 1 : kRolloutMinBlocks)
     sbs_rollout_kernel(const __grid_constant__ Params p) {
   using KC = typename std::conditional<MODEL, ModelC, DynC>::type;  // compiled-in robot model, or the parameter block
-  constexpr bool TSM = rollout_tsm<P, FC, SPLIT>();
   constexpr int D = 12 * P;
   constexpr int NR = D + 4;  // reduced rows (MPPI): w theta[D], w, w^2, J (finite), 1 (finite)
   constexpr int TS = kBlock;  // samples per tile
   __shared__ RobotSmem s;
-  extern __shared__ float s_red[];  // [NR][kBlock + 1] (MPPI) or L^T [D][D] (FC); SPLIT: + theta [TS][D + 1], fidx [TS]
-  float* s_th = TSM ? s_red : s_red + (EPI == EPI_MPPI ? NR * (kBlock + 1) : 0);  // TSM: [kBlock][kTsStride]
+  extern __shared__ float s_red[];  // [NR][kRedStride] (MPPI) or L^T [D][D] (FC); SPLIT: + theta [TS][D + 1], fidx [TS]
+  float* s_th = s_red + (EPI == EPI_MPPI ? NR * kRedStride : 0);
   int* s_fi = reinterpret_cast<int*>(s_th + TS * (D + 1));
   const bool sampler_thread = !SPLIT || threadIdx.x < kBlock;  // holds a sample in phase 2 / the epilogue
   __shared__ float s_wm[2][kBlock / 32], s_ws[2][kBlock / 32], s_wn[2][kBlock / 32];  // per warp, by tile parity
@@ -1439,16 +1364,13 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, (rollou
         fi = s_fi[tid];
       } else if (FC) {
         fi = draw_sample_fc<P, false>(p, robot_g, k, s, s_red, th);
-      } else if constexpr (TSM) {
-        fi = draw_sample_ts<P>(p, robot_g, k, s, s_th + tid * kTsStride);
       } else {
         fi = draw_sample<P, false>(p, robot_g, k, s, th);
       }
       if (blockIdx.x == 0) SBS_TS(2);
       SBS_CTS(1);
       SBS_CTS(4);
-      if constexpr (TSM) J = rollout<P, KC, ThetaRow4>(p, ThetaRow4{s_th + tid * kTsStride}, fi, s);
-      else J = rollout<P, KC>(p, th, fi, s);
+      J = rollout<P, KC>(p, th, fi, s);
       SBS_CTS(5);
       SBS_CTS(2);
       if (blockIdx.x == 0) SBS_TS(3);
@@ -1551,29 +1473,22 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, (rollou
         s_red[q * NR + row] = a0 + a1;
       }
       __syncthreads();
-    } else if constexpr (TSM) {  // theta is in the tile: only the weight rows are staged
-      float* s_w = s_th + kBlock * kTsStride;  // [4][kBlock]: w, w^2, finite J, finite
-      s_w[0 * kBlock + tid] = w;
-      s_w[1 * kBlock + tid] = w * w;
-      s_w[2 * kBlock + tid] = fin ? J : 0.0f;
-      s_w[3 * kBlock + tid] = fin ? 1.0f : 0.0f;
-      __syncthreads();
     } else {
       if (valid) {
 #pragma unroll
         for (int d = 0; d < D; d += 2) {  // w theta, two coordinates per packed multiply
           const float2 v = __fmul2_rn(make_float2(w, w), make_float2(theta_get(th, d), theta_get(th, d + 1)));
-          s_red[d * (kBlock + 1) + tid] = v.x;
-          s_red[(d + 1) * (kBlock + 1) + tid] = v.y;
+          s_red[d * kRedStride + tid] = v.x;
+          s_red[(d + 1) * kRedStride + tid] = v.y;
         }
       } else {
 #pragma unroll
-        for (int d = 0; d < D; ++d) s_red[d * (kBlock + 1) + tid] = 0.0f;
+        for (int d = 0; d < D; ++d) s_red[d * kRedStride + tid] = 0.0f;
       }
-      s_red[(D + 0) * (kBlock + 1) + tid] = w;
-      s_red[(D + 1) * (kBlock + 1) + tid] = w * w;
-      s_red[(D + 2) * (kBlock + 1) + tid] = fin ? J : 0.0f;
-      s_red[(D + 3) * (kBlock + 1) + tid] = fin ? 1.0f : 0.0f;
+      s_red[(D + 0) * kRedStride + tid] = w;
+      s_red[(D + 1) * kRedStride + tid] = w * w;
+      s_red[(D + 2) * kRedStride + tid] = fin ? J : 0.0f;
+      s_red[(D + 3) * kRedStride + tid] = fin ? 1.0f : 0.0f;
       __syncthreads();
     }
     const float mr = SPLIT ? h_m : s_rm[par];
@@ -1582,39 +1497,18 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, (rollou
       float v;
       if (SPLIT) {
         v = (s_red[0 * NR + tid] + s_red[1 * NR + tid]) + (s_red[2 * NR + tid] + s_red[3 * NR + tid]);
-      } else if (TSM) {  // row tid of the tile: w theta[d] from the theta rows, or a weight row
-        const float* s_w = s_th + kBlock * kTsStride;
-        float a0 = 0.f, a1 = 0.f;
-        if (tid < D) {
-          const int64_t left = p.K_local - (int64_t)tile * TS;
-          const int nv = left >= kBlock ? kBlock : (int)left;
-          const float* col = s_th + ts_slot(tid);
-          int i = 0;
-          for (; i + 1 < nv; i += 2) {
-            a0 = fmaf(s_w[i], col[i * kTsStride], a0);
-            a1 = fmaf(s_w[i + 1], col[(i + 1) * kTsStride], a1);
-          }
-          if (i < nv) a0 = fmaf(s_w[i], col[i * kTsStride], a0);
-        } else {
-          const float* rw = s_w + (tid - D) * kBlock;
-#pragma unroll 8
-          for (int i = 0; i < kBlock; i += 2) {
-            a0 += rw[i];
-            a1 += rw[i + 1];
-          }
-        }
-        v = a0 + a1;
       } else {
-        const float* rowp = &s_red[tid * (kBlock + 1)];
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        // row tid: 16-byte loads (kRedStride keeps rows aligned and 8 consecutive rows on
+        // distinct banks), two packed accumulators
+        const float4* rowp = reinterpret_cast<const float4*>(&s_red[tid * kRedStride]);
+        float2 a01 = f2(0.f, 0.f), a23 = f2(0.f, 0.f);
 #pragma unroll 8
-        for (int i = 0; i < kBlock; i += 4) {
-          a0 += rowp[i];
-          a1 += rowp[i + 1];
-          a2 += rowp[i + 2];
-          a3 += rowp[i + 3];
+        for (int i = 0; i < kBlock / 4; ++i) {
+          const float4 q = rowp[i];
+          a01 = fadd2(a01, f2(q.x, q.y));
+          a23 = fadd2(a23, f2(q.z, q.w));
         }
-        v = (a0 + a1) + (a2 + a3);
+        v = (a01.x + a01.y) + (a23.x + a23.y);
       }
       const float sa = (mr < kInf) ? __expf((mn - mr) * p.inv_lambda) : 0.0f;
       const float sb = (mt < kInf) ? __expf((mn - mt) * p.inv_lambda) : 0.0f;
@@ -1664,11 +1558,11 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, (rollou
     if (arrive_last(p.counter + r, gridDim.x)) {
       SBS_TS(5);
       if (p.emit) {  // world > 1: this rank's record per robot (the exchange and rank-order merge follow)
-        if (EPI == EPI_MPPI) mppi_merge_block<true>(p, r, p.emit, s_red, NR * (kBlock + 1));
+        if (EPI == EPI_MPPI) mppi_merge_block<true>(p, r, p.emit, s_red, NR * kRedStride);
         else merge_diag(p, r, p.emit + (size_t)r * p.ex_stride, true);
         publish_to_peers(p);
       } else {
-        if (EPI == EPI_MPPI) mppi_merge_block<false>(p, r, nullptr, s_red, NR * (kBlock + 1));
+        if (EPI == EPI_MPPI) mppi_merge_block<false>(p, r, nullptr, s_red, NR * kRedStride);
         else naive_finalize_block<P>(p, r, s);
       }
       SBS_TS(6);
@@ -2426,8 +2320,7 @@ struct PEntry {
 template <int P, int EPI, bool FC, bool SPLIT>
 constexpr size_t rollout_smem() {
   constexpr int D = 12 * P;
-  if (rollout_tsm<P, FC, SPLIT>()) return (size_t)kBlock * kTsStride * sizeof(float) + (EPI == EPI_MPPI ? 4 * kBlock * sizeof(float) : 0);
-  return (EPI == EPI_MPPI ? (size_t)(D + 4) * (kBlock + 1) * sizeof(float) : (FC ? (size_t)D * D * sizeof(float) : 0)) +
+  return (EPI == EPI_MPPI ? (size_t)(D + 4) * kRedStride * sizeof(float) : (FC ? (size_t)D * D * sizeof(float) : 0)) +
          (SPLIT ? (size_t)kBlock * (D + 2) * sizeof(float) : 0);
 }
 
