@@ -2,21 +2,26 @@
 """Benchmark of one SBS MPC iteration (arxiv 2403.11383) on B200.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sbs|reference]
+                  [--exchange peer|nccl] [--scaling strong|weak]
 
-Workload at N = 1: BASELINE.json configs[1] -- MPPI at the paper's settings,
-K = 10,000 samples, H = 12, dt = 0.02 s, fixed trot.  With N > 1
-(torchrun, one process per GPU) every rank owns 10,000 samples of one
-K = 10,000 N MPPI iteration (weak scaling): the ranks' (min, sum w, sum w theta)
-records are exchanged over peer memory (each rank's finishing CTA stores its
-record into every peer's buffer over NVLink; the peers' streams wait on a flag)
-with an NCCL all-gather as the fallback.
+Headline workload: BASELINE.json configs[3], the large-batch MPPI iteration, at
+K = 2^22 samples, H = 12, dt = 0.02 s, fixed trot (the largest single-GPU config;
+SURVEY 8(d1)).  With N > 1 (torchrun, one process per GPU) the same K = 2^22
+samples are sharded over the N ranks (strong scaling; `--scaling weak` keeps
+2^22 samples per GPU instead); the ranks' (min, sum w, sum w theta) records are
+exchanged over peer memory (each rank's finishing CTA stores its record into
+every peer's buffer over NVLink; the peers' streams wait on a flag), or with one
+NCCL all-gather (`--exchange nccl`).
 
-One JSON line on rank 0.  `value` = sample-steps/s (K_total H / device time
-per iteration, inputs resident in HBM, L2 flushed between timed iterations);
-`e2e` = the same metric through the public host API (sbs_set_reference +
-sbs_step with host buffers, host clock).  `--impl reference` times the CPU
-oracle (the reference arm of this tier) on a bounded sample of the same
-workload.
+One JSON line on rank 0.  `value` = sample-steps/s (K_total H / device time per
+iteration, inputs resident in HBM, L2 flushed between timed iterations, max over
+ranks); `e2e` = the same metric through the public host API (sbs_set_reference +
+sbs_step with host buffers, host clock); `latency` = config 2 (BASELINE.json
+configs[1], K = 10,000, the paper's settings) per-iteration device time and e2e;
+`roofline` = the fused rollout kernel against the FP32 ALU peak, with the
+algorithmic FLOPs per sample-step from the oracle's op-counting mode.
+`--impl reference` times the CPU oracle (the reference arm of this tier) on a
+bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -32,7 +37,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-K_PER_GPU = 10000
+K_HEADLINE = 1 << 22          # BASELINE configs[3] at its largest single-GPU size
+K_LATENCY = 10000             # BASELINE configs[1]
 H = 12
 # Algorithmic FLOPs per sample-step, frozen from the oracle's
 # op-counting mode over the config-2 workload (scripts/op_count.py, 256 samples;
@@ -41,21 +47,27 @@ H = 12
 ALG_FLOP_ROLLOUT = 9343.0 / 12.0          # 778.58
 ALG_FLOP_FUSED = 886.1419270833334        # rollout 778.58 + sampling 95.16 + MPPI 12.40
 ALG_FLOP_PER_SAMPLE_STEP = ALG_FLOP_FUSED
+FLOP_BREAKDOWN = {"rollout_a2_a4": ALG_FLOP_ROLLOUT, "sampling_a1": 95.15755208333333, "mppi_a5": 12.401041666666666,
+                  "total": ALG_FLOP_FUSED, "unit": "FLOP per sample-step",
+                  "source": "oracle op-counting mode (oracle/opcount.cpp, scripts/op_count.py), config 2 trot average"}
 # per-kernel CUDA events (for the roofline's kernel time) bracket every PROFILE_EVERY-th
 # timed step, so their own cost stays out of the headline per-iteration time
 PROFILE_EVERY = 10
 FP32_LANES_PER_SM = 128
+METRIC = "sample-steps/sec and MPC-iteration latency (us) at N samples"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10000)
-    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="sbs", choices=["sbs", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=500)
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-other-configs", action="store_true", help="skip the configs 3/4/5 lines (ncu launch lists)")
+    ap.add_argument("--no-other-configs", action="store_true", help="skip the config 2/3/5 lines (ncu launch lists)")
     return ap.parse_args()
 
 
@@ -64,6 +76,23 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
     return rank, world, local
+
+
+def k_total(args, world):
+    return K_HEADLINE * (world if args.scaling == "weak" else 1)
+
+
+def headline_config(args, world, exchange=None):
+    """The `config` dict of the JSON line (shared by both arms, so they compare equal)."""
+    K = k_total(args, world)
+    par = "samples sharded over %d GPU(s)" % world
+    if world > 1:
+        par += ", rank records by " + (exchange or ("NCCL all-gather" if args.exchange == "nccl" else
+                                                   "peer-memory stores (NVLink) + stream flag waits"))
+    return {"workload": "config4: MPPI, K=%d samples, H=12, dt=0.02 s, fixed trot 1.3 Hz, cmd 0.5 m/s "
+                        "(BASELINE.json configs[3], largest single-GPU size)" % K,
+            "K_total": K, "K_per_gpu": K // world, "H": H, "mode": "mppi", "scaling": args.scaling,
+            "parallelism": par, "l2": "flushed between timed iterations (256 MiB memset, outside the events)"}
 
 
 # ---------------------------------------------------------------------------
@@ -115,12 +144,13 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline leg and the reference arm)
 # ---------------------------------------------------------------------------
-def oracle_rate(K_sample: int, n_steps: int, warmup: int = 1):
-    """Time the oracle as it stands (single thread) on K_sample samples of config 2."""
+def oracle_rate(K_sample: int, n_steps: int, warmup: int = 1, workload: str = "config4"):
+    """Time the oracle as it stands (single thread): n_steps iterations of the workload's
+    scenario on K_sample of its samples each.  Returns (sample-steps/s, per-step seconds)."""
     from oracle import Oracle
     from paper_2403_11383_b200 import workloads as W
     orc = Oracle()
-    cfg, inputs = W.config2(K=K_sample)
+    cfg, inputs = (W.config4 if workload == "config4" else W.config2)(K_sample)
     st = W.initial_distribution(cfg)
     for _ in range(warmup):
         orc.step(cfg, 0, inputs[0], st, keep=False)
@@ -129,20 +159,19 @@ def oracle_rate(K_sample: int, n_steps: int, warmup: int = 1):
         t = time.perf_counter()
         orc.step(cfg, 0, inputs[0], st, keep=False)
         times.append(time.perf_counter() - t)
-    tot = sum(times)
-    return K_sample * H * n_steps / tot, times
+    return K_sample * H * n_steps / sum(times), times
 
 
 def _oracle_worker(args):
     K_sample, n_steps = args
-    rate, times = oracle_rate(K_sample, n_steps, warmup=0)
+    _, times = oracle_rate(K_sample, n_steps, warmup=0)
     return K_sample * H * n_steps, sum(times)
 
 
 def oracle_rate_all_cores(K_sample: int, n_steps: int):
-    """The same oracle iteration run concurrently in one process per host core (each on its
-    own K_sample-sample slice-sized iteration): the oracle as it stands, parallelised by the
-    harness only.  Returns (sample-steps/s over the wall time, processes)."""
+    """The same oracle iteration run concurrently in one process per host core (the oracle
+    as it stands, parallelised by the harness only).  Returns (sample-steps/s over the wall
+    time, processes)."""
     import multiprocessing as mp
     n = os.cpu_count() or 1
     ctx = mp.get_context("fork")
@@ -157,22 +186,21 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    # each step: a bounded sample of the config-2 iteration sized so the whole run takes ~1-3 minutes
+    # each step: a bounded sample of the config-4 iteration sized so the whole run takes ~1-3 minutes
     budget_s = 120.0
-    per_sample_step_s = 2.0e-6
+    per_sample_step_s = 0.6e-6
     n = max(args.steps + args.warmup, 1)
-    K_s = int(max(64, min(K_PER_GPU, budget_s / (n * H * per_sample_step_s))))
+    K_s = int(max(64, min(65536, budget_s / (n * H * per_sample_step_s))))
     value, times = oracle_rate(K_s, args.steps, warmup=args.warmup)
     ms = 1e3 * sum(times) / len(times)
     line = {
-        "impl": "reference", "metric": "sample-steps/sec and MPC-iteration latency (us) at N samples",
-        "value": value, "unit": "sample-steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": "config2: MPPI, K=10000 samples, H=12, dt=0.02 s, fixed trot 1.3 Hz, cmd 0.5 m/s",
-                   "K_per_step": K_s, "H": H},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "sample-steps/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": headline_config(args, world),
         "cpu_baseline": {"value": value, "unit": "sample-steps/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{K_s} of the 10000 samples per step (same iteration), {args.steps} steps"},
+                         "sample": f"{K_s} of the {k_total(args, world)} samples of the config-4 iteration per "
+                                   f"step (same scenario and seeds), {args.steps} steps, single thread"},
         "e2e": {"value": value, "unit": "sample-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -182,6 +210,32 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def _device_inputs(B, C, np, torch, inputs):
+    R = len(inputs)
+    d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
+    d_out = torch.zeros(R * C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+    return d_in, d_out
+
+
+def _peer_connect(ctrl, dist, world):
+    """Trade the exchange buffers' IPC handles; every rank must end on the same exchange."""
+    ok, why = True, ""
+    try:
+        handle, _ = ctrl.peer_handle()
+        handles = [None] * world
+        dist.all_gather_object(handles, handle)
+        ctrl.peer_connect(handles=handles)
+    except Exception as exc:  # noqa: BLE001
+        ok, why = False, str(exc)[:80]
+    oks = [None] * world
+    dist.all_gather_object(oks, ok)
+    if all(oks):
+        return "peer-memory stores (NVLink) + stream flag waits"
+    if ok:
+        ctrl.peer_connect()  # disconnect
+    return f"NCCL all-gather (peer exchange unavailable on some rank: {why})"
+
+
 def run_sbs(args):
     import ctypes as C
 
@@ -197,6 +251,8 @@ def run_sbs(args):
     assert world == args.gpus or world == 1, "launch N > 1 with torchrun --nproc-per-node N"
     torch.cuda.set_device(local)
     if world > 1:
+        if args.exchange == "nccl" and rank == 0:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # the communicator lines go to stderr
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if rank == 0:
         build.build()
@@ -204,8 +260,8 @@ def run_sbs(args):
         dist.barrier()
     B.load_library()
 
-    K_total = K_PER_GPU * world
-    cfg, inputs = W.config2(K=K_total)
+    K = k_total(args, world)
+    cfg, inputs = W.config4(K)
     nccl_id = None
     if world > 1:
         obj = [B.nccl_unique_id() if rank == 0 else None]
@@ -213,30 +269,12 @@ def run_sbs(args):
         nccl_id = obj[0]
     ctrl = B.Controller(cfg, device=local, rank=rank, world=world, nccl_id=nccl_id)
     ctrl.set_reference(0, inputs[0]["xref"])
-    exchange = "none"
+    exchange = "none (one GPU)"
     if world > 1:
-        # rank records exchanged over peer memory (the finishing CTA stores into every peer's
-        # buffer over NVLink; streams wait on the peers' flags); NCCL all-gather as fallback
-        ok, why = True, ""
-        try:
-            handle, _ = ctrl.peer_handle()
-            handles = [None] * world
-            dist.all_gather_object(handles, handle)
-            ctrl.peer_connect(handles=handles)
-        except Exception as exc:  # noqa: BLE001
-            ok, why = False, str(exc)[:80]
-        oks = [None] * world
-        dist.all_gather_object(oks, ok)  # every rank must use the same exchange
-        if all(oks):
-            exchange = "peer memory (NVLink stores + stream flag waits)"
-        else:
-            if ok:
-                ctrl.peer_connect()  # disconnect
-            exchange = f"NCCL all-gather (peer exchange unavailable on some rank: {why})"
+        exchange = _peer_connect(ctrl, dist, world) if args.exchange == "peer" else \
+            "NCCL all-gather (ncclAllGather of the rank records on the context's stream)"
         dist.barrier()
-    in_arr = B.make_inputs(inputs)
-    d_in = torch.from_numpy(np.frombuffer(bytes(in_arr), dtype=np.uint8).copy()).cuda()
-    d_out = torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+    d_in, d_out = _device_inputs(B, C, np, torch, inputs)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
@@ -244,7 +282,7 @@ def run_sbs(args):
     def step():
         ctrl.step_device(d_in.data_ptr(), d_out.data_ptr(), sp)
 
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 3)):
         flush.zero_()
         step()
     torch.cuda.synchronize()
@@ -274,23 +312,32 @@ def run_sbs(args):
     clk = clocks.stop()
     per = [a.elapsed_time(b) for a, b in ev]  # ms
     tot = sum(per)
+    r_ms, r_n = ktimes["rollout"]
+    r_avg_s = (r_ms / max(r_n, 1)) * 1e-3
+    rank_times = None
     if world > 1:
         t = torch.tensor([tot], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot = float(t.item())
+        tot_max = float(t.item())
+        mine = torch.tensor([tot / args.steps * 1e3, r_avg_s * 1e6], dtype=torch.float64, device="cuda")
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        rank_times = [{"rank": i, "us_per_step": float(x[0]), "rollout_kernel_us": float(x[1]),
+                       "exchange_and_merge_us": float(x[0] - x[1])} for i, x in enumerate(allr)]
+        tot = tot_max
     ms = tot / args.steps
-    value = K_total * H / (ms * 1e-3)
+    value = K * H / (ms * 1e-3)
     per_sorted = sorted(per)
+
     def pct(q):
         return 1e3 * per_sorted[min(len(per) - 1, int(q * len(per)))]
 
     lat = {"p5": pct(0.05), "p50": pct(0.5), "p95": pct(0.95), "p99": pct(0.99), "mean": 1e3 * ms,
            "note": "per-iteration device time, L2 flushed before each; every 10th step carries per-kernel events"}
 
-    # ---- roofline of the dominant kernel (rollout), timed live in the same region ----
-    r_ms, r_n = ktimes["rollout"]
-    r_avg_s = (r_ms / max(r_n, 1)) * 1e-3
-    flops = ALG_FLOP_PER_SAMPLE_STEP * K_PER_GPU * H
+    # ---- roofline of the dominant kernel (the fused rollout), timed live in the same region ----
+    K_local = K // world
+    flops = ALG_FLOP_FUSED * K_local * H
     achieved = flops / r_avg_s / 1e12
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -300,79 +347,52 @@ def run_sbs(args):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("rollout_config2_bytes_per_launch")
+        traffic = json.load(open(tpath)).get("rollout_config4_bytes_per_launch")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "sbs_rollout_kernel<4,MPPI,fused>",
+            "traffic": traffic, "kernel": "sbs_rollout_kernel<4,MPPI,fused,...,model> (sampling + rollout + MPPI)",
             "kernel_us": r_avg_s * 1e6, "kernel_share_of_step": (r_avg_s * 1e3) / ms,
-            "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz (clocks.max.sm)",
-            "flop_per_sample_step": ALG_FLOP_PER_SAMPLE_STEP}
+            "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz (clocks.max.sm, "
+                          "MEASURED_PEAKS.json); derived from the profiling guide's unit counts",
+            "flop_per_sample_step": FLOP_BREAKDOWN, "units_per_launch": f"{K_local} samples x {H} steps",
+            "traffic_note": "dram__bytes_read + dram__bytes_write of one launch (ncu --set full, profiles/)"}
 
-    # ---- e2e: public host API (host buffers), host clock ----
-    out_arr = (B.sbs_output * 1)()
-    xref = np.ascontiguousarray(inputs[0]["xref"], dtype=np.float32)
-    for _ in range(10):
-        ctrl.set_reference(0, xref)
-        ctrl.step_raw(in_arr, out_arr)
-    if world > 1:
-        dist.barrier()
-    host_times = []
-    for _ in range(args.e2e_steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        ctrl.set_reference(0, xref)
-        ctrl.step_raw(in_arr, out_arr)
-        host_times.append(time.perf_counter() - t)
-    e2e_s = sum(host_times)
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_ms = 1e3 * e2e_s / args.e2e_steps
-    h2d = C.sizeof(B.sbs_input) + xref.nbytes
-    d2h = C.sizeof(B.sbs_output)
-    e2e = {"value": K_total * H / (e2e_ms * 1e-3), "unit": "sample-steps/s", "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-           "api": "sbs_set_reference + sbs_step (host buffers, synchronous)"}
+    # ---- e2e: public host API (host buffers), host clock, same workload ----
+    e2e = _e2e(ctrl, B, np, torch, inputs, flush, args.e2e_steps, world, dist, K)
 
-    # ---- the other BASELINE configs on this GPU (rank 0, N = 1): where the ALU roofline is
-    #      meaningful (config 4 at K = 2^22) and the CEM iteration (config 3) ----
+    line = None
     extra = None
+    latency = None
     if world == 1 and not args.no_other_configs:
-        extra = {"config4_K4M": _time_config(B, W, C, np, torch, W.config4(4194304), steps=20, warmup=3,
-                                             peak=peak, label="config4: MPPI, K=2^22, H=12 (BASELINE configs[3], 1 GPU)"),
-                 "config3_cem": _time_config(B, W, C, np, torch, W.config3("cem"), steps=200, warmup=10,
-                                             peak=peak, label="config3: CEM K_e=1000, K=10000, gait adaptation"),
+        latency = _latency_config2(B, W, C, np, torch, flush, args)
+        extra = {"config3_cem": _time_config(B, W, C, np, torch, W.config3("cem"), steps=200, warmup=10, peak=peak,
+                                             label="config3: CEM K_e=1000, K=10000, gait adaptation"),
                  "config5_batched": _time_config(B, W, C, np, torch, W.config5(), steps=20, warmup=3, peak=peak,
                                                  label="config5: 4096 robots x 1024 samples, MPPI (1 GPU)"),
                  "config5_closed_loop": _time_closed_loop(B, W, C, np, torch, W.config5(), n_iter=50)}
-
-    line = None
+    elif world > 1 and not args.no_other_configs:
+        extra = {"config5_robot_sharded": _config5_sharded(B, W, C, np, torch, dist, rank, world, local, flush)}
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
-            K_s = 2000
-            cv, ctimes = oracle_rate(K_s, n_steps=max(1, int(12.0 / (K_s * H * 2.3e-6))))
+            K_s = 16384
+            cv, ctimes = oracle_rate(K_s, n_steps=max(1, int(15.0 / (K_s * H * 0.6e-6))))
             cpu = {"value": cv, "unit": "sample-steps/s", "cores": 1, "kind": "oracle",
-                   "sample": f"{len(ctimes)} oracle iterations of config 2 on {K_s} of its 10000 samples "
+                   "sample": f"{len(ctimes)} oracle iterations of the config-4 scenario on {K_s} of its {K} samples "
                              f"({sum(ctimes):.1f} s, single thread)"}
             try:  # the same oracle on every host core (one process each), for context
-                av, ncores = oracle_rate_all_cores(2000, 150)
+                av, ncores = oracle_rate_all_cores(4096, 10)
                 cpu["all_cores"] = {"value": av, "unit": "sample-steps/s", "cores": ncores,
-                                    "sample": f"{ncores} processes x 150 oracle iterations of config 2 on 2000 samples (wall clock incl. process start)"}
+                                    "sample": f"{ncores} processes x 10 oracle iterations of the config-4 scenario on "
+                                              "4096 samples (wall clock incl. process start)"}
             except Exception as exc:  # noqa: BLE001
                 cpu["all_cores"] = {"error": str(exc)[:200]}
         line = {
-            "metric": "sample-steps/sec and MPC-iteration latency (us) at N samples",
-            "value": value, "unit": "sample-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "latency_us": lat, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "config2: MPPI, K=10000 samples per GPU, H=12, dt=0.02 s, fixed trot 1.3 Hz, "
-                                   "cmd 0.5 m/s (BASELINE.json configs[1])",
-                       "K_total": K_total, "K_per_gpu": K_PER_GPU, "H": H, "mode": "mppi",
-                       "parallelism": f"samples sharded over {world} GPU(s)" + (f", rank records by {exchange}" if world > 1 else ""),
-                       "l2": "flushed between timed iterations (256 MiB memset, outside the events)"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "other_configs": extra,
+            "metric": METRIC, "value": value, "unit": "sample-steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "latency_us": lat, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": headline_config(args, world, exchange if world > 1 else None),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "latency": latency, "exchange": exchange,
+            "per_rank": rank_times, "other_configs": extra,
             "gpu_launches": int(ctrl.launches_per_step() * args.steps), "clocks": clk,
         }
         print(json.dumps(line), flush=True)
@@ -383,6 +403,69 @@ def run_sbs(args):
     return 0
 
 
+def _e2e(ctrl, B, np, torch, inputs, flush, n, world, dist, K):
+    """sbs_set_reference + sbs_step with host buffers (inputs copied up, outputs read back
+    every step), host clock, max over ranks."""
+    out_arr = (B.sbs_output * 1)()
+    in_arr = B.make_inputs(inputs)
+    xref = np.ascontiguousarray(inputs[0]["xref"], dtype=np.float32)
+    for _ in range(5):
+        ctrl.set_reference(0, xref)
+        ctrl.step_raw(in_arr, out_arr)
+    if world > 1:
+        dist.barrier()
+    times = []
+    for _ in range(n):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        ctrl.set_reference(0, xref)
+        ctrl.step_raw(in_arr, out_arr)
+        times.append(time.perf_counter() - t)
+    e2e_s = sum(times)
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_ms = 1e3 * e2e_s / n
+    import ctypes as C
+    return {"value": K * H / (e2e_ms * 1e-3), "unit": "sample-steps/s",
+            "h2d_bytes_per_step": C.sizeof(B.sbs_input) + xref.nbytes, "d2h_bytes_per_step": C.sizeof(B.sbs_output),
+            "ms_per_step": e2e_ms, "api": "sbs_set_reference + sbs_step (host buffers, synchronous), host clock"}
+
+
+def _latency_config2(B, W, C, np, torch, flush, args):
+    """Config 2 (the paper's settings, K = 10,000): per-iteration device latency with the
+    L2 flushed before each, and the same through sbs_set_reference + sbs_step."""
+    cfg, inputs = W.config2(K_LATENCY)
+    ctrl = B.Controller(cfg)
+    ctrl.set_reference(0, inputs[0]["xref"])
+    d_in, d_out = _device_inputs(B, C, np, torch, inputs)
+    s = torch.cuda.current_stream()
+    for _ in range(20):
+        ctrl.step_device(d_in.data_ptr(), d_out.data_ptr(), s.cuda_stream)
+    n = 1000
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    torch.cuda.synchronize()
+    for e0, e1 in ev:
+        flush.zero_()
+        e0.record(s)
+        ctrl.step_device(d_in.data_ptr(), d_out.data_ptr(), s.cuda_stream)
+        e1.record(s)
+    torch.cuda.synchronize()
+    us = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
+    e2e = _e2e(ctrl, B, np, torch, inputs, flush, 500, 1, None, K_LATENCY)
+    ctrl.close()
+    mean = sum(us) / n
+    return {"workload": "config2: MPPI, K=10000, H=12, dt=0.02 s, fixed trot, cmd 0.5 m/s (BASELINE.json configs[1])",
+            "us_per_iteration": {"p5": us[n // 20], "p50": us[n // 2], "p95": us[19 * n // 20], "p99": us[99 * n // 100],
+                                 "mean": mean},
+            "value": K_LATENCY * H / (mean * 1e-6), "unit": "sample-steps/s",
+            "e2e_us": e2e["ms_per_step"] * 1e3, "e2e": e2e,
+            "timing": "1000 isolated iterations, L2 flushed before each, CUDA events; e2e: host clock around "
+                      "sbs_set_reference + sbs_step"}
+
+
 def _time_config(B, W, C, np, torch, cfg_inputs, steps, warmup, peak, label):
     """Device time per iteration of another BASELINE config (inputs resident, L2 flushed
     between iterations), with the rollout kernel's live roofline fraction."""
@@ -391,8 +474,7 @@ def _time_config(B, W, C, np, torch, cfg_inputs, steps, warmup, peak, label):
     ctrl = B.Controller(cfg)
     for r, inp in enumerate(inputs):
         ctrl.set_reference(r, inp["xref"])
-    d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
-    d_out = torch.zeros(R * C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+    d_in, d_out = _device_inputs(B, C, np, torch, inputs)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for _ in range(warmup):
@@ -418,7 +500,7 @@ def _time_config(B, W, C, np, torch, cfg_inputs, steps, warmup, peak, label):
     K = cfg["n_samples"] * R
     r_ms, r_n = kt["rollout"]
     r_s = r_ms / max(r_n, 1) * 1e-3
-    achieved = ALG_FLOP_PER_SAMPLE_STEP * K * H / r_s / 1e12
+    achieved = ALG_FLOP_FUSED * K * H / r_s / 1e12
     ctrl.close()
     return {"workload": label, "K_total": K, "steps": steps, "ms_per_step": ms,
             "timing": "L2 flushed before every step; ms_per_step over the odd steps, kernels_us from the even "
@@ -437,8 +519,7 @@ def _time_closed_loop(B, W, C, np, torch, cfg_inputs, n_iter):
     ctrl = B.Controller(cfg)
     for r, inp in enumerate(inputs):
         ctrl.set_reference(r, inp["xref"])
-    d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
-    d_out = torch.zeros(R * C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+    d_in, d_out = _device_inputs(B, C, np, torch, inputs)
     fallen = torch.zeros(R, dtype=torch.int32, device="cuda")
     lc = W.loop_config()
     s = torch.cuda.current_stream()
@@ -458,6 +539,42 @@ def _time_closed_loop(B, W, C, np, torch, cfg_inputs, n_iter):
             "K_total": K, "control_steps": n_iter, "ms_per_control_step": ms,
             "value": K * H / (ms * 1e-3), "unit": "sample-steps/s",
             "robot_control_steps_per_s": R / (ms * 1e-3), "fallen": n_fallen}
+
+
+def _config5_sharded(B, W, C, np, torch, dist, rank, world, local, flush, steps=20):
+    """Config 5 sharded by robot (BASELINE configs[4]): rank g owns robots
+    [g R/N, (g+1) R/N) through `robot_offset` (the noise counter carries the global robot
+    index, so every robot draws the same samples as in one context); no collective."""
+    cfg, inputs = W.config5()
+    R = len(inputs)
+    R_loc = R // world
+    lo = rank * R_loc
+    mine = inputs[lo:lo + R_loc]
+    cfg = dict(cfg, n_robots=R_loc)
+    ctrl = B.Controller(cfg, device=local, robot_offset=lo)
+    for r, inp in enumerate(mine):
+        ctrl.set_reference(r, inp["xref"])
+    d_in, d_out = _device_inputs(B, C, np, torch, mine)
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        ctrl.step_device(d_in.data_ptr(), d_out.data_ptr(), s.cuda_stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    for e0, e1 in ev:
+        flush.zero_()
+        e0.record(s)
+        ctrl.step_device(d_in.data_ptr(), d_out.data_ptr(), s.cuda_stream)
+        e1.record(s)
+    torch.cuda.synchronize()
+    tot = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = float(tot.item()) / steps
+    ctrl.close()
+    K = cfg["n_samples"] * R
+    return {"workload": f"config5: {R} robots x 1024 samples, MPPI, {R_loc} robots per GPU via robot_offset "
+                        "(no collective)", "K_total": K, "ms_per_step": ms, "value": K * H / (ms * 1e-3),
+            "unit": "sample-steps/s", "scaling": "strong", "timing": "max over ranks, L2 flushed before each step"}
 
 
 def main():
