@@ -324,6 +324,17 @@ int sbs_debug_elites(sbs_ctx* ctx, int32_t robot, int64_t* idx);
 /* Stand-alone elite selection (the K_e smallest of J by (J, k); NaN as +inf)
  * on device `device`; host J[K] in, host idx[K_e] out (ascending). */
 int sbs_debug_select(const float* J, int64_t K, int64_t K_e, int64_t* idx, int32_t device);
+/* The normative binary32 noise recipe (O3-O4; "theta_k ~ N(theta, C)")
+ * applied to given Philox output words on device `device`: host words[n][4] in (one Philox
+ * block each: Box-Muller pairs (w0, w1) and (w2, w3)), host z[n][4] out, in the order the
+ * sampler uses (z0 = r cos, z1 = r sin of the first pair, then the second pair).  n <= 2^28.
+ * Tests only (exhaustive recipe checks); no context needed. */
+int sbs_debug_noise(const uint32_t* words, int64_t n, float* z, int32_t device);
+/* Philox4x32-10 (O1) on given counters ctr[n][4] and keys key[n][2] on device `device`:
+ * ours[n][2][4] = the library's plain and round-key forms, curand_words[n][4] = cuRAND's
+ * curand_Philox4x32_10 of the same inputs.  n <= 2^26.  Tests only. */
+int sbs_debug_philox(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* ours, uint32_t* curand_words,
+                     int32_t device);
 /* Slice [k_begin, k_begin + K_local) of the samples owned by this rank. */
 int sbs_local_range(const sbs_ctx* ctx, int64_t* k_begin, int64_t* K_local);
 /* Per-kernel CUDA-event timing (enable = 1 records events around every launch). */

@@ -178,6 +178,7 @@ class Oracle:
         L.orc_ln_u24.restype = C.c_float
         L.orc_sincos_2pi_u.argtypes = [C.c_uint32, C.POINTER(C.c_float), C.POINTER(C.c_float)]
         L.orc_normal4.argtypes = [u32p, C.POINTER(C.c_float)]
+        L.orc_normal4_batch.argtypes = [u32p, C.c_int64, C.POINTER(C.c_float)]
         L.orc_sample.argtypes = [cfgp, dp, dp, C.c_int32, C.c_uint32, C.c_uint32, C.c_int64,
                                  dp, C.POINTER(C.c_float), i32p]
         L.orc_warm_shift.argtypes = [cfgp, dp, dp]
@@ -234,6 +235,14 @@ class Oracle:
         z = (C.c_float * 4)()
         self.lib.orc_normal4(ww, z)
         return np.array(z, dtype=np.float32)
+
+    def normal4_batch(self, words):
+        """orc_normal4 over [n][4] Philox words: z [n][4] (float32)."""
+        w = np.ascontiguousarray(np.asarray(words, dtype=np.uint32).reshape(-1, 4))
+        z = np.zeros(w.shape, dtype=np.float32)
+        self.lib.orc_normal4_batch(w.ctypes.data_as(C.POINTER(C.c_uint32)), w.shape[0],
+                                   z.ctypes.data_as(C.POINTER(C.c_float)))
+        return z
 
     def sample(self, cfg, mu_shift, var, cur_idx, it, robot, k):
         c = make_config(cfg)

@@ -140,6 +140,11 @@ void orc_normal4(const uint32_t w[4], float z[4]) {
   }
 }
 
+/* orc_normal4 over n Philox blocks (tests: exhaustive recipe comparisons). */
+void orc_normal4_batch(const uint32_t* w, int64_t n, float* z) {
+  for (int64_t i = 0; i < n; ++i) orc_normal4(&w[4 * i], &z[4 * i]);
+}
+
 /* ======================================================================
  * a0  Warm start ("initiating each new search from the solution
  * obtained in the previous iteration"; reading L20): the previous mean's

@@ -67,6 +67,7 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
 float orc_ln_u24(uint32_t w);                   /* ln(u1), u1 = (2(w>>9)+1) 2^-24  */
 void orc_sincos_2pi_u(uint32_t w, float* s, float* c); /* sin/cos(2 pi u2)        */
 void orc_normal4(const uint32_t w[4], float z[4]);      /* Box-Muller, 2 pairs     */
+void orc_normal4_batch(const uint32_t* w /*[n][4]*/, int64_t n, float* z /*[n][4]*/);
 
 /* ---- O5-O6: one sample theta_k = [theta1, theta2] ---- */
 void orc_sample(const orc_config* c, const double* mu_shift, const double* var,

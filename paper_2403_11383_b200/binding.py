@@ -120,6 +120,9 @@ def load_library(path: str = LIB_PATH):
         "sbs_debug_elites": ([ctxp, C.c_int32, P(C.c_int64)], C.c_int),
         "sbs_debug_select": ([P(C.c_float), C.c_int64, C.c_int64, P(C.c_int64), C.c_int32], C.c_int),
         "sbs_local_range": ([ctxp, P(C.c_int64), P(C.c_int64)], C.c_int),
+        "sbs_debug_noise": ([P(C.c_uint32), C.c_int64, P(C.c_float), C.c_int32], C.c_int),
+        "sbs_debug_philox": ([P(C.c_uint32), P(C.c_uint32), C.c_int64, P(C.c_uint32), P(C.c_uint32), C.c_int32],
+                             C.c_int),
         "sbs_profile": ([ctxp, C.c_int32], C.c_int),
         "sbs_kernel_times": ([ctxp, P(C.c_double), P(C.c_int64)], C.c_int),
         "sbs_launches_per_step": ([ctxp], C.c_int),
@@ -401,6 +404,33 @@ def debug_select(J, K_e: int, device: int = 0):
     if st < 0:
         raise SBSError(st, (L.sbs_last_error(None) or b"").decode())
     return idx
+
+
+def debug_noise(words, device: int = 0):
+    """The noise recipe on given Philox words [n][4] (uint32) on the GPU: z [n][4] (float32)."""
+    L = load_library()
+    w = np.ascontiguousarray(np.asarray(words, dtype=np.uint32).reshape(-1, 4))
+    z = np.zeros(w.shape, dtype=np.float32)
+    st = L.sbs_debug_noise(w.ctypes.data_as(C.POINTER(C.c_uint32)), w.shape[0], _fp(z), device)
+    if st < 0:
+        raise SBSError(st, (L.sbs_last_error(None) or b"").decode())
+    return z
+
+
+def debug_philox(ctr, key, device: int = 0):
+    """Philox4x32-10 on the GPU for counters [n][4] and keys [n][2]: (ours [n][2][4], cuRAND's [n][4])."""
+    L = load_library()
+    c = np.ascontiguousarray(np.asarray(ctr, dtype=np.uint32).reshape(-1, 4))
+    k = np.ascontiguousarray(np.asarray(key, dtype=np.uint32).reshape(-1, 2))
+    n = c.shape[0]
+    ours = np.zeros((n, 2, 4), dtype=np.uint32)
+    cur = np.zeros((n, 4), dtype=np.uint32)
+    u32p = C.POINTER(C.c_uint32)
+    st = L.sbs_debug_philox(c.ctypes.data_as(u32p), k.ctypes.data_as(u32p), n, ours.ctypes.data_as(u32p),
+                            cur.ctypes.data_as(u32p), device)
+    if st < 0:
+        raise SBSError(st, (L.sbs_last_error(None) or b"").decode())
+    return ours, cur
 
 
 def nccl_unique_id() -> bytes:

@@ -1397,6 +1397,53 @@ int sbs_debug_select(const float* J, int64_t K, int64_t K_e, int64_t* idx, int32
   return SBS_OK;
 }
 
+extern "C++" {
+namespace {
+// host in -> device kernel -> host out, for the stand-alone debug kernels
+template <typename F>
+int debug_roundtrip(int32_t device, const char* what, const std::vector<std::pair<const void*, size_t>>& ins,
+                    const std::vector<std::pair<void*, size_t>>& outs, F launch) {
+  sbs_ctx* c = nullptr;
+  CK(cudaSetDevice(device));
+  std::vector<void*> din(ins.size(), nullptr), dout(outs.size(), nullptr);
+  cudaError_t e = cudaSuccess;
+  for (size_t i = 0; i < ins.size() && e == cudaSuccess; ++i) {
+    e = cudaMalloc(&din[i], ins[i].second);
+    if (e == cudaSuccess) e = cudaMemcpy(din[i], ins[i].first, ins[i].second, cudaMemcpyHostToDevice);
+  }
+  for (size_t i = 0; i < outs.size() && e == cudaSuccess; ++i) e = cudaMalloc(&dout[i], outs[i].second);
+  if (e == cudaSuccess) e = launch(din, dout);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  for (size_t i = 0; i < outs.size() && e == cudaSuccess; ++i)
+    e = cudaMemcpy(outs[i].first, dout[i], outs[i].second, cudaMemcpyDeviceToHost);
+  for (void* p : din) cudaFree(p);
+  for (void* p : dout) cudaFree(p);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, what);
+  return SBS_OK;
+}
+}  // namespace
+}  // extern "C++"
+
+int sbs_debug_noise(const uint32_t* words, int64_t n, float* z, int32_t device) {
+  if (!words || !z || n < 1 || n > (1LL << 28)) return fail(nullptr, SBS_ERR_INVALID_ARG, "bad argument");
+  const size_t b = (size_t)n * 16;
+  return debug_roundtrip(device, "sbs_debug_noise", {{words, b}}, {{z, b}},
+                         [&](std::vector<void*>& i, std::vector<void*>& o) {
+                           return sbs::launch_debug_noise(i[0], n, o[0], 0);
+                         });
+}
+
+int sbs_debug_philox(const uint32_t* ctr, const uint32_t* key, int64_t n, uint32_t* ours, uint32_t* curand_words,
+                     int32_t device) {
+  if (!ctr || !key || !ours || !curand_words || n < 1 || n > (1LL << 26))
+    return fail(nullptr, SBS_ERR_INVALID_ARG, "bad argument");
+  return debug_roundtrip(device, "sbs_debug_philox", {{ctr, (size_t)n * 16}, {key, (size_t)n * 8}},
+                         {{ours, (size_t)n * 32}, {curand_words, (size_t)n * 16}},
+                         [&](std::vector<void*>& i, std::vector<void*>& o) {
+                           return sbs::launch_debug_philox(i[0], i[1], n, o[0], o[1], 0);
+                         });
+}
+
 int sbs_local_range(const sbs_ctx* c, int64_t* k_begin, int64_t* K_local) {
   if (!c || !k_begin || !K_local) return SBS_ERR_INVALID_ARG;
   *k_begin = c->P.k_begin;

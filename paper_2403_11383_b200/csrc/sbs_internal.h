@@ -151,6 +151,11 @@ cudaError_t launch_elite(const Params& p, cudaStream_t s);
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                  int* fidx, cudaStream_t s);
 cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s);
+// tests only: the noise recipe on given Philox words [n][4] -> z [n][4]; Philox on given
+// counters [n] / keys [n] -> ours [n][2] (plain and round-key forms), cuRAND's [n]
+cudaError_t launch_debug_noise(const void* w, int64_t n, void* z, cudaStream_t s);
+cudaError_t launch_debug_philox(const void* ctr, const void* key, int64_t n, void* ours, void* curand_out,
+                                cudaStream_t s);
 int rollout_occupancy(int P, int mode, bool fc = false, bool split = false, bool model = false);
 // kernel attributes (dynamic shared memory limits), once per process and P, never inside a capture
 cudaError_t prepare_kernels(int P);  // resident CTAs per SM of the rollout kernel

@@ -31,6 +31,9 @@
 
 #include "sbs_internal.h"
 #include "sbs_noise.cuh"
+#if defined(SBS_TU_COMMON)
+#include <curand_philox4x32_x.h>  // tests only: cuRAND's Philox4x32-10 next to ours
+#endif
 #include "sbs_robot_model.h"
 
 namespace sbs {
@@ -1961,6 +1964,45 @@ __global__ void __launch_bounds__(kSelBlock) sbs_select_small_raw_kernel(const f
   select_block_small(J, (int)K, (int)K_e, 0, idx, nullptr, sel_smem);
 }
 
+
+// ---- tests only: the normative noise on given Philox words, and the Philox rounds on
+//      given counters / keys next to cuRAND's curand_Philox4x32_10 (same definition) ----
+__global__ void sbs_debug_noise_kernel(const uint4* w, int64_t n, float4* z) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 v = w[i];
+  float o[4];
+  box_muller_x2(U4{v.x, v.y, v.z, v.w}, o);
+  z[i] = make_float4(o[0], o[1], o[2], o[3]);
+}
+__global__ void sbs_debug_philox_kernel(const uint4* ctr, const uint2* key, int64_t n, uint4* ours, uint4* curand_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 c = ctr[i];
+  const uint2 k = key[i];
+  const U4 a = philox4x32_10(c.x, c.y, c.z, c.w, k.x, k.y);
+  uint32_t rk[10][2];
+  for (int r = 0; r < 10; ++r) {
+    rk[r][0] = k.x + (uint32_t)r * 0x9E3779B9u;
+    rk[r][1] = k.y + (uint32_t)r * 0xBB67AE85u;
+  }
+  const U4 b = philox4x32_10_rk(c.x, c.y, c.z, c.w, rk);  // the round-key form the rollout uses
+  ours[2 * i] = make_uint4(a.x, a.y, a.z, a.w);
+  ours[2 * i + 1] = make_uint4(b.x, b.y, b.z, b.w);
+  curand_out[i] = curand_Philox4x32_10(c, k);
+}
+cudaError_t launch_debug_noise(const void* w, int64_t n, void* z, cudaStream_t s) {
+  sbs_debug_noise_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(static_cast<const uint4*>(w), n,
+                                                                       static_cast<float4*>(z));
+  return cudaGetLastError();
+}
+cudaError_t launch_debug_philox(const void* ctr, const void* key, int64_t n, void* ours, void* curand_out,
+                                cudaStream_t s) {
+  sbs_debug_philox_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+      static_cast<const uint4*>(ctr), static_cast<const uint2*>(key), n, static_cast<uint4*>(ours),
+      static_cast<uint4*>(curand_out));
+  return cudaGetLastError();
+}
 #endif  // SBS_TU_COMMON
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,247 @@
+"""GPU parity, second set: the launch shapes and edge cases the first set did not
+reach.
+
+  * the normative noise recipe over every one of its 2^23 radius inputs and 2^23
+    angle inputs, bit for bit against the oracle (O3-O4; "theta_k ~ N(theta, C)");
+  * Philox4x32-10 against cuRAND's curand_Philox4x32_10 on the device (O1);
+  * theta2 within the stated ulp contract;
+  * MPPI at K = 2^16 and 2^18 (more CTA records than the one-pass merge holds: the
+    chunked merge the K = 2^22 bench launch takes) against the oracle (Alg. 4,
+    P:188-201), and the conditioning check of SURVEY 8(c4) over lambda = 1, 10, 100;
+  * yaw near +-pi (the MUFU sincos and the rint wrap against libm and remainder);
+  * CEM with fewer finite costs than elites (Alg. 1; L17, L26);
+  * robot sharding: two contexts with robot_offset = one context of all robots, bitwise.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2403_11383_b200 import workloads as W
+from test_gpu_parity import _check_costs, _check_outputs, _ctrl, _tol_vec
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2403_11383_b200 import binding, build
+    build.build()
+    binding.load_library()
+    return binding
+
+
+# ---------------------------------------------------------------------------
+# O1, O3-O4: noise
+# ---------------------------------------------------------------------------
+def _exhaustive_words(seed=0):
+    """2^22 Philox blocks whose radius words (w0, w2) run through all 2^23 values of
+    w >> 9 and whose angle words (w1, w3) do too (an odd multiplier permutes [0, 2^23));
+    the 9 low bits, which the recipe discards, are random."""
+    n = 1 << 22
+    b = np.arange(n, dtype=np.uint64)
+    low = np.random.default_rng(seed).integers(0, 512, size=(n, 4), dtype=np.uint64)
+    w = np.empty((n, 4), dtype=np.uint32)
+    w[:, 0] = ((2 * b) << 9 | low[:, 0]).astype(np.uint32)
+    w[:, 2] = ((2 * b + 1) << 9 | low[:, 2]).astype(np.uint32)
+    w[:, 1] = ((((2 * b) * 2654435761) % (1 << 23)) << 9 | low[:, 1]).astype(np.uint32)
+    w[:, 3] = ((((2 * b + 1) * 2654435761) % (1 << 23)) << 9 | low[:, 3]).astype(np.uint32)
+    return w
+
+
+def test_noise_recipe_exhaustive(B, orc):
+    w = _exhaustive_words()
+    assert len(np.unique(np.concatenate([w[:, 0], w[:, 2]]) >> 9)) == 1 << 23
+    assert len(np.unique(np.concatenate([w[:, 1], w[:, 3]]) >> 9)) == 1 << 23
+    zg = B.debug_noise(w)
+    zo = orc.normal4_batch(w)
+    bad = np.nonzero(zg.view(np.uint32) != zo.view(np.uint32))
+    assert bad[0].size == 0, f"{bad[0].size} of {zg.size} z differ, first block {bad[0][:4]}"
+    # edge words: all-zero and all-one words in every position
+    edge = np.array([[0, 0, 0, 0], [0xFFFFFFFF] * 4, [0, 0xFFFFFFFF, 0, 0xFFFFFFFF], [0xFFFFFFFF, 0, 0xFFFFFFFF, 0],
+                     [0x1FF, 0x1FF, 0x200, 0x200], [0xFFFFFE00, 0xE0000000, 0x1FFFFFFF, 0x20000000]], dtype=np.uint32)
+    np.testing.assert_array_equal(B.debug_noise(edge).view(np.uint32), orc.normal4_batch(edge).view(np.uint32))
+
+
+def test_philox_matches_curand_and_oracle(B, orc):
+    rng = np.random.default_rng(7)
+    n = 1 << 20
+    ctr = rng.integers(0, 1 << 32, size=(n, 4), dtype=np.uint64).astype(np.uint32)
+    key = rng.integers(0, 1 << 32, size=(n, 2), dtype=np.uint64).astype(np.uint32)
+    ctr[:4] = [[0, 0, 0, 0], [0xFFFFFFFF] * 4, [0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0x80000000, 5, 7, 1]]
+    key[:4] = [[0, 0], [0xFFFFFFFF] * 2, [0xa4093822, 0x299f31d0], [0x40311383, 2]]
+    ours, cur = B.debug_philox(ctr, key)
+    np.testing.assert_array_equal(ours[:, 0], cur)          # plain form == cuRAND
+    np.testing.assert_array_equal(ours[:, 1], cur)          # round-key form == cuRAND
+    for i in list(range(4)) + list(rng.integers(0, n, 200)):
+        np.testing.assert_array_equal(orc.philox(ctr[i], key[i]), cur[i])
+
+
+def _ulp(x):
+    """binary32 ulp of |x| (x > 0): 2^(floor(log2 x) - 23), normal range."""
+    return np.ldexp(1.0, np.floor(np.log2(np.maximum(np.abs(x), np.finfo(np.float32).tiny))).astype(int) - 23)
+
+
+def test_theta2_ulp_contract(B, orc):
+    """theta2 = fma(sqrt(var), z, mu') in binary32 with mu' the binary32 warm shift (L20) of
+    the previous mean: within 4 ulp of the operation's magnitude max(|theta2|, sum_q |WS_pq
+    mean_q|, sigma |z|) of the oracle's binary64 value (the warm shift's
+    dot product rounds on the scale of its terms, not of its result)."""
+    worst = 0.0
+    for it in (0, 1, 7):
+        cfg, inputs = W.config3("cem", K=2000)
+        st = W.initial_distribution(cfg)
+        st["iter"] = it
+        st["mean"] = st["mean"] + np.random.default_rng(it).normal(0, 20, 48)  # a non-constant spline
+        c = _ctrl(B, cfg, inputs, st)
+        z_g, th, _ = c.debug_samples(0, 0, 2000)
+        r = orc.step(cfg, 0, inputs[0], dict(st))
+        D = 48
+        WS = np.stack([orc.warm_shift(cfg, np.eye(D)[q]) for q in range(D)], axis=1)  # mu' = WS mean
+        terms = np.abs(WS) @ np.abs(st["mean"])
+        sig_z = np.sqrt(st["var"])[None, :] * np.abs(r.z)
+        scale = _ulp(np.maximum(np.maximum(np.abs(r.theta), terms[None, :]), sig_z))
+        worst = max(worst, float(np.max(np.abs(th - r.theta) / scale)))
+    assert worst <= 4.0, worst
+
+
+# ---------------------------------------------------------------------------
+# a5 at the chunked-merge launch shape, conditioning
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("K", [1 << 16, 1 << 18])
+def test_mppi_chunked_merge_against_oracle(B, orc, K):
+    cfg, inputs = W.config4(K)
+    st = W.initial_distribution(cfg)
+    c = _ctrl(B, cfg, inputs, st)
+    ro = orc.step(cfg, 0, inputs[0], st)
+    status, outs = c.step(inputs)
+    assert status == ro.status == 0
+    _check_costs(c.debug_costs()[0], ro.J)
+    _check_outputs(outs[0], ro, cfg)
+    assert outs[0]["ess"] == pytest.approx(ro.ess, rel=1e-3)
+
+
+def test_mppi_conditioning_lambda_sweep(B, orc):
+    """kappa = max_k |J_gpu - J_orc| / lambda bounds the weight perturbation,
+    so |mu_gpu - mu_orc| <= kappa max_k ||theta_k - mu_new|| to first order (plus the
+    binary32 rounding of the sums); a larger lambda shrinks kappa and the error."""
+    errs = {}
+    for lam in (1.0, 10.0, 100.0):
+        cfg, inputs = W.config2(K=10000)
+        cfg = dict(cfg, **{"lambda": lam})
+        st = W.initial_distribution(cfg)
+        c = _ctrl(B, cfg, inputs, st)
+        ro = orc.step(cfg, 0, inputs[0], st)
+        _, outs = c.step(inputs)
+        Jg = c.debug_costs()[0].astype(np.float64)
+        kappa = float(np.max(np.abs(Jg - ro.J))) / lam
+        spread = float(np.max(np.abs(ro.theta - ro.mean[None, :])))
+        err = float(np.max(np.abs(outs[0]["mean"] - ro.mean)))
+        assert err <= kappa * spread + 1e-5 * max(float(np.max(np.abs(ro.mean))), 1.0), (lam, err, kappa, spread)
+        errs[lam] = err
+    # the lambda-driven part of the error shrinks; what stays is the binary32 rounding of the sums
+    assert errs[100.0] <= errs[1.0] + 1e-5 * max(float(np.max(np.abs(ro.mean))), 1.0), errs
+
+
+# ---------------------------------------------------------------------------
+# yaw near +-pi
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("yaw0,yaw_ref,wz", [(3.0, 3.05, 1.0), (-3.1, 3.1, -0.5), (3.1, -3.12, 2.0)])
+def test_yaw_near_pi(B, orc, yaw0, yaw_ref, wz):
+    """|yaw| ~ pi in the state and the reference (a yaw rate carries the state across +-pi
+    within the horizon; the reference may sit on the other branch): costs, mean, u0 against
+    the oracle's libm trigonometry and remainder wrap."""
+    cfg, inputs = W.config2(K=4000)
+    inp = dict(inputs[0])
+    x0 = inp["x0"].copy()
+    x0[8] = W.f32(yaw0)
+    x0[11] = W.f32(wz)
+    inp["x0"] = x0
+    xr = inp["xref"].copy()
+    xr[:, 8] = W.f32(yaw_ref)
+    inp["xref"] = xr
+    st = W.initial_distribution(cfg)
+    c = _ctrl(B, cfg, [inp], st)
+    ro = orc.step(cfg, 0, inp, st)
+    _, outs = c.step([inp])
+    _check_costs(c.debug_costs()[0], ro.J)
+    _check_outputs(outs[0], ro, cfg)
+
+
+# ---------------------------------------------------------------------------
+# CEM with most samples diverged
+# ---------------------------------------------------------------------------
+def test_cem_fewer_finite_than_elites(B, orc):
+    """Pitched over with a large pitch rate: ~20 % of the rollouts cross the pitch limit
+    (J = +inf, L26) and K_e exceeds the finite count, so the elite list ends in diverged
+    samples that must not enter the moments (L17).  Near the Euler singularity the binary32
+    and binary64 trajectories separate (L35): there the divergence decision itself can
+    differ, so the update is checked on the GPU's own costs -- the oracle's CEM update
+    (orc_cem_update) on the GPU's J and the oracle's samples -- and the costs on the
+    samples whose oracle trajectory stays 0.12 rad or more from the singularity."""
+    cfg, inputs = W.config3("cem", K=3000)
+    cfg = dict(cfg, n_elite=2900)
+    inp = dict(inputs[0])
+    x0 = inp["x0"].copy()
+    x0[7] = W.f32(1.0)
+    x0[10] = W.f32(8.0)
+    inp["x0"] = x0
+    st = W.initial_distribution(cfg)
+    c = _ctrl(B, cfg, [inp], st)
+    ro = orc.step(cfg, 0, inp, dict(st))
+    _, outs = c.step([inp])
+    Jg = c.debug_costs()[0].astype(np.float64)
+    n_fin = int(np.sum(np.isfinite(Jg)))
+    assert 0 < n_fin < cfg["n_elite"]
+    mu_s = orc.warm_shift(cfg, st["mean"])
+    max_pitch = np.empty(3000)
+    for k in range(3000):
+        th, _, f = orc.sample(cfg, mu_s, st["var"], st["freq_idx"], 0, 0, k)
+        _, tr = orc.rollout(cfg, inp["x0"], inp["phase"], inp["feet_cur"], inp["feet_next"], inp["xref"], th, f,
+                            traj=True)
+        max_pitch[k] = np.max(np.abs(tr[:, 7])) if np.all(np.isfinite(tr)) else np.inf
+    regular = np.isfinite(Jg) & np.isfinite(ro.J) & (max_pitch < 1.45)  # 0.12 rad from the singularity
+    if regular.any():
+        _check_costs(Jg[regular], ro.J[regular])
+    D = 12 * cfg["knots"]
+    floor = np.array([(cfg["sigma_min_frac"] * cfg["sigma"][d % 3]) ** 2 for d in range(D)])
+    rc, mu, var, e, dg = orc.cem_update(Jg, ro.theta, cfg["n_elite"], floor, 1, st["var"])
+    assert rc == 0 and dg.n_diverged == 3000 - n_fin
+    np.testing.assert_array_equal(np.sort(c.debug_elites(0)), np.sort(e))
+    assert outs[0]["n_diverged"] == 3000 - n_fin
+    assert np.max(np.abs(outs[0]["mean"] - mu)) <= _tol_vec(mu)
+    assert np.max(np.abs(outs[0]["var"] - var)) <= _tol_vec(var)
+
+
+# ---------------------------------------------------------------------------
+# config 5 sharded by robot (BASELINE configs[4])
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", ["mppi", "cem"])
+def test_robot_offset_shards_equal_one_context(B, mode):
+    """Two contexts owning robots [0, 3) and [3, 6) (robot_offset = 3) reproduce one
+    six-robot context bit for bit over two iterations: the noise counter carries the global
+    robot index (O2), so sharding by robot changes nothing but where the work runs."""
+    R = 6
+    cfg = W.base_config(n_samples=1024, n_robots=R, mode=mode, n_elite=100 if mode == "cem" else 1)
+    rng = np.random.default_rng(5)
+    inputs = [W.robot_input(cfg, r, cmd=(rng.uniform(-.5, .5), rng.uniform(-.5, .5), 0),
+                            phase=int(rng.integers(0, 2 ** 32))) for r in range(R)]
+    full = B.Controller(cfg)
+    halves = [B.Controller(dict(cfg, n_robots=3), robot_offset=0), B.Controller(dict(cfg, n_robots=3), robot_offset=3)]
+    for r in range(R):
+        full.set_reference(r, inputs[r]["xref"])
+        halves[r // 3].set_reference(r % 3, inputs[r]["xref"])
+    for _ in range(2):
+        _, of = full.step(inputs)
+        _, o0 = halves[0].step(inputs[:3])
+        _, o1 = halves[1].step(inputs[3:])
+        Jf = full.debug_costs()
+        np.testing.assert_array_equal(Jf[:3], halves[0].debug_costs())
+        np.testing.assert_array_equal(Jf[3:], halves[1].debug_costs())
+        for r, o in enumerate(o0 + o1):
+            for key in ("mean", "var", "u0"):
+                np.testing.assert_array_equal(of[r][key], o[key])
+            assert of[r]["freq_idx"] == o["freq_idx"] and of[r]["j_min"] == o["j_min"]
