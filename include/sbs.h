@@ -98,7 +98,7 @@ typedef struct sbs_config {
   /* optimiser */
   int32_t mode;           /* sbs_mode */
   int32_t elite_preserve; /* 1: sample 0 is the (shifted) mean with the current theta1 (L21) */
-  int64_t n_samples;      /* K per robot, summed over all ranks, 1..2^31-1 */
+  int64_t n_samples;      /* K per robot, summed over all ranks, 1..2^24 (finite counts are binary32) */
   int64_t n_elite;        /* K_e for SBS_CEM (1..K); ignored for MPPI; forced to 1 for NAIVE */
   float lambda;           /* MPPI temperature, > 0 */
   float sigma[3];         /* initial std per force axis (x, y, z), > 0 (L19) */

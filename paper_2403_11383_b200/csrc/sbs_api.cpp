@@ -87,6 +87,10 @@ struct sbs_ctx {
   Params P{};
   int sm_count = 0;
   cudaStream_t stream = nullptr;
+  // device-path calls run on the caller's stream: the last one's completion event, so that
+  // state getters / setters and the host path order themselves after it
+  cudaEvent_t dev_ev = nullptr;
+  bool dev_pending = false;
   // device buffers
   float* d_mean = nullptr;
   float* d_var = nullptr;
@@ -156,6 +160,22 @@ struct sbs_ctx {
 };
 
 namespace {
+// a device-path call enqueued work on the caller's stream s
+cudaError_t note_device_work(sbs_ctx* c, cudaStream_t s) {
+  c->dev_pending = true;
+  return cudaEventRecord(c->dev_ev, s);
+}
+// the context's own stream and the last device-path work have completed (getters / setters:
+// a checkpoint is never torn by a step still running on a caller stream)
+cudaError_t sync_ctx(sbs_ctx* c) {
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && c->dev_pending) {
+    e = cudaEventSynchronize(c->dev_ev);
+    if (e == cudaSuccess) c->dev_pending = false;
+  }
+  return e;
+}
+
 // the pinned block may be rewritten once its last upload (blk_ev) has completed;
 // a host flag skips the driver call when nothing was recorded since the last wait
 cudaError_t blk_wait(sbs_ctx* c) {
@@ -273,7 +293,8 @@ int validate(const sbs_config* c, std::string& why) {
     if (!(c->Q[i] >= 0) || !(c->R[i] >= 0)) return bad("Q and R must be >= 0");
   if (!(c->rho >= 0) || !(c->w_fc >= 0) || !std::isfinite(c->f_nominal)) return bad("bad rho / w_fc / f_nominal");
   if (c->mode < SBS_MPPI || c->mode > SBS_NAIVE) return bad("bad mode");
-  if (c->n_samples < 1 || c->n_samples > 0x7fffffffLL) return bad("n_samples out of range");
+  // the finite / diverged counts ride in binary32 record fields (exact below 2^24)
+  if (c->n_samples < 1 || c->n_samples > (1LL << 24)) return bad("n_samples out of range (1 .. 2^24)");
   if (c->mode == SBS_CEM && (c->n_elite < 1 || c->n_elite > c->n_samples)) return bad("need 1 <= n_elite <= n_samples");
   if (!(c->lambda > 0)) return bad("lambda must be > 0");
   for (int a = 0; a < 3; ++a)
@@ -374,7 +395,9 @@ int enqueue_step(sbs_ctx* c, cudaStream_t s) {
       // raises the peer's flag; this stream waits (front-end, no SM) for the peers' flags
       // (two gather buffers alternate with the sequence number: a rank publishing step t + 1
       // cannot overwrite what a slower peer still reads for step t)
-      const uint32_t seq = ++c->xseq;
+      // (the sequence number is committed only once the publishing launch is enqueued: an
+      // early return leaves it -- and this rank's state -- unchanged)
+      const uint32_t seq = c->xseq + 1;
       const size_t par = (seq & 1u) * c->xgather_bytes;
       float* gat = reinterpret_cast<float*>(c->d_xbuf + par);
       P.n_peers = c->cfg.world;
@@ -384,6 +407,7 @@ int enqueue_step(sbs_ctx* c, cudaStream_t s) {
       int rc = enqueue_records(c, s, gat + (size_t)c->cfg.rank * n);
       P.n_peers = 0;
       if (rc != SBS_OK) return rc;
+      c->xseq = seq;
       for (int j = 0; j < c->cfg.world; ++j) {
         if (j == c->cfg.rank) continue;
         const int r2 = g_wait_value32(s, c->d_xflags + j, seq);
@@ -468,6 +492,7 @@ void sbs_destroy(sbs_ctx* c) {
   for (auto e : c->free_events) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->dev_ev) cudaEventDestroy(c->dev_ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   (void)cudaGetLastError();  // teardown errors (e.g. a context that failed half-way) must not leak into later launches
@@ -498,6 +523,7 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   CKC(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, cfg->device));
   CKC(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CKC(sbs::prepare_kernels(cfg->knots));
+  CKC(cudaEventCreateWithFlags(&c->dev_ev, cudaEventDisableTiming));
   CKC(cudaEventCreate(&c->ev0));
   CKC(cudaEventCreate(&c->ev1));
 
@@ -775,6 +801,7 @@ int sbs_set_reference_device(sbs_ctx* c, const float* d_x_ref, void* stream) {
   CK(cudaMemcpyAsync(c->h_xref, d_x_ref, (size_t)c->P.R * c->P.H * 12 * sizeof(float), cudaMemcpyDeviceToHost,
                      (cudaStream_t)stream));
   CK(blk_record(c, (cudaStream_t)stream));
+  CK(note_device_work(c, (cudaStream_t)stream));
   std::fill(c->ref_set.begin(), c->ref_set.end(), 1);
   return SBS_OK;
 }
@@ -788,6 +815,7 @@ int sbs_set_distribution(sbs_ctx* c, int32_t robot, const float* mean, const flo
   for (int d = 0; d < D; ++d)
     if (!(var[d] >= 0)) return fail(c, SBS_ERR_INVALID_ARG, "var must be >= 0");
   CK(cudaSetDevice(c->cfg.device));
+  CK(sync_ctx(c));  // never under a step still running on a caller stream
   CK(cudaMemcpyAsync(c->d_mean + (size_t)robot * D, mean, D * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->d_var + (size_t)robot * D, var, D * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->d_fidx + robot, &freq_idx, sizeof(int), cudaMemcpyHostToDevice, c->stream));
@@ -826,6 +854,7 @@ int sbs_set_covariance(sbs_ctx* c, int32_t robot, const float* C) {
   for (size_t i = 0; i < L.size(); ++i) L[i] = (float)Ld[i];
   for (int d = 0; d < D; ++d) v[d] = C[d * D + d];
   CK(cudaSetDevice(c->cfg.device));
+  CK(sync_ctx(c));
   CK(cudaMemcpyAsync(c->d_L + (size_t)robot * D * D, L.data(), L.size() * sizeof(float), cudaMemcpyHostToDevice,
                      c->stream));
   CK(cudaMemcpyAsync(c->d_var + (size_t)robot * D, v.data(), D * sizeof(float), cudaMemcpyHostToDevice, c->stream));
@@ -839,7 +868,7 @@ int sbs_get_cholesky(sbs_ctx* c, int32_t robot, float* L) {
   if (robot < 0 || robot >= c->P.R) return fail(c, SBS_ERR_INVALID_ARG, "robot out of range");
   const int D = c->P.D;
   CK(cudaSetDevice(c->cfg.device));
-  CK(cudaDeviceSynchronize());
+  CK(sync_ctx(c));
   CK(cudaMemcpy(L, c->d_L + (size_t)robot * D * D, (size_t)D * D * sizeof(float), cudaMemcpyDeviceToHost));
   return SBS_OK;
 }
@@ -849,7 +878,7 @@ int sbs_get_distribution(sbs_ctx* c, int32_t robot, float* mean, float* var, int
   if (robot < 0 || robot >= c->P.R) return fail(c, SBS_ERR_INVALID_ARG, "robot out of range");
   const int D = c->P.D;
   CK(cudaSetDevice(c->cfg.device));
-  CK(cudaStreamSynchronize(c->stream));
+  CK(sync_ctx(c));
   if (mean) CK(cudaMemcpy(mean, c->d_mean + (size_t)robot * D, D * sizeof(float), cudaMemcpyDeviceToHost));
   if (var) CK(cudaMemcpy(var, c->d_var + (size_t)robot * D, D * sizeof(float), cudaMemcpyDeviceToHost));
   if (freq_idx) CK(cudaMemcpy(freq_idx, c->d_fidx + robot, sizeof(int), cudaMemcpyDeviceToHost));
@@ -920,6 +949,10 @@ int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
   if (c->external) return fail(c, SBS_ERR_STATE, "external exchange: use sbs_step_records / sbs_finish_records");
   CK(cudaSetDevice(c->cfg.device));
   cudaStream_t s = c->stream;
+  if (c->dev_pending) {  // a device-path step on a caller stream goes first (stream order on the GPU)
+    CK(cudaStreamWaitEvent(s, c->dev_ev, 0));
+    c->dev_pending = false;  // this step's own completion wait covers it from here on
+  }
   if (R == 1 && c->P.H * 12 <= sbs::kInlineRefFloats && c->cfg.world == 1) {
     // inputs, reference and iteration counter ride in the kernel parameters: no copy node,
     // no graph (direct launches); outputs land in mapped pinned memory
@@ -952,12 +985,15 @@ int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
     if (timed) CK(cudaEventRecord(c->ev1, s));
     HT(6);
     if (poll) {
-      const volatile uint32_t* flag = c->h_done;
-      for (uint32_t n = 1; *flag != c->done_seq; ++n) {
+      // acquire loads: the outputs the finishing CTA wrote before its release store are
+      // visible once the flag is (on weakly ordered hosts too)
+      uint32_t* flag = c->h_done;
+      for (uint32_t n = 1; __atomic_load_n(flag, __ATOMIC_ACQUIRE) != c->done_seq; ++n) {
         if ((n & 1023u) == 0) {  // a failed launch never raises the flag: ask the stream now and then
           const cudaError_t e = cudaStreamQuery(s);
           if (e != cudaErrorNotReady && e != cudaSuccess) CK(e);
-          if (e == cudaSuccess && *flag != c->done_seq) return fail(c, SBS_ERR_CUDA, "step completed without its flag");
+          if (e == cudaSuccess && __atomic_load_n(flag, __ATOMIC_ACQUIRE) != c->done_seq)
+            return fail(c, SBS_ERR_CUDA, "step completed without its flag");
         }
 #if defined(__x86_64__)
         __builtin_ia32_pause();
@@ -1036,6 +1072,7 @@ int sbs_step_device(sbs_ctx* c, const sbs_input* d_in, sbs_output* d_out, void* 
   int rc = enqueue_step(c, (cudaStream_t)stream);
   if (rc != SBS_OK) return rc;
   c->iter += 1;
+  CK(note_device_work(c, (cudaStream_t)stream));
   return SBS_OK;
 }
 
@@ -1115,7 +1152,10 @@ int sbs_step_records(sbs_ctx* c, const sbs_input* d_in, float* d_rec, void* stre
     c->ref_dirty = false;
   }
   c->P.in = d_in;
-  return enqueue_records(c, (cudaStream_t)stream, d_rec);
+  const int rc = enqueue_records(c, (cudaStream_t)stream, d_rec);
+  if (rc != SBS_OK) return rc;
+  CK(note_device_work(c, (cudaStream_t)stream));
+  return SBS_OK;
 }
 
 int sbs_finish_records(sbs_ctx* c, const float* d_recs, const sbs_input* d_in, sbs_output* d_out, void* stream) {
@@ -1125,8 +1165,10 @@ int sbs_finish_records(sbs_ctx* c, const float* d_recs, const sbs_input* d_in, s
   c->P.in = d_in;
   c->P.out = d_out;
   const int rc = enqueue_finish(c, (cudaStream_t)stream, d_recs);
-  if (rc == SBS_OK) c->iter += 1;
-  return rc;
+  if (rc != SBS_OK) return rc;
+  c->iter += 1;
+  CK(note_device_work(c, (cudaStream_t)stream));
+  return SBS_OK;
 }
 
 namespace {
@@ -1175,6 +1217,7 @@ int sbs_advance(sbs_ctx* c, sbs_input* d_in, const sbs_output* d_out, const sbs_
   if (rc != SBS_OK) return rc;
   const sbs::LoopArgs a = loop_args(lc, d_cmd, d_wrench, d_fallen, nullptr);
   CK(timed(c, SBS_KERNEL_ADVANCE, s, [&] { return sbs::launch_advance(c->P, a, d_in, d_out, s); }));
+  CK(note_device_work(c, s));
   std::fill(c->ref_set.begin(), c->ref_set.end(), 1);
   return SBS_OK;
 }
@@ -1261,6 +1304,7 @@ int sbs_run_loop(sbs_ctx* c, int32_t n_iter, sbs_input* d_in, sbs_output* d_out,
     for (; i < n_iter; ++i) CK(cudaGraphLaunch(c->loop_graph, s));
   }
   c->iter += (uint32_t)n_iter * (uint32_t)lc->n_inner;
+  CK(note_device_work(c, s));
   return SBS_OK;
 }
 
@@ -1273,7 +1317,7 @@ int sbs_get_reference(sbs_ctx* c, int32_t robot, float* x_ref) {
     return SBS_OK;
   }
   CK(cudaSetDevice(c->cfg.device));
-  CK(cudaDeviceSynchronize());  // the reference may be rebuilt on any caller stream
+  CK(sync_ctx(c));  // the reference may be rebuilt on any caller stream
   CK(cudaMemcpy(x_ref, c->d_xref + (size_t)robot * n, n * sizeof(float), cudaMemcpyDeviceToHost));
   return SBS_OK;
 }
@@ -1293,7 +1337,7 @@ int sbs_get_state(sbs_ctx* c, void* buf, uint64_t* nbytes) {
                            ((uint64_t)R << 32) | (uint64_t)D};
   memcpy(b, hdr, 32);
   CK(cudaSetDevice(c->cfg.device));
-  CK(cudaStreamSynchronize(c->stream));
+  CK(sync_ctx(c));
   CK(cudaMemcpy(b + 32, c->d_mean, (size_t)R * D * sizeof(float), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(b + 32 + (size_t)R * D * 4, c->d_var, (size_t)R * D * sizeof(float), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(b + 32 + (size_t)R * D * 8, c->d_fidx, R * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1315,7 +1359,7 @@ int sbs_set_state(sbs_ctx* c, const void* buf, uint64_t nbytes) {
   if (hdr[0] != 0x5342535354415445ull || hdr[2] != c->cfg.seed || hdr[3] != (((uint64_t)R << 32) | (uint64_t)D))
     return fail(c, SBS_ERR_INVALID_ARG, "state does not match this context");
   CK(cudaSetDevice(c->cfg.device));
-  CK(cudaStreamSynchronize(c->stream));
+  CK(sync_ctx(c));
   CK(cudaMemcpy(c->d_mean, b + 32, (size_t)R * D * sizeof(float), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_var, b + 32 + (size_t)R * D * 4, (size_t)R * D * sizeof(float), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_fidx, b + 32 + (size_t)R * D * 8, R * sizeof(int), cudaMemcpyHostToDevice));

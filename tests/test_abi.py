@@ -73,3 +73,13 @@ def test_sm100a_cubin_and_no_fallback():
         if f.endswith(".py"):
             txt = open(os.path.join(pkg, f)).read()
             assert "from oracle" not in txt and "import oracle" not in txt, f
+
+
+def test_sample_count_limit(lib):
+    """n_samples is capped at 2^24 (the finite / diverged counts ride in binary32 fields)."""
+    from paper_2403_11383_b200 import binding as B
+    from paper_2403_11383_b200 import workloads as W
+    cc = B.make_config(W.base_config(n_samples=(1 << 24) + 1))
+    ctx = C.c_void_p()
+    assert lib.sbs_create(C.byref(cc), C.byref(ctx)) == -1
+    assert b"2^24" in lib.sbs_last_error(None)

@@ -245,3 +245,32 @@ def test_robot_offset_shards_equal_one_context(B, mode):
             for key in ("mean", "var", "u0"):
                 np.testing.assert_array_equal(of[r][key], o[key])
             assert of[r]["freq_idx"] == o["freq_idx"] and of[r]["j_min"] == o["j_min"]
+
+
+def test_checkpoint_after_side_stream_step(B):
+    """State getters wait for device-path work enqueued on a caller's side stream (the
+    checkpoint is the state after that step, never a torn one), and a host-path step
+    issued after it is ordered behind it."""
+    import ctypes as C
+
+    import torch
+    cfg, inputs = W.config4(1 << 20)
+    a = _ctrl(B, cfg, inputs)
+    b = _ctrl(B, cfg, inputs)
+    side = torch.cuda.Stream()
+    d_in = torch.from_numpy(np.frombuffer(bytes(B.make_inputs(inputs)), dtype=np.uint8).copy()).cuda()
+    d_out = torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    a.step_device(d_in.data_ptr(), d_out.data_ptr(), side.cuda_stream)   # ~0.3 ms on the side stream
+    snap = a.get_state()                                                  # no explicit synchronisation
+    m_a, _, _ = a.get_distribution(0)
+    b.step_device(d_in.data_ptr(), d_out.data_ptr(), side.cuda_stream)
+    side.synchronize()
+    m_b, _, _ = b.get_distribution(0)
+    np.testing.assert_array_equal(m_a, m_b)
+    c = _ctrl(B, cfg, inputs)
+    c.set_state(snap)
+    np.testing.assert_array_equal(c.get_distribution(0)[0], m_b)
+    _, o1 = a.step(inputs)                     # host path after the side-stream step
+    _, o2 = b.step(inputs)
+    np.testing.assert_array_equal(o1[0]["mean"], o2[0]["mean"])
