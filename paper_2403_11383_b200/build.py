@@ -9,6 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsbs.so")
+# the same sources with device-side bounds checks (SBS_CHECK, sbs_internal.h): tests only
+CHECKED_LIB = os.path.join(HERE, "libsbs_checked.so")
 SOURCES = ["sbs_kernels.cu", "sbs_loop.cu", "sbs_api.cpp"]
 HEADERS = ["sbs_internal.h", "sbs_noise.cuh", "sbs_robot_model.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -24,10 +26,10 @@ def _inputs():
     return files
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(out: str = LIB) -> bool:
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(out)
     return any(os.path.getmtime(f) > t for f in _inputs())
 
 
@@ -45,8 +47,10 @@ def _units(only_p=None):
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=(), only_p=None) -> str:
     """Compile csrc/ into `out` (default: the in-tree libsbs.so).  Experiment builds (another
     `out`) may add `defines` and restrict the knot count with `only_p`."""
-    if out == LIB and not force and not stale():
-        return LIB
+    if out in (LIB, CHECKED_LIB) and not force and not stale(out):
+        return out
+    if out == CHECKED_LIB:
+        defines = (*defines, "SBS_CHECKED")
     from concurrent.futures import ThreadPoolExecutor
     tag = "" if out == LIB else "." + os.path.basename(out)
     if only_p is not None:
@@ -71,5 +75,12 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     return out
 
 
+def build_checked(force: bool = False) -> str:
+    """The bounds-checked variant of the library (tests: tests/test_gpu_checked.py)."""
+    return build(force=force, out=CHECKED_LIB)
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv))

@@ -6,6 +6,25 @@
 
 #include "../../include/sbs.h"
 
+// Device-side bounds checks (the SBS_CHECKED build, tests only: compute-sanitizer is not
+// available on the GPU pool): every kernel index that addresses a context buffer is
+// checked against the bound its allocation was sized with; a violation prints and traps.
+#if defined(SBS_CHECKED)
+#include <cstdio>
+#define SBS_CHECK(cond)                                                                               \
+  do {                                                                                                \
+    if (!(cond)) {                                                                                    \
+      printf("SBS_CHECK failed: %s (%s:%d) block (%d,%d) thread %d\n", #cond, __FILE__, __LINE__,       \
+             (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);                                     \
+      __trap();                                                                                       \
+    }                                                                                                 \
+  } while (0)
+#else
+#define SBS_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace sbs {
 
 constexpr int kBlock = 128;         // samples per tile = threads per rollout CTA

@@ -124,9 +124,11 @@ static __device__ void load_robot(const Params& p, int r, RobotSmem& s, bool rol
     s.sig[d] = __fsqrt_rn(var[d]);
   }
   const sbs_input* in = robot_in(p, r);
+  SBS_CHECK(r >= 0 && r < p.R);
   if (threadIdx.x == 0) {
     s.cur_idx = p.fidx[r];
     s.iter = step_iter(p);
+    SBS_CHECK(s.cur_idx >= 0 && s.cur_idx < p.n_freq);
   }
   if (!rollout_inputs) return;  // sampling only (elite regeneration, debug draws)
   for (int a = threadIdx.x; a < 12; a += blockDim.x) {
@@ -697,6 +699,7 @@ static __device__ float rollout(const Params& p, const TH& th, int fi, const Rob
   float2 pxy = f2(s.x0[0], s.x0[1]), vxy = f2(s.x0[3], s.x0[4]);
   float pz = s.x0[2], vz = s.x0[5];
   float2 A = f2(s.x0[6], s.x0[7]), Bq = f2(s.x0[8], s.x0[9]), C = f2(s.x0[10], s.x0[11]);
+  SBS_CHECK(fi >= 0 && fi < p.n_freq && p.H <= SBS_MAX_HORIZON);
   const uint8_t* ct = s.ctab[fi];
   float J = 0.0f;
   bool bad = false;
@@ -798,6 +801,7 @@ __device__ __forceinline__ void warp_argmin(float& m, int& mk, int& mf) {
 //   [0] min J  [1] k_argmin  [2] theta1 of argmin  [3] S = sum w  [4] S2 = sum w^2
 //   [5] sum of finite J  [6] number finite  [7] 0  [8 ..] V = sum w theta2
 __device__ __forceinline__ const float* part_rec(const Params& p, int r, int c) {
+  SBS_CHECK(r >= 0 && r < p.R && c >= 0 && c < p.n_cta);
   return p.part_c_stride == 1 ? p.part + ((size_t)r * p.n_cta + c) * p.part_stride
                               : p.part + ((size_t)c * p.part_c_stride + r) * p.part_stride;
 }
@@ -830,6 +834,7 @@ __device__ __forceinline__ void stage_copy(float* dst, const float* src, int n) 
 static __device__ void write_output(const Params& p, int r, int status, const float* mean_new, const float* var_new,
                              int fi, float jmin, float jmean, float omega, float ess, int ndiv,
                              const uint32_t* pre = nullptr) {
+  SBS_CHECK(r >= 0 && r < p.R);
   sbs_output* o = p.out + r;
   const int D = p.D;
   const uint32_t ph0 = pre ? pre[0] : robot_in(p, r)->phase_q32;
@@ -1357,6 +1362,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
         if (blockIdx.x == 0) SBS_TS(3);
         if (valid) {
           J = Ja;
+          SBS_CHECK(kl >= 0 && kl < p.K_local);
           p.J[(size_t)r * p.K_local + kl] = J;
         }
       }
@@ -1377,6 +1383,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
       SBS_CTS(5);
       SBS_CTS(2);
       if (blockIdx.x == 0) SBS_TS(3);
+      SBS_CHECK(kl >= 0 && kl < p.K_local);
       p.J[(size_t)r * p.K_local + kl] = J;
     }
     // ---- per-tile argmin (J, k) ----
@@ -1538,6 +1545,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
   // kernel scheduled early, next to the running rollout, was measured 1.5x slower
   // after an L2 flush (its CTA then starts at grid completion, still PDL-ordered)
   if (FUSED) griddep_launch_dependents();
+  SBS_CHECK((int)blockIdx.x < p.n_cta && r < p.R);
   float* out = p.part + ((size_t)r * p.n_cta + blockIdx.x) * p.part_stride;
   if (EPI == EPI_MPPI) {
     if (tid < D) out[kPartHdr + tid] = run;
@@ -1710,6 +1718,7 @@ static __device__ void select_block(const float* J, int64_t K, int64_t K_e, int6
     const bool sel = lt || (eq && eq_before < n_eq);
     if (sel) {
       const uint32_t pos = sel_base + lt_before + eq_sel_before_me;
+      SBS_CHECK(pos < (uint64_t)K_e);
       elite[pos] = k_begin + k;
       if (eJ) eJ[pos] = J[k];
     }
@@ -1858,6 +1867,7 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
     const bool take = key[i] < T || (is_eq && eq_before < n_eq);  // ties: lowest indices first
     eq_before += is_eq ? 1u : 0u;
     if (take) {
+      SBS_CHECK(pos < (uint32_t)K_e);
       const float Jv = key_cost(key[i]);  // (J itself up to NaN -> +inf, -0 -> +0)
       if (stage) {
         s_eJ[pos] = Jv;
@@ -2030,8 +2040,10 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   griddep_wait();              // the select kernel's elite list and diagnostics
   if (blockIdx.x == 0) SBS_TS(11);
   const bool has_e = e < p.n_elite;
+  SBS_CHECK((int)blockIdx.x < p.n_eblk && r < p.R);
   const int64_t k = has_e ? p.elite[(size_t)r * p.n_elite + e] : 0;
   const float Je = has_e ? p.elite_J[(size_t)r * p.n_elite + e] : kInf;
+  SBS_CHECK(k >= 0 && k < p.K_global);
   __syncthreads();
   const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
   float dev[4] = {0.f, 0.f, 0.f, 0.f};
