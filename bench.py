@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true", help="skip the config 2/3/5 lines (ncu launch lists)")
+    ap.add_argument("--same-gpu", action="store_true",
+                    help="code-path check only: every rank on device 0 (peer exchange between processes of one "
+                         "GPU); its timings are not multi-GPU numbers")
     return ap.parse_args()
 
 
@@ -217,6 +220,11 @@ def _device_inputs(B, C, np, torch, inputs):
     return d_in, d_out
 
 
+def _red_dev(dist):
+    """Device of the small max / gather tensors: the GPU under NCCL, the host under gloo."""
+    return "cpu" if dist.get_backend() == "gloo" else "cuda"
+
+
 def _peer_connect(ctrl, dist, world):
     """Trade the exchange buffers' IPC handles; every rank must end on the same exchange."""
     ok, why = True, ""
@@ -249,11 +257,15 @@ def run_sbs(args):
 
     rank, world, local = dist_env()
     assert world == args.gpus or world == 1, "launch N > 1 with torchrun --nproc-per-node N"
+    if args.same_gpu:
+        assert args.exchange == "peer", "--same-gpu checks the peer-memory path (NCCL needs distinct GPUs)"
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         if args.exchange == "nccl" and rank == 0:
             os.environ.setdefault("NCCL_DEBUG", "INFO")  # the communicator lines go to stderr
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo" if args.same_gpu else "nccl",
+                                device_id=None if args.same_gpu else torch.device("cuda", local))
     if rank == 0:
         build.build()
     if world > 1:
@@ -263,7 +275,7 @@ def run_sbs(args):
     K = k_total(args, world)
     cfg, inputs = W.config4(K)
     nccl_id = None
-    if world > 1:
+    if world > 1 and not args.same_gpu:  # (NCCL rejects two ranks on one GPU; --same-gpu uses the peer path only)
         obj = [B.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
@@ -316,10 +328,10 @@ def run_sbs(args):
     r_avg_s = (r_ms / max(r_n, 1)) * 1e-3
     rank_times = None
     if world > 1:
-        t = torch.tensor([tot], dtype=torch.float64, device="cuda")
+        t = torch.tensor([tot], dtype=torch.float64, device=_red_dev(dist))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_max = float(t.item())
-        mine = torch.tensor([tot / args.steps * 1e3, r_avg_s * 1e6], dtype=torch.float64, device="cuda")
+        mine = torch.tensor([tot / args.steps * 1e3, r_avg_s * 1e6], dtype=torch.float64, device=_red_dev(dist))
         allr = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(allr, mine)
         rank_times = [{"rank": i, "us_per_step": float(x[0]), "rollout_kernel_us": float(x[1]),
@@ -393,6 +405,7 @@ def run_sbs(args):
             "config": headline_config(args, world, exchange if world > 1 else None),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "latency": latency, "exchange": exchange,
             "per_rank": rank_times, "other_configs": extra,
+            "same_gpu_code_path_check": bool(args.same_gpu) or None,
             "gpu_launches": int(ctrl.launches_per_step() * args.steps), "clocks": clk,
         }
         print(json.dumps(line), flush=True)
@@ -424,7 +437,7 @@ def _e2e(ctrl, B, np, torch, inputs, flush, n, world, dist, K):
         times.append(time.perf_counter() - t)
     e2e_s = sum(times)
     if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=_red_dev(dist))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_ms = 1e3 * e2e_s / n
@@ -567,7 +580,7 @@ def _config5_sharded(B, W, C, np, torch, dist, rank, world, local, flush, steps=
         ctrl.step_device(d_in.data_ptr(), d_out.data_ptr(), s.cuda_stream)
         e1.record(s)
     torch.cuda.synchronize()
-    tot = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([sum(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=_red_dev(dist))
     dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     ms = float(tot.item()) / steps
     ctrl.close()

@@ -946,7 +946,8 @@ int sbs_step(sbs_ctx* c, const sbs_input* in, sbs_output* out) {
       return fail(c, SBS_ERR_NONFINITE, "non-finite x0 / feet");
     if (!(fabsf(in[r].x0[7]) < 1.5697963267948966f)) return fail(c, SBS_ERR_SINGULAR, "|pitch(x0)| >= pi/2 - 1e-3");
   }
-  if (c->external) return fail(c, SBS_ERR_STATE, "external exchange: use sbs_step_records / sbs_finish_records");
+  if (c->external && !c->peer)
+    return fail(c, SBS_ERR_STATE, "external exchange: use sbs_step_records / sbs_finish_records");
   CK(cudaSetDevice(c->cfg.device));
   cudaStream_t s = c->stream;
   if (c->dev_pending) {  // a device-path step on a caller stream goes first (stream order on the GPU)
