@@ -65,10 +65,12 @@ def full(rep, out, K, H):
             flop = rate * cyc
             scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             dram = sum(g[k] * scale.get(u[h.index(k)], 1.0) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-            f.write(f"\nDerived (scalar FFMA/FMUL/FADD counters only; packed FFMA2/FADD2/FMUL2 are not counted): FP32 FLOP = {flop:.4e}; per sample-step = {flop/(K*H):.1f}; "
-                    f"instructions per sample = {g['inst_executed']*32/K:.0f}; "
-                    f"FP32 FLOP/cycle/SM = {rate/148:.1f} of 256 ({rate/148/256:.1%}); "
-                    f"DRAM bytes per launch = {dram:.4g}\n\n")
+            alg = 886.1419270833334 * K * H  # bench.py ALG_FLOP_FUSED (oracle op-counting mode) x units
+            f.write(f"\nDerived: algorithmic FLOPs (oracle op count, 886.14 per sample-step) per launch = {alg:.4e}, "
+                    f"{alg / t / 1e12:.2f} TFLOP/s under ncu ({alg / t / 74.45e12:.3f} of 74.45 TFLOP/s; ncu's clock "
+                    f"{cyc / t / 1e6:.0f} MHz); instructions per sample = {g['inst_executed']*32/K:.0f}; "
+                    f"scalar FFMA/FMUL/FADD counters alone (packed FFMA2/FADD2/FMUL2 not counted) = {flop/(K*H):.1f} "
+                    f"FLOP per sample-step; DRAM bytes per launch = {dram:.4g}\n\n")
             st = sorted(((k[len(STALLS):].replace('_per_issue_active.ratio', ''), float(row[i] or 0))
                          for i, k in enumerate(h) if k.startswith(STALLS) and k.endswith("per_issue_active.ratio")),
                         key=lambda x: -x[1])
