@@ -274,3 +274,27 @@ def test_checkpoint_after_side_stream_step(B):
     _, o1 = a.step(inputs)                     # host path after the side-stream step
     _, o2 = b.step(inputs)
     np.testing.assert_array_equal(o1[0]["mean"], o2[0]["mean"])
+
+
+def test_config4_full_size_update_recomputed(B):
+    """The bench's launch configuration (K = 2^22: 592 CTA records, the chunked merge): the
+    MPPI update (Alg. 4) recomputed in binary64 from the GPU's own costs and
+    samples -- the costs are oracle-checked on samples (test_config4_full_size_sampled), the
+    samples bitwise (the noise tests) -- must match the kernel's mean, Omega and ESS."""
+    K = 1 << 22
+    cfg, inputs = W.config4(K)
+    st = W.initial_distribution(cfg)
+    c = _ctrl(B, cfg, inputs, st)
+    chunk = 1 << 20
+    thetas = [c.debug_samples(0, k0, chunk)[1].astype(np.float64) for k0 in range(0, K, chunk)]  # this step's draws
+    status, outs = c.step(inputs)
+    assert status == 0
+    J = c.debug_costs()[0].astype(np.float64)
+    beta = np.min(J)
+    w = np.exp(-(J - beta) / cfg["lambda"])
+    omega = np.sum(w)
+    mu = sum(w[i * chunk:(i + 1) * chunk] @ th for i, th in enumerate(thetas)) / omega
+    assert np.max(np.abs(outs[0]["mean"] - mu)) <= 1e-4 * max(float(np.max(np.abs(mu))), 1.0)
+    assert outs[0]["omega"] == pytest.approx(omega, rel=1e-4)
+    assert outs[0]["ess"] == pytest.approx(omega ** 2 / np.sum(w * w), rel=1e-3)
+    assert outs[0]["j_min"] == beta
