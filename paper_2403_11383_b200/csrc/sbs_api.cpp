@@ -423,7 +423,9 @@ int enqueue_step(sbs_ctx* c, cudaStream_t s) {
     return enqueue_finish(c, s, c->d_gather);
   }
   CK(timed(c, SBS_KERNEL_ROLLOUT, s, [&] { return sbs::launch_rollout(P, mode, true, s); }));
-  if (mode == SBS_CEM) {
+  if (mode == SBS_CEM && P.cem_cluster) {
+    CK(timed(c, SBS_KERNEL_SELECT, s, [&] { return sbs::launch_cem_cluster(P, s); }));
+  } else if (mode == SBS_CEM) {
     CK(timed(c, SBS_KERNEL_SELECT, s, [&] { return sbs::launch_select(P, s); }));
     CK(timed(c, SBS_KERNEL_ELITE, s, [&] { return sbs::launch_elite(P, s); }));
   }
@@ -747,6 +749,14 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.elite_J = c->d_eJ;
   P.Lmat = c->d_L;
   P.cand = c->d_cand;
+  // CEM at world = 1: select + elite moments + finish as one cluster launch (bitwise the
+  // two-kernel path's results; SBS_CEM_CLUSTER=0 keeps the two kernels, for tests / A/B)
+  // (SBS_CEM_CLUSTER=8 / 16 caps the cluster size)
+  P.cem_cluster = 0;
+  if (cfg->world == 1 && sbs::cem_cluster_fits(P)) {
+    const char* e = getenv("SBS_CEM_CLUSTER");
+    P.cem_cluster = sbs::cem_cluster_size(P.P, e ? atoi(e) : 16);
+  }
   c->ref_set.assign(R, 0);
   // ---- NCCL (sample sharding) ----
   if (cfg->world > 1) {
@@ -1527,7 +1537,7 @@ int sbs_kernel_times(sbs_ctx* c, double* total_ms, int64_t* launches) {
 int sbs_launches_per_step(const sbs_ctx* c) {
   if (!c) return 0;
   if (c->cfg.world > 1) return c->cfg.mode == SBS_CEM ? 4 : 2;  // + the exchange (peer stores or ncclAllGather)
-  return c->cfg.mode == SBS_CEM ? 3 : 1;
+  return c->cfg.mode == SBS_CEM ? (c->P.cem_cluster ? 2 : 3) : 1;
 }
 
 }  // extern "C"

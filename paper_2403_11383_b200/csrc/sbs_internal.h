@@ -87,6 +87,7 @@ struct Params {
   int split;                  // latency mode: kSplitTile samples per tile, sampler split over 4 lanes
   int ab;                     // latency mode: 12 producer warps tabulate the stance-leg forces for the 4 integrator warps
   int full_cov;               // f3 (L42): CEM with a full covariance C = L L^T
+  int cem_cluster;            // CEM at world = 1: cluster size of the one-launch select + elite path, 0: two kernels
   int model;                  // 1: the constants equal the compiled-in robot model (sbs_robot_model.h)
   float* Lmat;                // [R][D][D] lower Cholesky factor (row-major), full_cov only
   int n_sig_groups;           // multiple Gaussians (L41): sample k uses sig_scale[k mod n_sig_groups]
@@ -167,6 +168,11 @@ cudaError_t launch_select_merge(const Params& p, cudaStream_t s);
 // world > 1 Naive: merge of the gathered rank argmin records + finish
 cudaError_t launch_naive_finalize(const Params& p, cudaStream_t s);
 cudaError_t launch_elite(const Params& p, cudaStream_t s);
+// CEM at world = 1: select + elite moments + finish in one cluster launch (bitwise the
+// same results as launch_select + launch_elite) when cem_cluster_fits
+cudaError_t launch_cem_cluster(const Params& p, cudaStream_t s);
+bool cem_cluster_fits(const Params& p);
+int cem_cluster_size(int P, int want);  // the largest resident cluster <= want (16 or 8), 0 if none
 cudaError_t launch_debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                  int* fidx, cudaStream_t s);
 cudaError_t launch_select_raw(const float* J, int64_t K, int64_t K_e, int64_t* idx, cudaStream_t s);

@@ -38,7 +38,7 @@
 
 namespace sbs {
 #if defined(SBS_TIMING)  // experiments only: phase timestamps (%globaltimer) of CTA 0 / the last CTA
-__device__ unsigned long long g_sbs_ts[16];
+__device__ unsigned long long g_sbs_ts[32];  // [16, 32): the CEM cluster kernel
 #define SBS_TS(i)                                                               \
   do {                                                                          \
     if (threadIdx.x == 0) {                                                     \
@@ -1544,7 +1544,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
   // the next iteration's kernels may be scheduled.  Not for the CEM rollout: a select
   // kernel scheduled early, next to the running rollout, was measured 1.5x slower
   // after an L2 flush (its CTA then starts at grid completion, still PDL-ordered)
-  if (FUSED) griddep_launch_dependents();
+  if (FUSED || p.cem_cluster) griddep_launch_dependents();  // (the CEM cluster kernel starts on idle SMs)
   SBS_CHECK((int)blockIdx.x < p.n_cta && r < p.R);
   float* out = p.part + ((size_t)r * p.n_cta + blockIdx.x) * p.part_stride;
   if (EPI == EPI_MPPI) {
@@ -1739,6 +1739,11 @@ static __device__ void select_block(const float* J, int64_t K, int64_t K_e, int6
 constexpr int kSelSmallMax = 16384;
 constexpr int kSelKPT = kSelSmallMax / kSelBlock;
 constexpr int kSelSmallSmemBytes = 32768 * 4;
+#if defined(SBS_TU_COMMON)
+constexpr int kSelTs = 0;  // SBS_TIMING slots of select_block_small: the select kernel's ...
+#else
+constexpr int kSelTs = 16;  // ... or the CEM cluster kernel's
+#endif
 constexpr int kSelHdrMax = 256;  // rollout records whose headers the select kernel stages (world = 1)
 
 // exclusive block scan of v over kSelBlock threads; returns the total in *tot
@@ -1868,7 +1873,7 @@ static __device__ void digit_pass_narrow(const uint32_t (&key)[kSelKPT], int nk,
 }
 
 static __device__ void select_block_small(const float* J, int K, int K_e, int64_t k_begin, int64_t* elite, float* eJ,
-                                          uint32_t* hist, bool zeroed = false) {
+                                          uint32_t* hist, bool zeroed = false, bool to_global = true) {
   __shared__ uint32_t s_w[33];
   __shared__ uint32_t s_res[2];
   const int tid = threadIdx.x;
@@ -1878,25 +1883,25 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
   uint32_t key[kSelKPT];
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i) key[i] = i < nk ? cost_key(J[k0 + i]) : 0xFFFFFFFFu;
-  if (blockIdx.x == 0) SBS_TS(2);
+  if (blockIdx.x == 0) SBS_TS(kSelTs + 2);
 #if SBS_SEL_DIGITS == 11
   // three narrow passes (bits 31..21, 20..10, 9..0): 2048-bin histograms, cheap scans
   (void)zeroed;
   digit_pass_narrow<11>(key, nk, 0u, 0u, 21, (uint32_t)K_e, hist, s_w, s_res);
   const uint32_t dA = s_res[0], bA = s_res[1];
   digit_pass_narrow<11>(key, nk, 0xFFE00000u, dA << 21, 10, (uint32_t)K_e - bA, hist, s_w, s_res);
-  if (blockIdx.x == 0) SBS_TS(3);
+  if (blockIdx.x == 0) SBS_TS(kSelTs + 3);
   const uint32_t dB = s_res[0], bB = s_res[1];
   digit_pass_narrow<10>(key, nk, 0xFFFFFC00u, (dA << 21) | (dB << 10), 0, (uint32_t)K_e - bA - bB, hist, s_w, s_res);
-  if (blockIdx.x == 0) SBS_TS(4);
+  if (blockIdx.x == 0) SBS_TS(kSelTs + 4);
   const uint32_t T = (dA << 21) | (dB << 10) | s_res[0];
   const uint32_t n_eq = (uint32_t)K_e - bA - bB - s_res[1];  // ties at T to take, lowest indices first
 #else
   digit16_pass(key, nk, 0u, 0u, 16, (uint32_t)K_e, hist, s_w, s_res, zeroed);
-  if (blockIdx.x == 0) SBS_TS(3);
+  if (blockIdx.x == 0) SBS_TS(kSelTs + 3);
   const uint32_t hi = s_res[0], below_hi = s_res[1];
   digit16_pass(key, nk, 0xFFFF0000u, hi << 16, 0, (uint32_t)K_e - below_hi, hist, s_w, s_res);
-  if (blockIdx.x == 0) SBS_TS(4);
+  if (blockIdx.x == 0) SBS_TS(kSelTs + 4);
   const uint32_t T = (hi << 16) | s_res[0];
   const uint32_t n_eq = (uint32_t)K_e - below_hi - s_res[1];  // ties at T to take, lowest indices first
 #endif
@@ -1912,7 +1917,7 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
   const uint32_t lt_before = both & 0xFFFFu;
   uint32_t eq_before = both >> 16;
   uint32_t pos = lt_before + min(eq_before, n_eq);
-  if (blockIdx.x == 0) SBS_TS(5);
+  if (blockIdx.x == 0) SBS_TS(kSelTs + 5);
   // the compacted list goes through shared memory (the histogram is free now) so that
   // the global writes are coalesced; scattered per-lane writes were measured at ~3 us
   const bool stage = (size_t)K_e * (sizeof(int64_t) + sizeof(float)) <= (size_t)kSelSmallSmemBytes;
@@ -1937,14 +1942,14 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
     }
     pos += take ? 1u : 0u;
   }
-  if (stage) {
+  if (stage) {  // (to_global false: the list stays staged at the start of `hist`, caller's use)
     __syncthreads();
-    for (int e = tid; e < K_e; e += blockDim.x) {
+    for (int e = tid; to_global && e < K_e; e += blockDim.x) {
       elite[e] = s_el[e];
       if (eJ) eJ[e] = s_eJ[e];
     }
   }
-  if (blockIdx.x == 0) SBS_TS(7);
+  if (blockIdx.x == 0) SBS_TS(kSelTs + 7);
 }
 
 
@@ -2081,81 +2086,15 @@ cudaError_t launch_debug_philox(const void* ctr, const void* key, int64_t n, voi
 // S2 = sum (theta - mu')^2.  The last CTA of a robot merges the records in
 // order and finishes: mean = mu' + S1/n, var = max(S2/n - (S1/n)^2, floor).
 // ---------------------------------------------------------------------------
-constexpr int kEliteGroup = 32;  // elites per CTA
-
+// The end of a CEM iteration (Alg. 1 UpdateMean / UpdateCov, L17), one CTA: from the merged
+// moments s_tot = [S1[D], n, S2[D]] about mu' and the select kernel's diagnostics s_diag =
+// [J_min, k_min, f_min, sum J, n_finite]: mean = mu' + S1/n, var = max(S2/n - (S1/n)^2,
+// floor); every sample diverged keeps mean and var.
 template <int P>
-__global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_constant__ Params p) {
+static __device__ void cem_finish(const Params& p, int r, const RobotSmem& s, const float* s_tot,
+                                  const float* s_diag, const uint32_t* s_pre, float* s_mean, float* s_var) {
   constexpr int D = 12 * P;
-  __shared__ RobotSmem s;
-  __shared__ float s_mean[D], s_var[D];
-  __shared__ float s_tot[2 * D + 1];
-  constexpr int kChunk = 32;  // elite records staged per round trip in the last CTA
-  __shared__ __align__(16) float s_stage[kChunk * kEPartStride];
-  __shared__ float s_diag[5];
-  const int r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
-  const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
-  load_robot(p, r, s, false);  // (not written by the select kernel: may overlap it)
-  griddep_wait();              // the select kernel's elite list and diagnostics
-  if (blockIdx.x == 0) SBS_TS(11);
-  const bool has_e = e < p.n_elite;
-  SBS_CHECK((int)blockIdx.x < p.n_eblk && r < p.R);
-  const int64_t k = has_e ? p.elite[(size_t)r * p.n_elite + e] : 0;
-  const float Je = has_e ? p.elite_J[(size_t)r * p.n_elite + e] : kInf;
-  SBS_CHECK(k >= 0 && k < p.K_global);
-  __syncthreads();
-  const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
-  float dev[4] = {0.f, 0.f, 0.f, 0.f};
-  float n = 0.f;
-  if (has_e) {
-    if (Je < kInf) {  // diverged samples never enter the moments (L17)
-      float th4[4];
-      sample_block(p, robot_g, k, q, s, th4);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dev[i] = th4[i] - s.mu[4 * q + i];
-      n = 1.f;
-    }
-  }
-  float* rec = p.epart + ((size_t)r * gridDim.x + blockIdx.x) * kEPartStride;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float a = dev[i], b2 = dev[i] * dev[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b2 += __shfl_xor_sync(0xffffffffu, b2, o);
-    }
-    if (lane == 0) {
-      rec[4 * q + i] = a;
-      rec[D + 1 + 4 * q + i] = b2;
-    }
-  }
-  if (q == 0) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-    if (lane == 0) rec[D] = n;
-  }
-  if (!arrive_last(p.ecounter + r, gridDim.x)) return;
-  // ---- last CTA: merge the elite records in order, finish the iteration ----
-  __shared__ uint32_t s_pre[2];
-  const float* sd = p.sdiag + (size_t)r * 8;
-  if (tid == 0) {  // issued with the record loads below
-    s_pre[0] = robot_in(p, r)->phase_q32;
-    s_pre[1] = step_iter(p);
-    for (int i = 0; i < 5; ++i) s_diag[i] = sd[i];  // rank-1 sample and diagnostics (select kernel)
-  }
-  {
-    float a0 = 0.f;  // row tid (2D + 1 <= blockDim = 8D); records summed in block order
-    for (int b0 = 0; b0 < (int)gridDim.x; b0 += kChunk) {
-      const int nb = min(kChunk, (int)gridDim.x - b0);
-      stage_copy(s_stage, p.epart + ((size_t)r * gridDim.x + b0) * kEPartStride, nb * kEPartStride);
-      __syncthreads();
-      if (tid < 2 * D + 1)
-        for (int b = 0; b < nb; ++b) a0 += s_stage[b * kEPartStride + tid];
-      __syncthreads();
-    }
-    if (tid < 2 * D + 1) s_tot[tid] = a0;
-  }
-  __syncthreads();
+  const int tid = threadIdx.x;
   const Best b{s_diag[0], __float_as_int(s_diag[1]), __float_as_int(s_diag[2])};
   const float ne = s_tot[D];
   const bool all_div = !(ne > 0.f);
@@ -2182,7 +2121,319 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
   }
   write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, b.m,
                s_diag[4] > 0.f ? s_diag[3] / s_diag[4] : kInf, ne, ne, (int)((float)p.K_global - s_diag[4]), s_pre);
+}
+
+constexpr int kEliteGroup = 32;  // elites per CTA
+
+// One warp, Philox block q (coordinates 4q..4q+3) of a group of 32 elites (lane = elite):
+// regenerate theta from the counter RNG, then the group's shifted moments about mu',
+// S1 = sum (theta - mu') and S2 = sum (theta - mu')^2 for the 4 coordinates, and the
+// finite count n.  The 8 lane sums run as a transposing butterfly: at lane bits 4, 3, 2
+// each lane keeps half of its values and adds the partner's copy of that half, then two
+// plain levels finish; value j = 4 b4 + 2 b3 + b2 (S1 of coordinate 4q + j for j < 4,
+// S2 of coordinate 4q + j - 4 after) ends on lanes 4j..4j+3.
+struct GroupMoments {
+  float t;  // this lane's value total
+  int j;    // its value index (lane >> 2)
+  float n;  // finite count (every lane)
+};
+__device__ __forceinline__ GroupMoments elite_group_moments(const Params& p, const RobotSmem& s, uint32_t robot_g,
+                                                            bool has_e, int64_t k, float Je, int q) {
+  const int lane = threadIdx.x & 31;
+  float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const bool fin = has_e && Je < kInf;  // diverged samples never enter the moments (L17)
+  if (fin) {
+    float th4[4];
+    sample_block(p, robot_g, k, q, s, th4);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = th4[i] - s.mu[4 * q + i];
+      v[4 + i] = v[i] * v[i];
+    }
+  }
+  float w4[4], w2[2];
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float keep = b4 ? v[4 + i] : v[i], give = b4 ? v[i] : v[4 + i];
+    w4[i] = keep + __shfl_xor_sync(0xffffffffu, give, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float keep = b3 ? w4[2 + i] : w4[i], give = b3 ? w4[i] : w4[2 + i];
+    w2[i] = keep + __shfl_xor_sync(0xffffffffu, give, 8);
+  }
+  GroupMoments m;
+  {
+    const float keep = b2 ? w2[1] : w2[0], give = b2 ? w2[0] : w2[1];
+    m.t = keep + __shfl_xor_sync(0xffffffffu, give, 4);
+  }
+  m.t += __shfl_xor_sync(0xffffffffu, m.t, 2);
+  m.t += __shfl_xor_sync(0xffffffffu, m.t, 1);
+  m.j = lane >> 2;
+  m.n = (float)__popc(__ballot_sync(0xffffffffu, fin));  // (exact)
+  return m;
+}
+// ... into the record rec = [S1[D], n, S2[D]] (lanes 4j; n by warp q = 0)
+template <int P>
+__device__ __forceinline__ void elite_group_record(const Params& p, const RobotSmem& s, uint32_t robot_g, bool has_e,
+                                                   int64_t k, float Je, int q, float* rec) {
+  constexpr int D = 12 * P;
+  const GroupMoments m = elite_group_moments(p, s, robot_g, has_e, k, Je, q);
+  const int lane = threadIdx.x & 31;
+  if ((lane & 3) == 0) rec[m.j < 4 ? 4 * q + m.j : D + 1 + 4 * q + m.j - 4] = m.t;
+  if (q == 0 && lane == 0) rec[D] = m.n;
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_constant__ Params p) {
+  constexpr int D = 12 * P;
+  __shared__ RobotSmem s;
+  __shared__ float s_mean[D], s_var[D];
+  __shared__ float s_tot[2 * D + 1];
+  constexpr int kChunk = 32;  // elite records staged per round trip in the last CTA
+  __shared__ __align__(16) float s_stage[kChunk * kEPartStride];
+  __shared__ float s_diag[5];
+  const int r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, q = tid >> 5;
+  const int64_t e = (int64_t)blockIdx.x * kEliteGroup + lane;
+  load_robot(p, r, s, false);  // (not written by the select kernel: may overlap it)
+  griddep_wait();              // the select kernel's elite list and diagnostics
+  if (blockIdx.x == 0) SBS_TS(11);
+  const bool has_e = e < p.n_elite;
+  SBS_CHECK((int)blockIdx.x < p.n_eblk && r < p.R);
+  const int64_t k = has_e ? p.elite[(size_t)r * p.n_elite + e] : 0;
+  const float Je = has_e ? p.elite_J[(size_t)r * p.n_elite + e] : kInf;
+  SBS_CHECK(k >= 0 && k < p.K_global);
+  __syncthreads();
+  elite_group_record<P>(p, s, (uint32_t)(p.robot_offset + r), has_e, k, Je, q,
+                        p.epart + ((size_t)r * gridDim.x + blockIdx.x) * kEPartStride);
+  if (!arrive_last(p.ecounter + r, gridDim.x)) return;
+  // ---- last CTA: merge the elite records in order, finish the iteration ----
+  __shared__ uint32_t s_pre[2];
+  const float* sd = p.sdiag + (size_t)r * 8;
+  if (tid == 0) {  // issued with the record loads below
+    s_pre[0] = robot_in(p, r)->phase_q32;
+    s_pre[1] = step_iter(p);
+    for (int i = 0; i < 5; ++i) s_diag[i] = sd[i];  // rank-1 sample and diagnostics (select kernel)
+  }
+  {
+    float a0 = 0.f;  // row tid (2D + 1 <= blockDim = 8D); records summed in block order
+    for (int b0 = 0; b0 < (int)gridDim.x; b0 += kChunk) {
+      const int nb = min(kChunk, (int)gridDim.x - b0);
+      stage_copy(s_stage, p.epart + ((size_t)r * gridDim.x + b0) * kEPartStride, nb * kEPartStride);
+      __syncthreads();
+      if (tid < 2 * D + 1)
+        for (int b = 0; b < nb; ++b) a0 += s_stage[b * kEPartStride + tid];
+      __syncthreads();
+    }
+    if (tid < 2 * D + 1) s_tot[tid] = a0;
+  }
+  __syncthreads();
+  cem_finish<P>(p, r, s, s_tot, s_diag, s_pre, s_mean, s_var);
   SBS_TS(12);
+}
+
+
+// ---------------------------------------------------------------------------
+// sbs_cem_cluster_kernel (CEM at world = 1, K <= kSelSmallMax, K_e <= 32 kCemMaxGroups,
+// diagonal covariance): the select kernel and the elite kernel in one launch, one
+// thread-block cluster of C = p.cem_cluster CTAs per robot (grid (C, R)).  The CTAs
+// exchange data only by asynchronous stores into each other's shared memory that
+// complete on the receiver's transaction barrier (st.async + mbarrier complete_tx):
+//   CTA 1, while CTA 0 selects: the robot's sampling distribution (warm-shifted mean,
+//     sigma), the rollout records' diagnostics and the output's phase / iteration
+//     -> CTA 0 (header barrier);
+//   CTA 0: the K_e elites (select_block_small, the select kernel's code) -> each CTA
+//     its groups of 32 (group g in CTA g mod C);
+//   every CTA: regenerates its groups, one warp per (group, Philox block q)
+//     (elite_group_moments, the elite kernel's arithmetic), the group records -> CTA 0
+//     (record barrier; CTA 0's own groups by plain stores);
+//   CTA 0: sums the records in group order (the elite kernel's last-CTA order) and
+//     finishes (cem_finish).
+// Same arithmetic in the same order as sbs_select_kernel + sbs_elite_kernel, so the
+// results are bitwise the same; what goes is the second launch, the elite list's round
+// trip through global memory and the arrival counter.  Every CTA waits only for data
+// addressed to it, so a CTA may leave once its last stores are issued.
+// ---------------------------------------------------------------------------
+constexpr int kCemMaxGroups = 64;  // K_e <= 2048
+constexpr int kCemSlots = kCemMaxGroups / 8;  // groups per CTA at the smallest cluster (8)
+constexpr int kCemRecStride = 2 * SBS_MAX_D + 4;  // cluster record [S1[D] | S2[D] | n, pad]: 16-byte aligned parts
+constexpr int kCemSmemBytes = kSelSmallSmemBytes + kCemMaxGroups * kCemRecStride * 4;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t n;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+  return n;
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// shared::cluster address of a shared variable's copy in CTA `rank`
+__device__ __forceinline__ uint32_t cl_addr(const void* local, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(local)), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {  // phase 0 of a fresh barrier
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t addr, float v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr),
+               "r"(__float_as_uint(v)), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t addr, uint32_t v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr), "r"(v),
+               "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t addr, int64_t v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr), "l"(v),
+               "r"(bar)
+               : "memory");
+}
+
+template <int P>
+__global__ void __launch_bounds__(kSelBlock) sbs_cem_cluster_kernel(const __grid_constant__ Params p) {
+  constexpr int D = 12 * P, NQ = 3 * P, RS = 2 * D + 4;
+  // dynamic: [select histogram / staged elite list (CTA 0) | group records [n_eblk][RS] (CTA 0)]
+  extern __shared__ __align__(16) uint32_t cem_smem[];
+  float* recs = reinterpret_cast<float*>(cem_smem + kSelSmallSmemBytes / 4);
+  __shared__ RobotSmem s;
+  __shared__ __align__(8) int64_t s_ek[kCemSlots * kEliteGroup];  // this CTA's elites (k, J) (CTAs > 0)
+  __shared__ float s_eJ[kCemSlots * kEliteGroup];
+  __shared__ float s_mean[D], s_var[D], s_tot[2 * D + 1], s_diag[5];
+  __shared__ uint32_t s_pre[2];
+  __shared__ __align__(8) uint64_t s_bar[2];  // [0]: elites (CTAs > 0) / records (CTA 0); [1]: header (CTA 0)
+  const int r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = cluster_rank(), C = cluster_size();
+  const int Ke = (int)p.n_elite, G = p.n_eblk;
+  SBS_CHECK(G <= kCemMaxGroups && (int)C * kCemSlots >= G && C >= 2 && p.K_local <= kSelSmallMax && r < p.R);
+  const int mine = (G - (int)rank + (int)C - 1) / (int)C;  // groups rank, rank + C, ...
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (rank == 0) {  // bytes CTA 0 receives: the other CTAs' group records, CTA 1's header
+      const int remote = G - (G + (int)C - 1) / (int)C;
+      mbar_expect_tx(&s_bar[0], (uint32_t)(remote * (NQ * 32 + 4)));
+      mbar_expect_tx(&s_bar[1], (uint32_t)((2 * D + 9) * 4));
+    } else {  // this CTA's elites (k, J): 12 bytes each
+      int n = 0;
+      for (int sl = 0; sl < mine; ++sl) n += max(0, min(kEliteGroup, Ke - ((int)rank + (int)C * sl) * kEliteGroup));
+      mbar_expect_tx(&s_bar[0], (uint32_t)(12 * n));
+    }
+  }
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // barriers initialised (waited before use)
+  if (rank != 0) {
+    load_robot(p, r, s, false);  // (the distribution: not written by the rollout)
+    griddep_wait();
+    griddep_launch_dependents();
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    if (rank == 1) {  // the header CTA 0 needs, while it selects
+      merge_diag(p, r, s_diag, false);
+      __syncthreads();
+      const uint32_t bar = cl_addr(&s_bar[1], 0);
+      for (int d = tid; d < D; d += blockDim.x) {
+        st_async(cl_addr(&s.mu[d], 0), s.mu[d], bar);
+        st_async(cl_addr(&s.sig[d], 0), s.sig[d], bar);
+      }
+      if (tid < 5) st_async(cl_addr(&s_diag[tid], 0), s_diag[tid], bar);
+      if (tid == 32) {
+        st_async(cl_addr(&s.cur_idx, 0), (uint32_t)s.cur_idx, bar);
+        st_async(cl_addr(&s.iter, 0), s.iter, bar);
+        st_async(cl_addr(&s_pre[0], 0), robot_in(p, r)->phase_q32, bar);
+        st_async(cl_addr(&s_pre[1], 0), s.iter, bar);
+      }
+    }
+    mbar_wait0(&s_bar[0]);  // this CTA's elites
+  } else {
+    griddep_wait();  // the rollout's J
+    griddep_launch_dependents();
+    if (blockIdx.y == 0) SBS_TS(16);
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // (long complete: the others' barriers exist)
+    select_block_small(p.J + (size_t)r * p.K_local, (int)p.K_local, Ke, p.k_begin, nullptr, nullptr, cem_smem, true,
+                       false);
+    if (blockIdx.y == 0) SBS_TS(24);
+    const int64_t* el = reinterpret_cast<const int64_t*>(cem_smem);  // select_block_small's staging
+    const float* eJ = reinterpret_cast<const float*>(el + Ke);
+    const int lc = __ffs((int)C) - 1;  // C = 2^lc
+    for (int e = tid; e < Ke; e += blockDim.x) {  // every CTA its groups' elites
+      const int g = e >> 5, dst = g & ((int)C - 1), i = ((g >> lc) << 5) + (e & 31);
+      if (dst != 0) {
+        const uint32_t bar = cl_addr(&s_bar[0], (uint32_t)dst);
+        st_async(cl_addr(&s_ek[i], (uint32_t)dst), el[e], bar);
+        st_async(cl_addr(&s_eJ[i], (uint32_t)dst), eJ[e], bar);
+      } else {
+        s_ek[i] = el[e];
+        s_eJ[i] = eJ[e];
+      }
+    }
+    for (int e = tid; e < Ke; e += blockDim.x) {  // the list in global memory too (sbs_debug_elites)
+      p.elite[(size_t)r * Ke + e] = el[e];
+      p.elite_J[(size_t)r * Ke + e] = eJ[e];
+    }
+    mbar_wait0(&s_bar[1]);  // CTA 1's header: the distribution for this CTA's own groups
+    __syncthreads();        // (and its own elites)
+  }
+  if (rank == 1 && blockIdx.y == 0) SBS_TS(17);
+  {
+    const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
+    const uint32_t bar = cl_addr(&s_bar[0], 0);
+    for (int t = warp; t < mine * NQ; t += kSelBlock / 32) {
+      const int slot = t / NQ, q = t - slot * NQ;
+      const int g = (int)rank + (int)C * slot, i = slot * kEliteGroup + lane;
+      const bool has_e = g * kEliteGroup + lane < Ke;
+      const int64_t k = has_e ? s_ek[i] : 0;
+      const float Je = has_e ? s_eJ[i] : kInf;
+      SBS_CHECK(k >= 0 && k < p.K_global);
+      const GroupMoments m = elite_group_moments(p, s, robot_g, has_e, k, Je, q);
+      float* rec = recs + g * RS;  // [S1[D] | S2[D] | n]
+      float* dst = rec + (m.j < 4 ? 4 * q + m.j : D + 4 * q + m.j - 4);
+      if (rank == 0) {
+        if ((lane & 3) == 0) *dst = m.t;
+        if (q == 0 && lane == 0) rec[2 * D] = m.n;
+      } else {
+        if ((lane & 3) == 0) st_async(cl_addr(dst, 0), m.t, bar);
+        if (q == 0 && lane == 0) st_async(cl_addr(rec + 2 * D, 0), m.n, bar);
+      }
+    }
+  }
+#if defined(SBS_TIMING)
+  __syncthreads();
+  if (rank == 0 && blockIdx.y == 0) SBS_TS(26);
+  if (rank == 1 && blockIdx.y == 0) SBS_TS(30);
+#endif
+  if (rank != 0) return;
+  mbar_wait0(&s_bar[0]);  // the other CTAs' records
+  __syncthreads();        // (and this CTA's own)
+  if (blockIdx.y == 0) SBS_TS(29);
+  if (tid < 2 * D + 1) {  // row tid of [S1 | n | S2] (the elite kernel's record order)
+    const int j = tid < D ? tid : (tid == D ? 2 * D : tid - 1);
+    float a0 = 0.f;  // records summed in group order (the elite kernel's order)
+#pragma unroll 8
+    for (int g = 0; g < G; ++g) a0 += recs[g * RS + j];
+    s_tot[tid] = a0;
+  }
+  __syncthreads();
+  if (blockIdx.y == 0) SBS_TS(25);
+  cem_finish<P>(p, r, s, s_tot, s_diag, s_pre, s_mean, s_var);
+  if (blockIdx.y == 0) SBS_TS(28);
 }
 
 // ---------------------------------------------------------------------------
@@ -2422,6 +2673,8 @@ struct PEntry {
   static cudaError_t rollout(const Params& p, int mode, bool fused, cudaStream_t s);
   static int occupancy(int mode, bool fc, bool split, bool model);
   static cudaError_t elite(const Params& p, cudaStream_t s);
+  static cudaError_t cem_cluster(const Params& p, cudaStream_t s);
+  static int cem_cluster_size(int want);
   static cudaError_t naive_finalize(const Params& p, cudaStream_t s);
   static cudaError_t debug_samples(const Params& p, int robot, int64_t k0, int64_t n, float* z, float* theta,
                                    int* fidx, cudaStream_t s);
@@ -2510,6 +2763,54 @@ cudaError_t PEntry<P>::elite(const Params& p, cudaStream_t s) {
 }
 
 template <int P>
+cudaError_t PEntry<P>::cem_cluster(const Params& p, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.cem_cluster, p.R);
+  cfg.blockDim = dim3(kSelBlock);
+  cfg.dynamicSmemBytes = kCemSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = p.cem_cluster;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, sbs_cem_cluster_kernel<P>, p);
+}
+
+// the largest cluster (of 16, 8; `want` caps it) that can be resident with the kernel's
+// block size and shared memory, 0 if none
+template <int P>
+int PEntry<P>::cem_cluster_size(int want) {
+  for (int c = 16; c >= 8; c /= 2) {
+    if (c > want) continue;
+    if (c > 8 && cudaFuncSetAttribute(sbs_cem_cluster_kernel<P>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                     cudaSuccess) {
+      (void)cudaGetLastError();
+      continue;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c, 1);
+    cfg.blockDim = dim3(kSelBlock);
+    cfg.dynamicSmemBytes = kCemSmemBytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, sbs_cem_cluster_kernel<P>, &cfg) == cudaSuccess && n > 0) return c;
+    (void)cudaGetLastError();
+  }
+  return 0;
+}
+
+template <int P>
 cudaError_t PEntry<P>::naive_finalize(const Params& p, cudaStream_t s) {
   sbs_naive_finalize_kernel<P><<<p.R, 128, 0, s>>>(p);
   return cudaGetLastError();
@@ -2538,6 +2839,8 @@ cudaError_t PEntry<P>::prepare() {
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_ARGMIN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              big);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(sbs_cov_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(sbs_cem_cluster_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCemSmemBytes);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(sbs_rollout_kernel<P, EPI_MPPI, true, false, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, huge);
@@ -2652,6 +2955,21 @@ int rollout_occupancy(int P, int mode, bool fc, bool split, bool model) {
 cudaError_t launch_elite(const Params& p, cudaStream_t s) {
   SBS_DISPATCH_P(p.P, elite(p, s));
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_cem_cluster(const Params& p, cudaStream_t s) {
+  SBS_DISPATCH_P(p.P, cem_cluster(p, s));
+  return cudaErrorInvalidValue;
+}
+
+int cem_cluster_size(int P, int want) {
+  SBS_DISPATCH_P(P, cem_cluster_size(want));
+  return 0;
+}
+
+bool cem_cluster_fits(const Params& p) {
+  return p.mode == SBS_CEM && !p.full_cov && p.K_local <= kSelSmallMax && p.n_eblk <= kCemMaxGroups &&
+         (int64_t)p.n_elite * (sizeof(int64_t) + sizeof(float)) <= (int64_t)kSelSmallSmemBytes;
 }
 
 cudaError_t launch_naive_finalize(const Params& p, cudaStream_t s) {

@@ -28,7 +28,7 @@ for name, (cfg, inputs) in [("c2", W.config2()), ("c3nv", W.config3("naive"))]:
         L.sbs_debug_bar_p4(bb)
         if it >= 5:
             bars.append(np.array(bb[:], dtype=np.float64).reshape(4, 8))
-        ts = (C.c_uint64 * 16)()
+        ts = (C.c_uint64 * 32)()
         L.sbs_debug_ts_p4(ts)
         a = np.array(buf[:], dtype=np.float64).reshape(256, 6)[:n]
         t0 = a[:, 0].min()

@@ -22,7 +22,7 @@ for name, (cfg, inputs) in [("c1", W.config1()), ("c2", W.config2()), ("c3cem", 
             flush.zero_()
         c.step_device(d_in.data_ptr(), d_out.data_ptr(), 0)
         torch.cuda.synchronize()
-        ts = (C.c_uint64 * 16)()
+        ts = (C.c_uint64 * 32)()
         L.sbs_debug_ts_p4(ts)
         t = np.array(ts[:11], dtype=np.float64)
         if it >= 5:

@@ -17,7 +17,7 @@ acc = []
 for it in range(30):
     c.step_device(d_in.data_ptr(), d_out.data_ptr(), 0)
     torch.cuda.synchronize()
-    ts = (C.c_uint64 * 16)()
+    ts = (C.c_uint64 * 32)()
     L.sbs_debug_ts_common(ts)
     t = np.array(ts[:7], dtype=np.float64)
     if it >= 5:

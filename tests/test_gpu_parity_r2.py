@@ -298,3 +298,67 @@ def test_config4_full_size_update_recomputed(B):
     assert outs[0]["omega"] == pytest.approx(omega, rel=1e-4)
     assert outs[0]["ess"] == pytest.approx(omega ** 2 / np.sum(w * w), rel=1e-3)
     assert outs[0]["j_min"] == beta
+
+
+# ---------------------------------------------------------------------------
+# a6: the one-launch CEM path (select + elite moments in one thread-block cluster)
+# ---------------------------------------------------------------------------
+def _pitched(inp):
+    inp = dict(inp)
+    x0 = inp["x0"].copy()
+    x0[7] = W.f32(1.0)
+    x0[10] = W.f32(8.0)
+    inp["x0"] = x0
+    return inp
+
+
+@pytest.mark.parametrize("case", ["config3", "ragged_R3", "max_groups", "one_elite", "diverged", "preserve"])
+def test_cem_cluster_path_is_bitwise_the_two_kernel_path(B, case, monkeypatch):
+    """CEM at world = 1 runs select + elite moments + finish as one cluster launch when
+    K <= 16384 and K_e <= 2048 (sbs_cem_cluster_kernel).  It performs the two-kernel
+    path's arithmetic in the same order (Alg. 1; L17), so means, variances,
+    outputs and elite lists are bitwise those of SBS_CEM_CLUSTER=0, over three
+    iterations; both are checked against the oracle elsewhere."""
+    R = 1
+    if case == "config3":
+        cfg, inputs = W.config3("cem", K=10000)
+    elif case == "ragged_R3":
+        R = 3
+        cfg = W.base_config(n_samples=3001, n_robots=R, mode="cem", n_elite=37)
+        inputs = [W.robot_input(cfg, r, cmd=(0.3 * r, 0.0, 0.1)) for r in range(R)]
+    elif case == "max_groups":
+        cfg = W.base_config(n_samples=16384, mode="cem", n_elite=2048)
+        inputs = [W.robot_input(cfg, 0, cmd=(0.5, 0.0, 0.0))]
+    elif case == "one_elite":
+        cfg = W.base_config(n_samples=64, mode="cem", n_elite=1)
+        inputs = [W.robot_input(cfg, 0)]
+    elif case == "diverged":  # fewer finite costs than elites
+        cfg, inputs = W.config3("cem", K=2100)
+        cfg = dict(cfg, n_elite=2048)
+        inputs = [_pitched(inputs[0])]
+    else:
+        cfg, inputs = W.config3("cem", K=4000)
+        cfg = dict(cfg, elite_preserve=0)
+    res = {}
+    for tag, env in (("cluster", None), ("cluster8", "8"), ("two", "0")):
+        monkeypatch.delenv("SBS_CEM_CLUSTER", raising=False)
+        if env is not None:
+            monkeypatch.setenv("SBS_CEM_CLUSTER", env)
+        c = _ctrl(B, cfg, inputs)
+        assert c.L.sbs_launches_per_step(c.ctx) == (3 if env == "0" else 2)
+        outs = [c.step(inputs)[1] for _ in range(3)]
+        res[tag] = (outs, [c.debug_elites(r).copy() for r in range(R)], c.debug_costs().copy())
+    ot, et, Jt = res["two"]
+    for tag in ("cluster", "cluster8"):
+        oc, ec, Jc = res[tag]
+        np.testing.assert_array_equal(Jc, Jt)
+        for r in range(R):
+            np.testing.assert_array_equal(ec[r], et[r])
+        for it in range(3):
+            for r in range(R):
+                for key in ("mean", "var", "u0", "j_min", "j_mean", "n_diverged", "freq_idx", "status", "iter"):
+                    np.testing.assert_array_equal(np.asarray(oc[it][r][key]), np.asarray(ot[it][r][key]),
+                                                  err_msg=f"{tag} {key}")
+    oc, _, Jc = res["cluster"]
+    if case == "diverged":
+        assert 0 < oc[0][0]["n_diverged"] and int(np.sum(np.isfinite(Jc[0]))) < cfg["n_elite"]
