@@ -536,10 +536,12 @@ struct StepForces {
 };
 constexpr int kStepForceFloats = 7;
 
-template <int P, class KC = DynC, class TH = Theta<P>>
+// MASK: the stance set as a compile-time constant (0: read from fl).  With a constant set
+// no accumulator needs its -0 start value in a register and no leg branches.
+template <int P, class KC = DynC, class TH = Theta<P>, uint32_t MASK = 0u>
 __device__ __forceinline__ StepForces step_forces(const Params& p, const TH& th, uint32_t fl, const float (&Wj)[P],
                                                   const RobotSmem& s) {
-  const float urz = KC::urz(p, __popc(fl & 0xFu));
+  const float urz = KC::urz(p, MASK ? __popc(MASK) : __popc(fl & 0xFu));
   // accumulators start at -0 (the additive identity), so the first add is not a real op
   StepForces o;
   o.F = f2(-0.f, -0.f);
@@ -548,7 +550,7 @@ __device__ __forceinline__ StepForces step_forces(const Params& p, const TH& th,
   float penz = -0.f, effz = -0.f;
 #pragma unroll
   for (int leg = 0; leg < 4; ++leg) {
-    if (fl & (1u << leg)) {
+    if ((MASK ? MASK : fl) & (1u << leg)) {
       float2 g;
       float gz;
       th.spline(leg, Wj, g, gz);
@@ -584,6 +586,20 @@ __device__ __forceinline__ StepForces step_forces(const Params& p, const TH& th,
   const float eff_s = (eff.x + eff.y) + effz;
   o.ju = fmaf(KC::w_fc(p), pen_s, KC::kStatic ? KC::Rw(p, 0) * eff_s : eff_s);
   return o;
+}
+
+// The stance sets of a trot (one diagonal pair, or all four legs in the double-support
+// phases of D_f > 0.5) as compile-time sets; any other set at run time.  Every lane of a
+// warp shares the set under a fixed gait, so the switch does not diverge there.
+template <int P, class KC = DynC, class TH = Theta<P>>
+__device__ __forceinline__ StepForces step_forces_any(const Params& p, const TH& th, uint32_t fl, const float (&Wj)[P],
+                                                      const RobotSmem& s) {
+  switch (fl & 0xFu) {
+    case 0x9u: return step_forces<P, KC, TH, 0x9u>(p, th, fl, Wj, s);
+    case 0x6u: return step_forces<P, KC, TH, 0x6u>(p, th, fl, Wj, s);
+    case 0xFu: return step_forces<P, KC, TH, 0xFu>(p, th, fl, Wj, s);
+    default: return step_forces<P, KC, TH, 0u>(p, th, fl, Wj, s);
+  }
 }
 
 // Latency mode, force-producer side: table [H][kStepForceFloats][kBlock] in shared
@@ -707,7 +723,7 @@ static __device__ float rollout(const Params& p, const TH& th, int fi, const Rob
     float Wj[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) Wj[q] = p.W[j][q];
-    const StepForces sf = step_forces<P, KC>(p, th, ct[j], Wj, s);
+    const StepForces sf = step_forces_any<P, KC>(p, th, ct[j], Wj, s);
     J += state_cost(p, &s.xref[12 * j], pxy, vxy, pz, vz, A, Bq, C) + sf.ju;
     srbd_step<KC>(p, sf, pxy, vxy, pz, vz, A, Bq, C);
     bad = bad || diverged(pxy, vxy, pz, vz, A, Bq, C);
@@ -768,7 +784,7 @@ __device__ __forceinline__ void produce_forces(const Params& p, const RobotSmem&
       float Wj[P];
 #pragma unroll
       for (int q = 0; q < P; ++q) Wj[q] = p.W[j][q];
-      store_forces(tab, j, col, step_forces<P, KC>(p, th, ct[j], Wj, s));
+      store_forces(tab, j, col, step_forces_any<P, KC>(p, th, ct[j], Wj, s));
     }
     named_arrive(1 + c, kBlock * (1 + kAbWarpsPerSmsp));
   }
