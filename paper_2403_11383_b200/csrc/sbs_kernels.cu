@@ -1897,6 +1897,12 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
   const int k0 = tid * per;
   const int nk = max(0, min(per, K - k0));
   uint32_t key[kSelKPT];
+#if defined(SBS_TIMING_FIRSTLOAD)  // (timing experiment: the first load alone)
+  if (tid == 0) {
+    const float j0 = *(volatile const float*)&J[0];
+    if (blockIdx.x == 0 && j0 != 12345.f) SBS_TS(kSelTs + 1);
+  }
+#endif
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i) key[i] = i < nk ? cost_key(J[k0 + i]) : 0xFFFFFFFFu;
   if (blockIdx.x == 0) SBS_TS(kSelTs + 2);
@@ -2407,7 +2413,7 @@ __global__ void __launch_bounds__(kSelBlock) sbs_cem_cluster_kernel(const __grid
     mbar_wait0(&s_bar[1]);  // CTA 1's header: the distribution for this CTA's own groups
     __syncthreads();        // (and its own elites)
   }
-  if (rank == 1 && blockIdx.y == 0) SBS_TS(17);
+  if (rank == 1 && blockIdx.y == 0) SBS_TS(22);
   {
     const uint32_t robot_g = (uint32_t)(p.robot_offset + r);
     const uint32_t bar = cl_addr(&s_bar[0], 0);

@@ -36,8 +36,8 @@ for fl in (False, True):
         t0 = a[0]
         if os.environ.get("SBS_CEM_CLUSTER", "1") != "0":  # one-launch path: slots 16.. of the P TU
             row = [(a[4] - t0), (a[16] - t0), (a[16 + 2] - t0), (a[16 + 3] - t0), (a[16 + 4] - t0), (a[16 + 5] - t0),
-                   (a[16 + 7] - t0), (a[24] - t0), (a[17] - t0), (a[26] - t0), (a[30] - t0), (a[29] - t0),
-                   (a[28] - t0), e0.elapsed_time(e1) * 1e3, (a[25] - t0)]
+                   (a[16 + 7] - t0), (a[24] - t0), (a[22] - t0), (a[26] - t0), (a[30] - t0), (a[29] - t0),
+                   (a[28] - t0), e0.elapsed_time(e1) * 1e3, (a[25] - t0), (a[17 + 0] - t0)]
             if it >= 5:
                 acc.append(np.array(row, dtype=np.float64))
             continue
@@ -49,7 +49,7 @@ for fl in (False, True):
     if os.environ.get("SBS_CEM_CLUSTER", "1") != "0":
         m[:13] /= 1e3
         print(f"{sys.argv[1] if len(sys.argv) > 1 else ''} {'flushed' if fl else 'warm'} cluster: rollout CTA0 record {m[0]:.2f} | "
-              f"released {m[1]:.2f} keys {m[2]:.2f} pass1-2 {m[3]:.2f} pass3 {m[4]:.2f} scan {m[5]:.2f} compact {m[6]:.2f} "
+              f"released {m[1]:.2f} first load {m[15] / 1e3:.2f} keys {m[2]:.2f} pass1-2 {m[3]:.2f} pass3 {m[4]:.2f} scan {m[5]:.2f} compact {m[6]:.2f} "
               f"selected {m[7]:.2f} | rank1 elites in {m[8]:.2f} | regen done rank0 {m[9]:.2f} rank1 {m[10]:.2f} | "
               f"records in {m[11]:.2f} summed {m[14] / 1e3:.2f} | end {m[12]:.2f} | events {m[13]:.2f} us")
         continue
