@@ -751,11 +751,15 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.cand = c->d_cand;
   // CEM at world = 1: select + elite moments + finish as one cluster launch (bitwise the
   // two-kernel path's results; SBS_CEM_CLUSTER=0 keeps the two kernels, for tests / A/B)
-  // (SBS_CEM_CLUSTER=8 / 16 caps the cluster size)
+  // (SBS_CEM_CLUSTER=8 / 16 caps the cluster size).  A latency path: every robot occupies
+  // a whole cluster of SMs, so it is taken only while all R clusters fit the GPU at once
+  // (many robots keep the two kernels: one select SM per robot).
   P.cem_cluster = 0;
   if (cfg->world == 1 && sbs::cem_cluster_fits(P)) {
     const char* e = getenv("SBS_CEM_CLUSTER");
-    P.cem_cluster = sbs::cem_cluster_size(P.P, e ? atoi(e) : 16);
+    int want = e ? atoi(e) : 16;
+    while (want >= 8 && (int64_t)R * want > c->sm_count) want /= 2;
+    P.cem_cluster = want >= 8 ? sbs::cem_cluster_size(P.P, want) : 0;
   }
   c->ref_set.assign(R, 0);
   // ---- NCCL (sample sharding) ----

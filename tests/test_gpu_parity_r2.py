@@ -362,3 +362,16 @@ def test_cem_cluster_path_is_bitwise_the_two_kernel_path(B, case, monkeypatch):
     oc, _, Jc = res["cluster"]
     if case == "diverged":
         assert 0 < oc[0][0]["n_diverged"] and int(np.sum(np.isfinite(Jc[0]))) < cfg["n_elite"]
+
+
+def test_cem_cluster_path_only_while_the_clusters_fit(B):
+    """The one-launch CEM path gives every robot a cluster of 16 (or 8) SMs; with more
+    robots than the GPU holds clusters at once the select + elite kernels (one select SM
+    per robot) are the better trade, and sbs_create keeps them."""
+    import torch
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    for R, launches in ((1, 2), (n_sm // 16, 2), (n_sm // 8 + 1, 3)):
+        cfg = W.base_config(n_samples=1024, n_robots=R, mode="cem", n_elite=64)
+        c = B.Controller(cfg)
+        assert c.L.sbs_launches_per_step(c.ctx) == launches, (R, launches)
+        c.close()
