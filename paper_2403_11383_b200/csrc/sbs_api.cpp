@@ -116,6 +116,8 @@ struct sbs_ctx {
   int* d_counter = nullptr;
   float* d_epart = nullptr;
   float* d_sdiag = nullptr;
+  float* d_dyn_rec = nullptr;  // dynamic tile scheduling: tile and subtree records
+  int* d_dyn_cnt = nullptr;    // ... its counters
   sbs_input* d_in = nullptr;
   sbs_output* d_out = nullptr;
   // host path staging: one pinned block [iter | R inputs | R x H x 12 reference], one H2D per step
@@ -476,7 +478,7 @@ void sbs_destroy(sbs_ctx* c) {
   for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
   for (void* p : {(void*)c->d_mean, (void*)c->d_var, (void*)c->d_fidx, (void*)c->d_J,
                   (void*)c->d_part, (void*)c->d_xbuf, (void*)c->d_elite, (void*)c->d_best, (void*)c->d_status, (void*)c->d_counter, (void*)c->d_epart, (void*)c->d_sdiag, (void*)c->d_eJ, (void*)c->d_cand, (void*)c->d_L,
-                  (void*)c->d_out})
+                  (void*)c->d_out, (void*)c->d_dyn_rec, (void*)c->d_dyn_cnt})
     if (p) cudaFree(p);
   if (c->h_out) cudaFreeHost(c->h_out);  // (h_in and h_xref point into h_blk)
   if (c->graph) cudaGraphExecDestroy(c->graph);
@@ -749,6 +751,34 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.elite_J = c->d_eJ;
   P.Lmat = c->d_L;
   P.cand = c->d_cand;
+  // throughput-mode MPPI for one robot with several tiles per CTA: dynamic tile scheduling
+  // (the CTAs sharing an SM do not progress at the same rate, so a static tile split ends
+  // with SMs running one or two CTAs; SBS_DYN=0 keeps the static split, for tests / A/B)
+  P.dyn = 0;
+  if (cfg->mode == SBS_MPPI && R == 1 && !P.split && !P.full_cov && P.n_tiles >= 2 * P.n_cta) {
+    const char* e = getenv("SBS_DYN");
+    P.dyn = (!e || atoi(e) != 0) ? 1 : 0;
+  }
+  if (P.dyn) {
+    int n = P.n_tiles, L = 0, recs = 0, cnts = 2;
+    P.dyn_n[0] = n;
+    while (n > 1) {
+      P.dyn_off[L] = recs;
+      recs += n;
+      n = (n + sbs::kDynFan - 1) / sbs::kDynFan;
+      ++L;
+      if (L > sbs::kDynMaxLevels) return bail(SBS_ERR_INVALID_ARG);
+      P.dyn_n[L] = n;
+      P.dyn_coff[L] = cnts;
+      cnts += n;
+    }
+    P.dyn_levels = L;
+    CKC(cudaMalloc(&c->d_dyn_rec, (size_t)recs * P.part_stride * sizeof(float)));
+    CKC(cudaMalloc(&c->d_dyn_cnt, (size_t)cnts * sizeof(int)));
+    CKC(cudaMemset(c->d_dyn_cnt, 0, (size_t)cnts * sizeof(int)));
+    P.dyn_rec = c->d_dyn_rec;
+    P.dyn_cnt = c->d_dyn_cnt;
+  }
   // CEM at world = 1: select + elite moments + finish as one cluster launch (bitwise the
   // two-kernel path's results; SBS_CEM_CLUSTER=0 keeps the two kernels, for tests / A/B)
   // (SBS_CEM_CLUSTER=8 / 16 caps the cluster size).  A latency path: every robot occupies

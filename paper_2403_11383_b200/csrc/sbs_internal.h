@@ -34,6 +34,9 @@ constexpr int kInlineRefFloats = 16 * 12;  // host path, R = 1, H <= 16: inputs 
 constexpr int kSplitLanes = 4;      // latency-mode (SPLIT) rollout: lanes per sample in the sampler phase
 constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, nfin, pad]
 constexpr int kEPartStride = 2 * SBS_MAX_D + 4;  // CEM elite-moment record [S1[D], n, S2[D]]
+constexpr int kDynFan = 64;                     // dynamic tile scheduling: reduction-tree fan-in
+constexpr int kDynMaxLevels = 5;                // 64^5 tiles
+constexpr int kDynBatch = 8;                    // tiles per release fence
 // full-covariance CEM elite record [S1[D], n, lower triangle of S2 (D (D + 1) / 2)], 16-byte multiple
 __host__ __device__ constexpr int fc_record_floats(int D) { return ((D + 1 + D * (D + 1) / 2) + 3) / 4 * 4; }
 // latency-mode shared memory: MPPI reduction rows, theta / theta1 of the tile, and (ab)
@@ -88,6 +91,16 @@ struct Params {
   int ab;                     // latency mode: 12 producer warps tabulate the stance-leg forces for the 4 integrator warps
   int full_cov;               // f3 (L42): CEM with a full covariance C = L L^T
   int cem_cluster;            // CEM at world = 1: cluster size of the one-launch select + elite path, 0: two kernels
+  // throughput-mode MPPI with dynamic tile scheduling (one robot): tiles are taken from a
+  // counter and reduced by a fixed tree of fan-in kDynFan over the tile index, so the result
+  // does not depend on which CTA ran which tile
+  int dyn;                    // 1: on
+  int dyn_levels;             // L: tree levels above the tiles (level L is the root)
+  int dyn_n[kDynMaxLevels + 1];     // nodes per level (dyn_n[0] = n_tiles, dyn_n[L] = 1)
+  int dyn_off[kDynMaxLevels + 1];   // record offset of level l in dyn_rec (levels 0..L-1)
+  int dyn_coff[kDynMaxLevels + 1];  // arrival counters of level l (1..L) in dyn_cnt
+  float* dyn_rec;             // [sum_l dyn_n[l]][part_stride] tile and subtree records
+  int* dyn_cnt;               // [0]: next tile, [1]: CTAs done, then the level counters
   int model;                  // 1: the constants equal the compiled-in robot model (sbs_robot_model.h)
   float* Lmat;                // [R][D][D] lower Cholesky factor (row-major), full_cov only
   int n_sig_groups;           // multiple Gaussians (L41): sample k uses sig_scale[k mod n_sig_groups]

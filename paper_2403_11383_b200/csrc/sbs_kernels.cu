@@ -47,11 +47,11 @@ __device__ unsigned long long g_sbs_ts[32];  // [16, 32): the CEM cluster kernel
       g_sbs_ts[i] = t_;                                                         \
     }                                                                           \
   } while (0)
-__device__ unsigned long long g_sbs_cta[256][6];
+__device__ unsigned long long g_sbs_cta[1024][6];
 __device__ unsigned long long g_sbs_bar[4][8];  // integrator warp x chunk: cycles waiting on the chunk barrier (CTA 0)  // per CTA: globaltimer x4, clock64 around the rollout
 #define SBS_CTS(i)                                                              \
   do {                                                                          \
-    if (threadIdx.x == 0 && blockIdx.x < 256 && blockIdx.y == 0) {              \
+    if (threadIdx.x == 0 && blockIdx.x < 1024 && blockIdx.y == 0) {             \
       unsigned long long t_;                                                    \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
       g_sbs_cta[blockIdx.x][i] = (i) >= 4 ? (unsigned long long)clock64() : t_; \
@@ -893,13 +893,14 @@ struct Best {
   float m;
   int k, f;
 };
-static __device__ Best merge_argmin(const Params& p, int r) {
+static __device__ Best merge_argmin(const Params& p, int r, const float* recs = nullptr, int nrec = 0) {
   __shared__ float s_m[32];
   __shared__ int s_k[32], s_f[32];
   float m = kInf;
   int mk = 0x7fffffff, mf = 0;
-  for (int c = threadIdx.x; c < p.n_cta; c += blockDim.x) {
-    const float* pc = part_rec(p, r, c);
+  const int nc = recs ? nrec : p.n_cta;
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    const float* pc = recs ? recs + (size_t)c * p.part_stride : part_rec(p, r, c);
     const float mc = __ldcg(pc);
     const int kc = __float_as_int(__ldcg(pc + 1));
     if (jk_less(mc, kc, m, mk)) {
@@ -925,11 +926,13 @@ static __device__ Best merge_argmin(const Params& p, int r) {
 // ---------------------------------------------------------------------------
 // MPPI UpdateMean (Alg. 4) over the partial records of robot r:
 // beta = min_c m_c; every record is rescaled by exp(-(m_c - beta)/lambda);
-// theta_new = sum V / sum S.  EMIT: write the merged record (rank partial)
-// instead of finishing.  blockDim.x = 128; rows split over two column groups.
+// theta_new = sum V / sum S.  EMIT: write the merged record (rank partial, or
+// out_rec) instead of finishing.  The records: the CTA records of robot r
+// (part_rec), or recs[0..nrec) (contiguous, stride part_stride).  blockDim.x = 128.
 // ---------------------------------------------------------------------------
 template <bool EMIT>
-static __device__ void mppi_merge_block(const Params& p, int r, float* emit, float* stage, int stage_floats) {
+static __device__ void mppi_merge_block(const Params& p, int r, float* emit, float* stage, int stage_floats,
+                                        const float* recs = nullptr, int nrec = 0, float* out_rec = nullptr) {
   const int tid = threadIdx.x, D = p.D, NR = D + 4, RL = p.part_stride;
   __shared__ float s_row[1][SBS_MAX_D + 4];
   __shared__ float s_sc[128];
@@ -938,13 +941,15 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   __shared__ float s_bm[32];
   __shared__ int s_bk[32], s_bf[32];
   __shared__ float s_part[16 * (SBS_MAX_D + 4)];
-  const int nc = p.n_cta;
+  const int nc = recs ? nrec : p.n_cta;
   const bool one_pass = nc <= 128 && nc * RL <= stage_floats;
   Best b;
   float bmin = kInf;
   if (one_pass) {
     // one load round trip: every record, this robot's variance, input phase and iteration counter
-    if (p.part_c_stride == 1) {
+    if (recs) {
+      stage_copy(stage, recs, nc * RL);
+    } else if (p.part_c_stride == 1) {
       stage_copy(stage, part_rec(p, r, 0), nc * RL);  // records of a robot are contiguous
     } else {
       for (int c = 0; c < nc; ++c) stage_copy(stage + c * RL, part_rec(p, r, c), RL);
@@ -985,7 +990,7 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
       }
     }
   } else {
-    b = merge_argmin(p, r);
+    b = merge_argmin(p, r, recs, nrec);
   }
   SBS_TS(8);
   const float beta = one_pass ? bmin : b.m;  // (one pass: b is read after the row sums' barrier)
@@ -994,7 +999,9 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   for (int c0 = 0; c0 < nc; c0 += CH) {
     const int n = min(CH, nc - c0);
     if (!one_pass) {
-      if (p.part_c_stride == 1) {
+      if (recs) {
+        stage_copy(stage, recs + (size_t)c0 * RL, n * RL);
+      } else if (p.part_c_stride == 1) {
         stage_copy(stage, part_rec(p, r, c0), n * RL);
       } else {
         for (int c = 0; c < n; ++c) stage_copy(stage + c * RL, part_rec(p, r, c0 + c), RL);
@@ -1069,7 +1076,7 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   if (one_pass) b = Best{s_bm[0], s_bk[0], s_bf[0]};  // (warp 0's argmin, ordered by the barriers above)
   SBS_TS(9);
   if (EMIT) {  // this rank's merged record, relative to its own beta
-    float* o = emit + (size_t)r * p.part_stride;
+    float* o = out_rec ? out_rec : emit + (size_t)r * p.part_stride;
     if (tid < D) o[kPartHdr + tid] = s_row[0][tid];
     else if (tid < NR) o[3 + tid - D] = s_row[0][tid];
     if (tid == 0) {
@@ -1272,7 +1279,71 @@ static __device__ void publish_to_peers(const Params& p) {
 enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
 
 
-template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false, bool AB = false, bool MODEL = false>
+// thread 0: the level-1 arrivals of the buffered tiles behind one release fence (one
+// fence per kDynBatch tiles instead of per tile: a fence waits for the CTA's writes)
+__device__ __forceinline__ void dyn_arrive(const Params& p, const int* pend, int& n_pend) {
+  if (n_pend == 0) return;
+  __threadfence();
+#pragma unroll
+  for (int i = 0; i < kDynBatch; ++i)
+    if (i < n_pend) atomicAdd(p.dyn_cnt + p.dyn_coff[1] + pend[i] / kDynFan, 1);
+  n_pend = 0;
+}
+
+// Dynamic tile scheduling (Params::dyn): the tiles' records are reduced by a fixed tree
+// of fan-in kDynFan over the tile index.  Once its tile loop is over, CTA c merges the
+// level-1 nodes c, c + n_cta, ... in index order, each as soon as its tiles' arrivals are
+// all in (a CTA takes a tile only while running, so every awaited tile is in a running
+// CTA that does not wait itself), then climbs: the CTA completing a higher node (one
+// arrival counter per node) merges it likewise; the root's merge finishes the iteration
+// (or emits the rank record).  The tree and its merge order are fixed by the tile indices
+// alone, so the result is the same whichever CTA ran which tile.
+static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int stage_floats) {
+  const int RL = p.part_stride, L = p.dyn_levels;
+  __shared__ int s_go;
+  for (int node = blockIdx.x; node < p.dyn_n[1]; node += gridDim.x) {
+    if (threadIdx.x == 0) {  // wait for the node's tile records (acquire)
+      int* c = p.dyn_cnt + p.dyn_coff[1] + node;
+      const int nk = min(kDynFan, p.dyn_n[0] - node * kDynFan);
+      for (;;) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+        if (v >= nk) break;
+        __nanosleep(128);
+      }
+      *c = 0;  // re-armed (nothing else touches it this launch)
+      s_go = 1;
+    }
+    __syncthreads();
+    int idx = node;
+    for (int l = 1; l <= L; ++l) {
+      if (l > 1) {  // arrive at the level-l node; its last arrival merges it
+        const int nkids_up = min(kDynFan, p.dyn_n[l - 1] - (idx / kDynFan) * kDynFan);
+        if (!arrive_last(p.dyn_cnt + p.dyn_coff[l] + idx / kDynFan, nkids_up)) break;
+        idx /= kDynFan;
+      }
+      const int nkids = min(kDynFan, p.dyn_n[l - 1] - idx * kDynFan);
+      const float* kids = p.dyn_rec + (size_t)(p.dyn_off[l - 1] + idx * kDynFan) * RL;
+      if (l < L) {
+        mppi_merge_block<true>(p, r, nullptr, stage, stage_floats, kids, nkids,
+                               p.dyn_rec + (size_t)(p.dyn_off[l] + idx) * RL);
+      } else if (p.emit) {  // world > 1: this rank's record (the exchange and rank-order merge follow)
+        SBS_TS(5);
+        mppi_merge_block<true>(p, r, p.emit, stage, stage_floats, kids, nkids);
+        publish_to_peers(p);
+        SBS_TS(6);
+      } else {
+        SBS_TS(5);
+        mppi_merge_block<false>(p, r, nullptr, stage, stage_floats, kids, nkids);
+        SBS_TS(6);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int P, int EPI, bool FUSED, bool FC = false, bool SPLIT = false, bool AB = false, bool MODEL = false,
+          bool DYN = false>
 __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ? 1 : kRolloutMinBlocks)
     sbs_rollout_kernel(const __grid_constant__ Params p) {
   using KC = typename std::conditional<MODEL, ModelC, DynC>::type;  // compiled-in robot model, or the parameter block
@@ -1324,7 +1395,20 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
   if (blockIdx.x == 0) SBS_TS(1);
   float run = 0.0f;  // running partial of row `tid` (MPPI)
 
-  for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+  // dynamic tile scheduling (throughput MPPI, one robot): the next tile index is fetched
+  // at the start of each tile (s_nx[par], read after the tile's last barrier)
+  constexpr bool dyn = DYN;  // (its own instantiation: the static kernel's registers are unchanged)
+  static_assert(!DYN || (EPI == EPI_MPPI && FUSED && !SPLIT && !FC), "dynamic tiles: throughput MPPI only");
+  __shared__ int s_nx[2];
+  __shared__ int s_pend[kDynBatch];  // thread 0: tiles whose level-1 arrivals are batched behind one fence
+  int n_pend = 0;
+  if (dyn) {  // every tile from the counter, the first one too
+    if (tid == 0) s_nx[1] = atomicAdd(p.dyn_cnt, 1);
+    __syncthreads();
+  }
+  for (int tile = dyn ? s_nx[1] : (int)blockIdx.x; tile < p.n_tiles; tile = dyn ? s_nx[par ^ 1] : tile + (int)gridDim.x) {
+    int nx = 0;  // (the next tile's index is consumed only at the tile's end: no wait here)
+    if (dyn && tid == 0) nx = atomicAdd(p.dyn_cnt, 1);
     const int64_t kl = (int64_t)tile * TS + tid;
     const bool valid = sampler_thread && kl < p.K_local;
     const int64_t k = p.k_begin + kl;
@@ -1536,11 +1620,23 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
         }
         v = (a01.x + a01.y) + (a23.x + a23.y);
       }
-      const float sa = (mr < kInf) ? __expf((mn - mr) * p.inv_lambda) : 0.0f;
-      const float sb = (mt < kInf) ? __expf((mn - mt) * p.inv_lambda) : 0.0f;
-      if (tid < D + 1) run = fmaf(run, sa, v * sb);
-      else if (tid == D + 1) run = fmaf(run, sa * sa, v * (sb * sb));
-      else run += v;
+      if (dyn) {  // this tile's record (relative to its own minimum mt)
+        float* o = p.dyn_rec + (size_t)tile * p.part_stride;
+        if (tid < D) o[kPartHdr + tid] = v;
+        else o[3 + tid - D] = v;
+        if (tid == 0) {
+          o[0] = mt;
+          o[1] = __int_as_float(tk);
+          o[2] = __int_as_float(tf);
+          o[7] = 0.0f;
+        }
+      } else {
+        const float sa = (mr < kInf) ? __expf((mn - mr) * p.inv_lambda) : 0.0f;
+        const float sb = (mt < kInf) ? __expf((mn - mt) * p.inv_lambda) : 0.0f;
+        if (tid < D + 1) run = fmaf(run, sa, v * sb);
+        else if (tid == D + 1) run = fmaf(run, sa * sa, v * (sb * sb));
+        else run += v;
+      }
     }
     if (SPLIT) {
       if (jk_less(mt, tk, h_m, h_k)) {
@@ -1554,45 +1650,61 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
       s_rk[par ^ 1] = t ? tk : s_rk[par];
       s_rf[par ^ 1] = t ? tf : s_rf[par];
     }
+    if (dyn && tid == 0) s_nx[par] = nx;
     par ^= 1;
     if (!SPLIT) __syncthreads();  // (measured: throughput mode runs faster with the CTA's warps in step)
+    if (dyn && tid == 0) {  // (the tile's record is written: barrier above)
+      s_pend[n_pend++] = tile;
+      if (n_pend == kDynBatch) dyn_arrive(p, s_pend, n_pend);
+    }
   }
   // the next iteration's kernels may be scheduled.  Not for the CEM rollout: a select
   // kernel scheduled early, next to the running rollout, was measured 1.5x slower
   // after an L2 flush (its CTA then starts at grid completion, still PDL-ordered)
   if (FUSED || p.cem_cluster) griddep_launch_dependents();  // (the CEM cluster kernel starts on idle SMs)
-  SBS_CHECK((int)blockIdx.x < p.n_cta && r < p.R);
-  float* out = p.part + ((size_t)r * p.n_cta + blockIdx.x) * p.part_stride;
-  if (EPI == EPI_MPPI) {
-    if (tid < D) out[kPartHdr + tid] = run;
-    else if (tid < NR) out[3 + tid - D] = run;
-  } else if (tid == 0) {
-    out[3] = 0.f;
-    out[4] = 0.f;
-    out[5] = SPLIT ? h_sj : s_rsj;
-    out[6] = SPLIT ? h_nf : s_rnf;
-  }
-  if (tid == 0) {
-    const int hp = EPI == EPI_MPPI ? par : 0;
-    out[0] = SPLIT ? h_m : s_rm[hp];
-    out[1] = __int_as_float(SPLIT ? h_k : s_rk[hp]);
-    out[2] = __int_as_float(SPLIT ? h_f : s_rf[hp]);
-    out[7] = 0.0f;
-  }
-  if (blockIdx.x == 0) SBS_TS(4);
-  SBS_CTS(3);
-  if (FUSED) {
-    if (arrive_last(p.counter + r, gridDim.x)) {
-      SBS_TS(5);
-      if (p.emit) {  // world > 1: this rank's record per robot (the exchange and rank-order merge follow)
-        if (EPI == EPI_MPPI) mppi_merge_block<true>(p, r, p.emit, s_red, NR * kRedStride);
-        else merge_diag(p, r, p.emit + (size_t)r * p.ex_stride, true);
-        publish_to_peers(p);
-      } else {
-        if (EPI == EPI_MPPI) mppi_merge_block<false>(p, r, nullptr, s_red, NR * kRedStride);
-        else naive_finalize_block<P>(p, r, s);
+  if constexpr (DYN) {
+    SBS_CTS(3);
+    if (tid == 0) dyn_arrive(p, s_pend, n_pend);
+    dyn_merge_nodes(p, r, s_red, NR * kRedStride);
+    // the last CTA to leave re-arms the tile counter (every CTA has taken its last index)
+    if (tid == 0 && atomicAdd(p.dyn_cnt + 1, 1) == (int)gridDim.x - 1) {
+      p.dyn_cnt[0] = 0;
+      p.dyn_cnt[1] = 0;
+    }
+  } else {
+    SBS_CHECK((int)blockIdx.x < p.n_cta && r < p.R);
+    float* out = p.part + ((size_t)r * p.n_cta + blockIdx.x) * p.part_stride;
+    if (EPI == EPI_MPPI) {
+      if (tid < D) out[kPartHdr + tid] = run;
+      else if (tid < NR) out[3 + tid - D] = run;
+    } else if (tid == 0) {
+      out[3] = 0.f;
+      out[4] = 0.f;
+      out[5] = SPLIT ? h_sj : s_rsj;
+      out[6] = SPLIT ? h_nf : s_rnf;
+    }
+    if (tid == 0) {
+      const int hp = EPI == EPI_MPPI ? par : 0;
+      out[0] = SPLIT ? h_m : s_rm[hp];
+      out[1] = __int_as_float(SPLIT ? h_k : s_rk[hp]);
+      out[2] = __int_as_float(SPLIT ? h_f : s_rf[hp]);
+      out[7] = 0.0f;
+    }
+    if (blockIdx.x == 0) SBS_TS(4);
+    SBS_CTS(3);
+    if (FUSED) {
+      if (arrive_last(p.counter + r, gridDim.x)) {
+        SBS_TS(5);
+        if (p.emit) {  // world > 1: this rank's record per robot (the exchange and rank-order merge follow)
+          if (EPI == EPI_MPPI) mppi_merge_block<true>(p, r, p.emit, s_red, NR * kRedStride);
+          else merge_diag(p, r, p.emit + (size_t)r * p.ex_stride, true);
+          publish_to_peers(p);
+        } else {
+          if (EPI == EPI_MPPI) mppi_merge_block<false>(p, r, nullptr, s_red, NR * kRedStride);
+          else naive_finalize_block<P>(p, r, s);
+        }
+        SBS_TS(6);
       }
-      SBS_TS(6);
     }
   }
 }
@@ -2724,6 +2836,11 @@ static cudaError_t launch_rollout_m(const Params& p, cudaStream_t s) {
                         split_smem_bytes(P, EPI == EPI_MPPI, p.H, true), 1, s, p);
   }
   const size_t smem = SPLIT ? split_smem_bytes(P, EPI == EPI_MPPI, p.H, false) : rollout_smem<P, EPI, FC, SPLIT>();
+  if constexpr (EPI == EPI_MPPI && FUSED && !SPLIT && !FC) {
+    if (p.dyn)
+      return launch_pdl(sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT, false, MODEL, true>, grid, dim3(kBlock), smem, 1,
+                        s, p);
+  }
   return launch_pdl(sbs_rollout_kernel<P, EPI, FUSED, FC, SPLIT, false, MODEL>, grid,
                     dim3(SPLIT ? kBlock * kSplitLanes : kBlock), smem, 1, s, p);
 }

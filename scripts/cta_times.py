@@ -22,7 +22,7 @@ for name, (cfg, inputs) in [("c2", W.config2()), ("c3nv", W.config3("naive"))]:
     for it in range(30):
         c.step_device(d_in.data_ptr(), d_out.data_ptr(), 0)
         torch.cuda.synchronize()
-        buf = (C.c_uint64 * (256 * 6))()
+        buf = (C.c_uint64 * (1024 * 6))()
         L.sbs_debug_cta_p4(buf)
         bb = (C.c_uint64 * 32)()
         L.sbs_debug_bar_p4(bb)
@@ -30,7 +30,7 @@ for name, (cfg, inputs) in [("c2", W.config2()), ("c3nv", W.config3("naive"))]:
             bars.append(np.array(bb[:], dtype=np.float64).reshape(4, 8))
         ts = (C.c_uint64 * 32)()
         L.sbs_debug_ts_p4(ts)
-        a = np.array(buf[:], dtype=np.float64).reshape(256, 6)[:n]
+        a = np.array(buf[:], dtype=np.float64).reshape(1024, 6)[:n]
         t0 = a[:, 0].min()
         rel = (a[:, :4] - t0) / 1e3
         cyc = a[:, 5] - a[:, 4]
