@@ -760,12 +760,17 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
     P.dyn = (!e || atoi(e) != 0) ? 1 : 0;
   }
   if (P.dyn) {
+    // fan-in 64 (measured against 32 and 122, the most one merge stages in the rollout's
+    // reduction buffer); SBS_DYN_FAN overrides (experiments)
+    P.dyn_fan = 64;
+    if (const char* e = getenv("SBS_DYN_FAN")) P.dyn_fan = std::max(2, atoi(e));
+    P.dyn_fan = std::min(P.dyn_fan, std::min(128, (D + 4) * (sbs::kBlock + 4) / (int)P.part_stride));
     int n = P.n_tiles, L = 0, recs = 0, cnts = 2;
     P.dyn_n[0] = n;
     while (n > 1) {
       P.dyn_off[L] = recs;
       recs += n;
-      n = (n + sbs::kDynFan - 1) / sbs::kDynFan;
+      n = (n + P.dyn_fan - 1) / P.dyn_fan;
       ++L;
       if (L > sbs::kDynMaxLevels) return bail(SBS_ERR_INVALID_ARG);
       P.dyn_n[L] = n;

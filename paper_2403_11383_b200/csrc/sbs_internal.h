@@ -34,8 +34,7 @@ constexpr int kInlineRefFloats = 16 * 12;  // host path, R = 1, H <= 16: inputs 
 constexpr int kSplitLanes = 4;      // latency-mode (SPLIT) rollout: lanes per sample in the sampler phase
 constexpr int kPartHdr = 8;         // [m, k_argmin, fidx_argmin, S, S2, sumJ, nfin, pad]
 constexpr int kEPartStride = 2 * SBS_MAX_D + 4;  // CEM elite-moment record [S1[D], n, S2[D]]
-constexpr int kDynFan = 64;                     // dynamic tile scheduling: reduction-tree fan-in
-constexpr int kDynMaxLevels = 5;                // 64^5 tiles
+constexpr int kDynMaxLevels = 5;                // dynamic tile scheduling: reduction-tree depth limit
 constexpr int kDynBatch = 8;                    // tiles per release fence
 // full-covariance CEM elite record [S1[D], n, lower triangle of S2 (D (D + 1) / 2)], 16-byte multiple
 __host__ __device__ constexpr int fc_record_floats(int D) { return ((D + 1 + D * (D + 1) / 2) + 3) / 4 * 4; }
@@ -92,10 +91,11 @@ struct Params {
   int full_cov;               // f3 (L42): CEM with a full covariance C = L L^T
   int cem_cluster;            // CEM at world = 1: cluster size of the one-launch select + elite path, 0: two kernels
   // throughput-mode MPPI with dynamic tile scheduling (one robot): tiles are taken from a
-  // counter and reduced by a fixed tree of fan-in kDynFan over the tile index, so the result
+  // counter and reduced by a fixed tree of fan-in dyn_fan over the tile index, so the result
   // does not depend on which CTA ran which tile
   int dyn;                    // 1: on
   int dyn_levels;             // L: tree levels above the tiles (level L is the root)
+  int dyn_fan;                // fan-in: as many records as one merge stages in shared memory (<= 128)
   int dyn_n[kDynMaxLevels + 1];     // nodes per level (dyn_n[0] = n_tiles, dyn_n[L] = 1)
   int dyn_off[kDynMaxLevels + 1];   // record offset of level l in dyn_rec (levels 0..L-1)
   int dyn_coff[kDynMaxLevels + 1];  // arrival counters of level l (1..L) in dyn_cnt

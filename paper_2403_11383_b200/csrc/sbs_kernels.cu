@@ -1286,12 +1286,12 @@ __device__ __forceinline__ void dyn_arrive(const Params& p, const int* pend, int
   __threadfence();
 #pragma unroll
   for (int i = 0; i < kDynBatch; ++i)
-    if (i < n_pend) atomicAdd(p.dyn_cnt + p.dyn_coff[1] + pend[i] / kDynFan, 1);
+    if (i < n_pend) atomicAdd(p.dyn_cnt + p.dyn_coff[1] + pend[i] / p.dyn_fan, 1);
   n_pend = 0;
 }
 
 // Dynamic tile scheduling (Params::dyn): the tiles' records are reduced by a fixed tree
-// of fan-in kDynFan over the tile index.  Once its tile loop is over, CTA c merges the
+// of fan-in Params::dyn_fan over the tile index.  Once its tile loop is over, CTA c merges the
 // level-1 nodes c, c + n_cta, ... in index order, each as soon as its tiles' arrivals are
 // all in (a CTA takes a tile only while running, so every awaited tile is in a running
 // CTA that does not wait itself), then climbs: the CTA completing a higher node (one
@@ -1304,7 +1304,7 @@ static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int
   for (int node = blockIdx.x; node < p.dyn_n[1]; node += gridDim.x) {
     if (threadIdx.x == 0) {  // wait for the node's tile records (acquire)
       int* c = p.dyn_cnt + p.dyn_coff[1] + node;
-      const int nk = min(kDynFan, p.dyn_n[0] - node * kDynFan);
+      const int nk = min(p.dyn_fan, p.dyn_n[0] - node * p.dyn_fan);
       for (;;) {
         int v;
         asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
@@ -1318,12 +1318,12 @@ static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int
     int idx = node;
     for (int l = 1; l <= L; ++l) {
       if (l > 1) {  // arrive at the level-l node; its last arrival merges it
-        const int nkids_up = min(kDynFan, p.dyn_n[l - 1] - (idx / kDynFan) * kDynFan);
-        if (!arrive_last(p.dyn_cnt + p.dyn_coff[l] + idx / kDynFan, nkids_up)) break;
-        idx /= kDynFan;
+        const int nkids_up = min(p.dyn_fan, p.dyn_n[l - 1] - (idx / p.dyn_fan) * p.dyn_fan);
+        if (!arrive_last(p.dyn_cnt + p.dyn_coff[l] + idx / p.dyn_fan, nkids_up)) break;
+        idx /= p.dyn_fan;
       }
-      const int nkids = min(kDynFan, p.dyn_n[l - 1] - idx * kDynFan);
-      const float* kids = p.dyn_rec + (size_t)(p.dyn_off[l - 1] + idx * kDynFan) * RL;
+      const int nkids = min(p.dyn_fan, p.dyn_n[l - 1] - idx * p.dyn_fan);
+      const float* kids = p.dyn_rec + (size_t)(p.dyn_off[l - 1] + idx * p.dyn_fan) * RL;
       if (l < L) {
         mppi_merge_block<true>(p, r, nullptr, stage, stage_floats, kids, nkids,
                                p.dyn_rec + (size_t)(p.dyn_off[l] + idx) * RL);
