@@ -1323,6 +1323,7 @@ static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int
         idx /= p.dyn_fan;
       }
       const int nkids = min(p.dyn_fan, p.dyn_n[l - 1] - idx * p.dyn_fan);
+      SBS_CHECK(l <= kDynMaxLevels && idx >= 0 && idx < p.dyn_n[l] && nkids > 0);
       const float* kids = p.dyn_rec + (size_t)(p.dyn_off[l - 1] + idx * p.dyn_fan) * RL;
       if (l < L) {
         mppi_merge_block<true>(p, r, nullptr, stage, stage_floats, kids, nkids,
@@ -1621,6 +1622,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
         v = (a01.x + a01.y) + (a23.x + a23.y);
       }
       if (dyn) {  // this tile's record (relative to its own minimum mt)
+        SBS_CHECK(tile >= 0 && tile < p.dyn_n[0]);
         float* o = p.dyn_rec + (size_t)tile * p.part_stride;
         if (tid < D) o[kPartHdr + tid] = v;
         else o[3 + tid - D] = v;
