@@ -118,6 +118,7 @@ struct sbs_ctx {
   float* d_sdiag = nullptr;
   float* d_dyn_rec = nullptr;  // dynamic tile scheduling: tile and subtree records
   int* d_dyn_cnt = nullptr;    // ... its counters
+  int dyn_recs = 0, dyn_cnts = 0;
   sbs_input* d_in = nullptr;
   sbs_output* d_out = nullptr;
   // host path staging: one pinned block [iter | R inputs | R x H x 12 reference], one H2D per step
@@ -374,6 +375,10 @@ int enqueue_finish(sbs_ctx* c, cudaStream_t s, const float* recs) {
   F.n_cta = c->cfg.world;
   F.part_c_stride = F.R;
   F.part_stride = F.ex_stride;
+  if (c->cfg.mode == SBS_MPPI) {  // every rank's records: the top tree nodes it emitted, in rank order
+    F.n_cta = c->cfg.world * (F.ex_stride / c->P.part_stride);
+    F.part_stride = c->P.part_stride;
+  }
   const int mode = c->cfg.mode;
   if (mode == SBS_MPPI) CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_mppi_finalize(F, s); }));
   else if (mode == SBS_NAIVE) CK(timed(c, SBS_KERNEL_REDUCE, s, [&] { return sbs::launch_naive_finalize(F, s); }));
@@ -653,8 +658,54 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   }
   P.part_c_stride = 1;
   P.part_stride = sbs::kPartHdr + D;
+  // throughput-mode MPPI for one robot with several tiles per CTA: dynamic tile scheduling
+  // (the CTAs sharing an SM do not progress at the same rate, so a static tile split ends
+  // with SMs running one or two CTAs; SBS_DYN=0 keeps the static split, for tests / A/B).
+  // The tile records are reduced by a tree of fan-in 64 over the tile index.  With world > 1
+  // and this rank's tiles made of whole nodes of the level just below the global tree's
+  // root, the rank emits those nodes' records instead of merging them, and the rank-order
+  // merge after the exchange is the global root's merge: the result does not depend on
+  // the number of GPUs.
+  P.dyn = 0;
+  if (cfg->mode == SBS_MPPI && R == 1 && !P.split && !cfg->full_cov && P.n_tiles >= 2 * P.n_cta) {
+    const char* e = getenv("SBS_DYN");
+    P.dyn = (!e || atoi(e) != 0) ? 1 : 0;
+  }
+  int emit_nodes = 1;  // MPPI rank records per robot in the world > 1 exchange
+  if (P.dyn) {
+    // fan-in 64 (measured against 32 and 122, the most one merge stages in the rollout's
+    // reduction buffer); SBS_DYN_FAN overrides (experiments)
+    P.dyn_fan = 64;
+    if (const char* e = getenv("SBS_DYN_FAN")) P.dyn_fan = std::max(2, atoi(e));
+    P.dyn_fan = std::min(P.dyn_fan, std::min(128, (D + 4) * (sbs::kBlock + 4) / (int)P.part_stride));
+    // the global tree's depth, and the node size (samples) of its level below the root
+    int Lg = 0;
+    int64_t node = sbs::kBlock;
+    for (int64_t n = (cfg->n_samples + sbs::kBlock - 1) / sbs::kBlock; n > 1; n = (n + P.dyn_fan - 1) / P.dyn_fan) {
+      ++Lg;
+      if (n > P.dyn_fan) node *= P.dyn_fan;
+    }
+    const bool aligned = cfg->world > 1 && Lg >= 2 && P.k_begin % node == 0 && P.K_local % node == 0;
+    int n = P.n_tiles, L = 0, recs = 0, cnts = 2;
+    P.dyn_n[0] = n;
+    while (n > 1 && !(aligned && L == Lg - 1)) {
+      P.dyn_off[L] = recs;
+      recs += n;
+      n = (n + P.dyn_fan - 1) / P.dyn_fan;
+      ++L;
+      if (L > sbs::kDynMaxLevels) return bail(SBS_ERR_INVALID_ARG);
+      P.dyn_n[L] = n;
+      P.dyn_coff[L] = cnts;
+      cnts += n;
+    }
+    P.dyn_levels = L;
+    P.dyn_ecnt = cnts++;  // arrivals of the emitted top-level records
+    emit_nodes = n;
+    c->dyn_recs = recs;
+    c->dyn_cnts = cnts;
+  }
   // rank record of the world > 1 exchange (16-byte multiple)
-  if (cfg->mode == SBS_MPPI) P.ex_stride = P.part_stride;
+  if (cfg->mode == SBS_MPPI) P.ex_stride = emit_nodes * P.part_stride;
   else if (cfg->mode == SBS_NAIVE) P.ex_stride = sbs::kPartHdr;
   else P.ex_stride = (int)((sbs::kPartHdr + 2 * cfg->n_elite + 3) / 4 * 4);
   // ---- device buffers ----
@@ -751,36 +802,10 @@ int sbs_create(const sbs_config* cfg, sbs_ctx** out) {
   P.elite_J = c->d_eJ;
   P.Lmat = c->d_L;
   P.cand = c->d_cand;
-  // throughput-mode MPPI for one robot with several tiles per CTA: dynamic tile scheduling
-  // (the CTAs sharing an SM do not progress at the same rate, so a static tile split ends
-  // with SMs running one or two CTAs; SBS_DYN=0 keeps the static split, for tests / A/B)
-  P.dyn = 0;
-  if (cfg->mode == SBS_MPPI && R == 1 && !P.split && !P.full_cov && P.n_tiles >= 2 * P.n_cta) {
-    const char* e = getenv("SBS_DYN");
-    P.dyn = (!e || atoi(e) != 0) ? 1 : 0;
-  }
   if (P.dyn) {
-    // fan-in 64 (measured against 32 and 122, the most one merge stages in the rollout's
-    // reduction buffer); SBS_DYN_FAN overrides (experiments)
-    P.dyn_fan = 64;
-    if (const char* e = getenv("SBS_DYN_FAN")) P.dyn_fan = std::max(2, atoi(e));
-    P.dyn_fan = std::min(P.dyn_fan, std::min(128, (D + 4) * (sbs::kBlock + 4) / (int)P.part_stride));
-    int n = P.n_tiles, L = 0, recs = 0, cnts = 2;
-    P.dyn_n[0] = n;
-    while (n > 1) {
-      P.dyn_off[L] = recs;
-      recs += n;
-      n = (n + P.dyn_fan - 1) / P.dyn_fan;
-      ++L;
-      if (L > sbs::kDynMaxLevels) return bail(SBS_ERR_INVALID_ARG);
-      P.dyn_n[L] = n;
-      P.dyn_coff[L] = cnts;
-      cnts += n;
-    }
-    P.dyn_levels = L;
-    CKC(cudaMalloc(&c->d_dyn_rec, (size_t)recs * P.part_stride * sizeof(float)));
-    CKC(cudaMalloc(&c->d_dyn_cnt, (size_t)cnts * sizeof(int)));
-    CKC(cudaMemset(c->d_dyn_cnt, 0, (size_t)cnts * sizeof(int)));
+    CKC(cudaMalloc(&c->d_dyn_rec, (size_t)c->dyn_recs * P.part_stride * sizeof(float)));
+    CKC(cudaMalloc(&c->d_dyn_cnt, (size_t)c->dyn_cnts * sizeof(int)));
+    CKC(cudaMemset(c->d_dyn_cnt, 0, (size_t)c->dyn_cnts * sizeof(int)));
     P.dyn_rec = c->d_dyn_rec;
     P.dyn_cnt = c->d_dyn_cnt;
   }

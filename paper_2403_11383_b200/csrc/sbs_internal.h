@@ -100,7 +100,8 @@ struct Params {
   int dyn_off[kDynMaxLevels + 1];   // record offset of level l in dyn_rec (levels 0..L-1)
   int dyn_coff[kDynMaxLevels + 1];  // arrival counters of level l (1..L) in dyn_cnt
   float* dyn_rec;             // [sum_l dyn_n[l]][part_stride] tile and subtree records
-  int* dyn_cnt;               // [0]: next tile, [1]: CTAs done, then the level counters
+  int* dyn_cnt;               // [0]: next tile, [1]: CTAs done, then the level counters, then dyn_ecnt
+  int dyn_ecnt;               // index in dyn_cnt of the emitted top-level records' arrivals (world > 1)
   int model;                  // 1: the constants equal the compiled-in robot model (sbs_robot_model.h)
   float* Lmat;                // [R][D][D] lower Cholesky factor (row-major), full_cov only
   int n_sig_groups;           // multiple Gaussians (L41): sample k uses sig_scale[k mod n_sig_groups]

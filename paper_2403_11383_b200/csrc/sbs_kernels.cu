@@ -1328,10 +1328,10 @@ static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int
       if (l < L) {
         mppi_merge_block<true>(p, r, nullptr, stage, stage_floats, kids, nkids,
                                p.dyn_rec + (size_t)(p.dyn_off[l] + idx) * RL);
-      } else if (p.emit) {  // world > 1: this rank's record (the exchange and rank-order merge follow)
+      } else if (p.emit) {  // world > 1: this rank's top-level record(s) (the exchange and rank-order merge follow)
         SBS_TS(5);
-        mppi_merge_block<true>(p, r, p.emit, stage, stage_floats, kids, nkids);
-        publish_to_peers(p);
+        mppi_merge_block<true>(p, r, p.emit, stage, stage_floats, kids, nkids, p.emit + (size_t)idx * RL);
+        if (arrive_last(p.dyn_cnt + p.dyn_ecnt, p.dyn_n[L])) publish_to_peers(p);
         SBS_TS(6);
       } else {
         SBS_TS(5);

@@ -420,3 +420,39 @@ def test_dynamic_tiles_are_deterministic_and_match_the_static_split(B, orc, monk
     w = np.exp(-(Jg[fin] - Jg[fin].min()) / cfg["lambda"])
     assert abs(float(o1[0]["j_min"]) - Jg[fin].min()) <= 1e-6 * abs(Jg[fin].min())
     assert np.isclose(float(o1[0]["ess"]), w.sum() ** 2 / (w * w).sum(), rtol=1e-4)
+
+
+@pytest.mark.parametrize("K,world", [(1 << 20, 2), (1 << 21, 2), (1 << 21, 4)])
+def test_sharded_mppi_is_bitwise_independent_of_the_gpu_count(B, K, world):
+    """SURVEY 8(e)'s fixed reduction tree: with dynamic tiles every rank reduces its
+    tiles' records by the same fan-in-64 tree over the global tile index; when a rank's
+    slice is made of whole nodes of the level below the global root, it emits those
+    nodes' records and the rank-order merge after the exchange is the global root's
+    merge.  The new mean, u0 and the diagnostics are then bitwise those of one GPU
+    (Alg. 4, P:188-201 evaluated by the same arithmetic in the same order)."""
+    import ctypes as C
+
+    import torch
+    cfg, inputs = W.config4(K)
+    st = W.initial_distribution(cfg)
+    arr = B.make_inputs(inputs)
+    d_in = torch.from_numpy(np.frombuffer(bytes(arr), dtype=np.uint8).copy()).cuda()
+    single = _ctrl(B, cfg, inputs, dict(st))
+    ranks = [B.Controller(cfg, rank=g, world=world) for g in range(world)]
+    for c in ranks:
+        c.set_reference(0, inputs[0]["xref"])
+    nrec = ranks[0].record_floats()
+    assert nrec == (K // world) // (1 << 19) * (8 + 48)  # whole level-2 nodes (2^19 samples) per rank
+    s = torch.cuda.current_stream().cuda_stream
+    for it in range(2):
+        _, so = single.step(inputs)
+        recs = torch.zeros((world, nrec), dtype=torch.float32, device="cuda")
+        for g, c in enumerate(ranks):
+            c.step_records(d_in.data_ptr(), recs[g].data_ptr(), s)
+        for c in ranks:
+            d_out = torch.zeros(C.sizeof(B.sbs_output), dtype=torch.uint8, device="cuda")
+            c.finish_records(recs.data_ptr(), d_in.data_ptr(), d_out.data_ptr(), s)
+            torch.cuda.synchronize()
+            o = B.output_dict(B.sbs_output.from_buffer_copy(d_out.cpu().numpy().tobytes()), 48)
+            for key in ("mean", "var", "u0", "j_min", "j_mean", "ess", "omega", "n_diverged", "freq_idx"):
+                np.testing.assert_array_equal(np.asarray(o[key]), np.asarray(so[0][key]), err_msg=f"iter {it} {key}")
