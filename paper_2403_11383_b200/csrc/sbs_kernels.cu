@@ -1291,16 +1291,17 @@ __device__ __forceinline__ void dyn_arrive(const Params& p, const int* pend, int
 }
 
 // Dynamic tile scheduling (Params::dyn): the tiles' records are reduced by a fixed tree
-// of fan-in Params::dyn_fan over the tile index.  Once its tile loop is over, CTA c merges the
-// level-1 nodes c, c + n_cta, ... in index order, each as soon as its tiles' arrivals are
-// all in (a CTA takes a tile only while running, so every awaited tile is in a running
-// CTA that does not wait itself), then climbs: the CTA completing a higher node (one
-// arrival counter per node) merges it likewise; the root's merge finishes the iteration
-// (or emits the rank record).  The tree and its merge order are fixed by the tile indices
-// alone, so the result is the same whichever CTA ran which tile.
+// of fan-in Params::dyn_fan over the tile index.  Once its tile loop is over (and its
+// arrivals flushed), CTA c merges the level-1 nodes c, c + n_cta, ... in index order, each
+// as soon as its tiles' arrivals are all in (a CTA takes a tile only while running, so
+// every awaited tile is in a running CTA that does not wait itself), then climbs: the CTA
+// completing a higher node (one arrival counter per node) merges it likewise.  The top
+// level's merge finishes the iteration (world = 1, a single root) or writes this rank's
+// top-level node records (world > 1: the rank-order merge after the exchange completes
+// the global tree).  The tree and its merge order are fixed by the tile indices alone,
+// so the result is the same whichever CTA ran which tile.
 static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int stage_floats) {
   const int RL = p.part_stride, L = p.dyn_levels;
-  __shared__ int s_go;
   for (int node = blockIdx.x; node < p.dyn_n[1]; node += gridDim.x) {
     if (threadIdx.x == 0) {  // wait for the node's tile records (acquire)
       int* c = p.dyn_cnt + p.dyn_coff[1] + node;
@@ -1312,7 +1313,6 @@ static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int
         __nanosleep(128);
       }
       *c = 0;  // re-armed (nothing else touches it this launch)
-      s_go = 1;
     }
     __syncthreads();
     int idx = node;
