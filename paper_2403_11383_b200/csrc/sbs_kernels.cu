@@ -1279,6 +1279,113 @@ static __device__ void publish_to_peers(const Params& p) {
 enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
 
 
+// Merge of n <= 128 MPPI records (contiguous, stride part_stride) into one record at
+// `out`, relative to their smallest minimum -- the tree's inner nodes (and a rank's
+// top-level nodes): warp 0 reads the n headers, takes beta = min m_c and the (J, k)
+// argmin, and writes every record's scale exp((beta - m_c)/lambda) to shared memory;
+// then row thread t sums column t over the records in index order (S2 with squared
+// scales, the finite-cost sums unscaled), its loads independent of one another.  The
+// same arithmetic for a node whichever GPU count or CTA schedule produced it.
+static __device__ void dyn_node_merge(const Params& p, const float* kids, int n, float* out, float* s_sc) {
+  const int tid = threadIdx.x, D = p.D, NR = D + 4, RL = p.part_stride;
+  __shared__ float s_beta, s_bm;
+  __shared__ int s_bk, s_bf;
+  if (tid < 32) {
+    float mc[4];
+    uint32_t kmin = 0xffffffffu;
+    float m = kInf;
+    int mk = 0x7fffffff, mf = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // n <= 128: four headers per lane, loads issued together
+      const int c = tid + 32 * u;
+      mc[u] = kInf;
+      if (c < n) {
+        const float* h = kids + (size_t)c * RL;
+        mc[u] = __ldcg(h);
+        const int kc = __float_as_int(__ldcg(h + 1)), fc = __float_as_int(__ldcg(h + 2));
+        kmin = min(kmin, cost_key(mc[u]));
+        if (jk_less(mc[u], kc, m, mk)) {
+          m = mc[u];
+          mk = kc;
+          mf = fc;
+        }
+      }
+    }
+    const float beta = key_cost(__reduce_min_sync(0xffffffffu, kmin));
+    warp_argmin(m, mk, mf);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = tid + 32 * u;
+      if (c < n) s_sc[c] = (mc[u] < kInf) ? __expf((beta - mc[u]) * p.inv_lambda) : 0.0f;
+    }
+    if (tid == 0) {
+      s_beta = beta;
+      s_bm = m;
+      s_bk = mk;
+      s_bf = mf;
+    }
+  }
+  __syncthreads();
+  if (tid < NR) {
+    const int col = tid < D ? kPartHdr + tid : 3 + (tid - D);
+    const int kind = tid < D + 1 ? 0 : (tid == D + 1 ? 1 : 2);
+    float a0 = 0.f, a1 = 0.f;
+    int c = 0;
+#pragma unroll 4
+    for (; c + 1 < n; c += 2) {
+      float s0 = s_sc[c], s1 = s_sc[c + 1];
+      if (kind == 1) { s0 *= s0; s1 *= s1; }
+      if (kind == 2) { s0 = 1.f; s1 = 1.f; }
+      a0 = fmaf(__ldcg(kids + (size_t)c * RL + col), s0, a0);
+      a1 = fmaf(__ldcg(kids + (size_t)(c + 1) * RL + col), s1, a1);
+    }
+    if (c < n) {
+      float s0 = kind == 2 ? 1.f : s_sc[c];
+      if (kind == 1) s0 *= s0;
+      a0 = fmaf(__ldcg(kids + (size_t)c * RL + col), s0, a0);
+    }
+    if (tid < D) out[kPartHdr + tid] = a0 + a1;
+    else out[3 + tid - D] = a0 + a1;
+  }
+  if (tid == 0) {
+    out[0] = s_bm;
+    out[1] = __int_as_float(s_bk);
+    out[2] = __int_as_float(s_bf);
+    out[7] = 0.0f;
+  }
+  (void)s_beta;
+}
+
+// The tree's root (world = 1), or the rank-order merge of the ranks' top-level records
+// (world > 1, sbs_mppi_finalize): dyn_node_merge into a shared-memory record, then the
+// finish of mppi_merge_block (new mean = V / S, outputs).  The finish's own loads
+// (variance, input phase, iteration) are issued first and overlap the merge.
+static __device__ void dyn_root_finish(const Params& p, int r, const float* kids, int n, float* stage) {
+  const int tid = threadIdx.x, D = p.D;
+  __shared__ __align__(16) float s_rec[kPartHdr + SBS_MAX_D + 4];
+  __shared__ float s_mean[SBS_MAX_D], s_var[SBS_MAX_D];
+  __shared__ uint32_t s_pre[2];
+  for (int d = tid; d < D; d += blockDim.x) s_var[d] = p.var[(size_t)r * D + d];
+  if (tid == 0) {
+    s_pre[0] = robot_in(p, r)->phase_q32;
+    s_pre[1] = step_iter(p);
+  }
+  dyn_node_merge(p, kids, n, s_rec, stage);
+  __syncthreads();
+  const float bm = s_rec[0];
+  const int bf = __float_as_int(s_rec[2]);
+  const bool all_div = !(bm < kInf);
+  const float S = s_rec[3], S2 = s_rec[4], sumJ = s_rec[5], nfin = s_rec[6];
+  float* mean = p.mean + (size_t)r * D;
+  for (int d = tid; d < D; d += blockDim.x) s_mean[d] = all_div ? mean[d] : s_rec[kPartHdr + d] / S;
+  const int fi = all_div ? p.fidx[r] : bf;
+  __syncthreads();
+  for (int d = tid; d < D; d += blockDim.x) mean[d] = s_mean[d];
+  if (tid == 0) p.fidx[r] = fi;
+  write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, bm,
+               nfin > 0.f ? sumJ / nfin : kInf, S, all_div ? 0.f : S * S / S2, (int)((float)p.K_global - nfin), s_pre);
+}
+
 // thread 0: the level-1 arrivals of the buffered tiles behind one release fence (one
 // fence per kDynBatch tiles instead of per tile: a fence waits for the CTA's writes)
 __device__ __forceinline__ void dyn_arrive(const Params& p, const int* pend, int& n_pend) {
@@ -1326,16 +1433,15 @@ static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int
       SBS_CHECK(l <= kDynMaxLevels && idx >= 0 && idx < p.dyn_n[l] && nkids > 0);
       const float* kids = p.dyn_rec + (size_t)(p.dyn_off[l - 1] + idx * p.dyn_fan) * RL;
       if (l < L) {
-        mppi_merge_block<true>(p, r, nullptr, stage, stage_floats, kids, nkids,
-                               p.dyn_rec + (size_t)(p.dyn_off[l] + idx) * RL);
+        dyn_node_merge(p, kids, nkids, p.dyn_rec + (size_t)(p.dyn_off[l] + idx) * RL, stage);
       } else if (p.emit) {  // world > 1: this rank's top-level record(s) (the exchange and rank-order merge follow)
         SBS_TS(5);
-        mppi_merge_block<true>(p, r, p.emit, stage, stage_floats, kids, nkids, p.emit + (size_t)idx * RL);
+        dyn_node_merge(p, kids, nkids, p.emit + (size_t)idx * RL, stage);
         if (arrive_last(p.dyn_cnt + p.dyn_ecnt, p.dyn_n[L])) publish_to_peers(p);
         SBS_TS(6);
       } else {
         SBS_TS(5);
-        mppi_merge_block<false>(p, r, nullptr, stage, stage_floats, kids, nkids);
+        dyn_root_finish(p, r, kids, nkids, stage);
         SBS_TS(6);
       }
     }
@@ -1715,7 +1821,10 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
 template <bool EMIT>
 __global__ void __launch_bounds__(128) sbs_mppi_finalize(const __grid_constant__ Params p, float* emit) {
   __shared__ __align__(16) float stage[4096];
-  mppi_merge_block<EMIT>(p, blockIdx.x, emit, stage, 4096);
+  if (!EMIT && p.dyn && p.R == 1 && p.n_cta <= 128)  // the ranks' tree-node records: the root's merge (GPU-count invariant)
+    dyn_root_finish(p, blockIdx.x, part_rec(p, blockIdx.x, 0), p.n_cta, stage);
+  else
+    mppi_merge_block<EMIT>(p, blockIdx.x, emit, stage, 4096);
 }
 
 // ---------------------------------------------------------------------------
