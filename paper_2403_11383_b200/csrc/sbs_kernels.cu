@@ -1286,23 +1286,34 @@ enum { EPI_MPPI = 0, EPI_ARGMIN = 1 };
 // then row thread t sums column t over the records in index order (S2 with squared
 // scales, the finite-cost sums unscaled), its loads independent of one another.  The
 // same arithmetic for a node whichever GPU count or CTA schedule produced it.
-static __device__ void dyn_node_merge(const Params& p, const float* kids, int n, float* out, float* s_sc) {
+static __device__ void dyn_node_merge(const Params& p, const float* kids, int n, float* out, float* stage,
+                                      int stage_floats) {
   const int tid = threadIdx.x, D = p.D, NR = D + 4, RL = p.part_stride;
-  __shared__ float s_beta, s_bm;
+  __shared__ float s_bm;
   __shared__ int s_bk, s_bf;
+  // the records staged in shared memory when they fit (every thread's loads in flight at
+  // once), else read from L2 by the row threads
+  const bool staged = n * RL + 128 <= stage_floats;
+  float* s_sc = staged ? stage + n * RL : stage;
+  const float* src = staged ? stage : kids;
+  if (staged) {
+    stage_copy(stage, kids, n * RL);
+    __syncthreads();
+  }
   if (tid < 32) {
     float mc[4];
     uint32_t kmin = 0xffffffffu;
     float m = kInf;
     int mk = 0x7fffffff, mf = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // n <= 128: four headers per lane, loads issued together
+    for (int u = 0; u < 4; ++u) {  // n <= 128: four headers per lane
       const int c = tid + 32 * u;
       mc[u] = kInf;
       if (c < n) {
-        const float* h = kids + (size_t)c * RL;
-        mc[u] = __ldcg(h);
-        const int kc = __float_as_int(__ldcg(h + 1)), fc = __float_as_int(__ldcg(h + 2));
+        const float* h = src + (size_t)c * RL;
+        mc[u] = staged ? h[0] : __ldcg(h);
+        const int kc = __float_as_int(staged ? h[1] : __ldcg(h + 1));
+        const int fc = __float_as_int(staged ? h[2] : __ldcg(h + 2));
         kmin = min(kmin, cost_key(mc[u]));
         if (jk_less(mc[u], kc, m, mk)) {
           m = mc[u];
@@ -1319,7 +1330,6 @@ static __device__ void dyn_node_merge(const Params& p, const float* kids, int n,
       if (c < n) s_sc[c] = (mc[u] < kInf) ? __expf((beta - mc[u]) * p.inv_lambda) : 0.0f;
     }
     if (tid == 0) {
-      s_beta = beta;
       s_bm = m;
       s_bk = mk;
       s_bf = mf;
@@ -1336,13 +1346,15 @@ static __device__ void dyn_node_merge(const Params& p, const float* kids, int n,
       float s0 = s_sc[c], s1 = s_sc[c + 1];
       if (kind == 1) { s0 *= s0; s1 *= s1; }
       if (kind == 2) { s0 = 1.f; s1 = 1.f; }
-      a0 = fmaf(__ldcg(kids + (size_t)c * RL + col), s0, a0);
-      a1 = fmaf(__ldcg(kids + (size_t)(c + 1) * RL + col), s1, a1);
+      const float v0 = staged ? src[(size_t)c * RL + col] : __ldcg(src + (size_t)c * RL + col);
+      const float v1 = staged ? src[(size_t)(c + 1) * RL + col] : __ldcg(src + (size_t)(c + 1) * RL + col);
+      a0 = fmaf(v0, s0, a0);
+      a1 = fmaf(v1, s1, a1);
     }
     if (c < n) {
       float s0 = kind == 2 ? 1.f : s_sc[c];
       if (kind == 1) s0 *= s0;
-      a0 = fmaf(__ldcg(kids + (size_t)c * RL + col), s0, a0);
+      a0 = fmaf(staged ? src[(size_t)c * RL + col] : __ldcg(src + (size_t)c * RL + col), s0, a0);
     }
     if (tid < D) out[kPartHdr + tid] = a0 + a1;
     else out[3 + tid - D] = a0 + a1;
@@ -1353,14 +1365,14 @@ static __device__ void dyn_node_merge(const Params& p, const float* kids, int n,
     out[2] = __int_as_float(s_bf);
     out[7] = 0.0f;
   }
-  (void)s_beta;
 }
 
 // The tree's root (world = 1), or the rank-order merge of the ranks' top-level records
 // (world > 1, sbs_mppi_finalize): dyn_node_merge into a shared-memory record, then the
 // finish of mppi_merge_block (new mean = V / S, outputs).  The finish's own loads
 // (variance, input phase, iteration) are issued first and overlap the merge.
-static __device__ void dyn_root_finish(const Params& p, int r, const float* kids, int n, float* stage) {
+static __device__ void dyn_root_finish(const Params& p, int r, const float* kids, int n, float* stage,
+                                       int stage_floats) {
   const int tid = threadIdx.x, D = p.D;
   __shared__ __align__(16) float s_rec[kPartHdr + SBS_MAX_D + 4];
   __shared__ float s_mean[SBS_MAX_D], s_var[SBS_MAX_D];
@@ -1370,7 +1382,7 @@ static __device__ void dyn_root_finish(const Params& p, int r, const float* kids
     s_pre[0] = robot_in(p, r)->phase_q32;
     s_pre[1] = step_iter(p);
   }
-  dyn_node_merge(p, kids, n, s_rec, stage);
+  dyn_node_merge(p, kids, n, s_rec, stage, stage_floats);
   __syncthreads();
   const float bm = s_rec[0];
   const int bf = __float_as_int(s_rec[2]);
@@ -1433,15 +1445,15 @@ static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int
       SBS_CHECK(l <= kDynMaxLevels && idx >= 0 && idx < p.dyn_n[l] && nkids > 0);
       const float* kids = p.dyn_rec + (size_t)(p.dyn_off[l - 1] + idx * p.dyn_fan) * RL;
       if (l < L) {
-        dyn_node_merge(p, kids, nkids, p.dyn_rec + (size_t)(p.dyn_off[l] + idx) * RL, stage);
+        dyn_node_merge(p, kids, nkids, p.dyn_rec + (size_t)(p.dyn_off[l] + idx) * RL, stage, stage_floats);
       } else if (p.emit) {  // world > 1: this rank's top-level record(s) (the exchange and rank-order merge follow)
         SBS_TS(5);
-        dyn_node_merge(p, kids, nkids, p.emit + (size_t)idx * RL, stage);
+        dyn_node_merge(p, kids, nkids, p.emit + (size_t)idx * RL, stage, stage_floats);
         if (arrive_last(p.dyn_cnt + p.dyn_ecnt, p.dyn_n[L])) publish_to_peers(p);
         SBS_TS(6);
       } else {
         SBS_TS(5);
-        dyn_root_finish(p, r, kids, nkids, stage);
+        dyn_root_finish(p, r, kids, nkids, stage, stage_floats);
         SBS_TS(6);
       }
     }
@@ -1822,7 +1834,7 @@ template <bool EMIT>
 __global__ void __launch_bounds__(128) sbs_mppi_finalize(const __grid_constant__ Params p, float* emit) {
   __shared__ __align__(16) float stage[4096];
   if (!EMIT && p.dyn && p.R == 1 && p.n_cta <= 128)  // the ranks' tree-node records: the root's merge (GPU-count invariant)
-    dyn_root_finish(p, blockIdx.x, part_rec(p, blockIdx.x, 0), p.n_cta, stage);
+    dyn_root_finish(p, blockIdx.x, part_rec(p, blockIdx.x, 0), p.n_cta, stage, 4096);
   else
     mppi_merge_block<EMIT>(p, blockIdx.x, emit, stage, 4096);
 }
