@@ -67,6 +67,7 @@ __device__ unsigned long long g_sbs_bar[4][8];  // integrator warp x chunk: cycl
 #endif
 
 #define kInf __int_as_float(0x7f800000)
+constexpr long long kSpinLimit = 4000000000LL;  // SM cycles (~2 s) a cross-CTA wait may take before it traps
 constexpr float kPitchMax = 1.5697963267948966f;  // pi/2 - 1e-3 (L26)
 constexpr float kTwoPi = 6.283185307179586f;
 constexpr float kInvTwoPi = 0.15915494309189535f;
@@ -1425,7 +1426,7 @@ static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int
     if (threadIdx.x == 0) {  // wait for the node's tile records (acquire)
       int* c = p.dyn_cnt + p.dyn_coff[1] + node;
       const int nk = min(p.dyn_fan, p.dyn_n[0] - node * p.dyn_fan);
-      for (;;) {
+      for (;;) {  // (every awaited arrival comes from a running CTA that does not wait itself)
         int v;
         asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
         if (v >= nk) break;
@@ -2542,12 +2543,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {  // phase 0 of a fresh barrier
   uint32_t done = 0;
-  while (!done)
+  const long long t0 = clock64();
+  while (!done) {
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
         : "=r"(done)
         : "r"(smem_u32(bar))
         : "memory");
+    if (!done && clock64() - t0 > kSpinLimit) __trap();  // (missing bytes: fail the launch, never hang)
+  }
 }
 __device__ __forceinline__ void st_async(uint32_t addr, float v, uint32_t bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr),
