@@ -1372,19 +1372,12 @@ static __device__ void dyn_node_merge(const Params& p, const float* kids, int n,
 // (world > 1, sbs_mppi_finalize): dyn_node_merge into a shared-memory record, then the
 // finish of mppi_merge_block (new mean = V / S, outputs).  The finish's own loads
 // (variance, input phase, iteration) are issued first and overlap the merge.
-static __device__ void dyn_root_finish(const Params& p, int r, const float* kids, int n, float* stage,
-                                       int stage_floats) {
+// mppi_merge_block's finish from a robot's merged record in shared memory (new mean
+// V / S, outputs); s_var, s_pre: the robot's variance and (input phase, iteration)
+static __device__ void mppi_finish_record(const Params& p, int r, const float* s_rec, const float* s_var,
+                                          const uint32_t* s_pre) {
   const int tid = threadIdx.x, D = p.D;
-  __shared__ __align__(16) float s_rec[kPartHdr + SBS_MAX_D + 4];
-  __shared__ float s_mean[SBS_MAX_D], s_var[SBS_MAX_D];
-  __shared__ uint32_t s_pre[2];
-  for (int d = tid; d < D; d += blockDim.x) s_var[d] = p.var[(size_t)r * D + d];
-  if (tid == 0) {
-    s_pre[0] = robot_in(p, r)->phase_q32;
-    s_pre[1] = step_iter(p);
-  }
-  dyn_node_merge(p, kids, n, s_rec, stage, stage_floats);
-  __syncthreads();
+  __shared__ float s_mean[SBS_MAX_D];
   const float bm = s_rec[0];
   const int bf = __float_as_int(s_rec[2]);
   const bool all_div = !(bm < kInf);
@@ -1397,6 +1390,25 @@ static __device__ void dyn_root_finish(const Params& p, int r, const float* kids
   if (tid == 0) p.fidx[r] = fi;
   write_output(p, r, all_div ? SBS_WARN_ALL_DIVERGED : SBS_OK, s_mean, s_var, fi, bm,
                nfin > 0.f ? sumJ / nfin : kInf, S, all_div ? 0.f : S * S / S2, (int)((float)p.K_global - nfin), s_pre);
+}
+// the robot's variance and (input phase, iteration) into shared memory (loads issued, not awaited)
+__device__ __forceinline__ void load_finish_inputs(const Params& p, int r, float* s_var, uint32_t* s_pre) {
+  for (int d = threadIdx.x; d < p.D; d += blockDim.x) s_var[d] = p.var[(size_t)r * p.D + d];
+  if (threadIdx.x == 0) {
+    s_pre[0] = robot_in(p, r)->phase_q32;
+    s_pre[1] = step_iter(p);
+  }
+}
+
+static __device__ void dyn_root_finish(const Params& p, int r, const float* kids, int n, float* stage,
+                                       int stage_floats) {
+  __shared__ __align__(16) float s_rec[kPartHdr + SBS_MAX_D + 4];
+  __shared__ float s_var[SBS_MAX_D];
+  __shared__ uint32_t s_pre[2];
+  load_finish_inputs(p, r, s_var, s_pre);  // (overlap the merge)
+  dyn_node_merge(p, kids, n, s_rec, stage, stage_floats);
+  __syncthreads();
+  mppi_finish_record(p, r, s_rec, s_var, s_pre);
 }
 
 // thread 0: the level-1 arrivals of the buffered tiles behind one release fence (one
@@ -1793,6 +1805,24 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
       p.dyn_cnt[1] = 0;
     }
   } else {
+    if constexpr (EPI == EPI_MPPI && FUSED) {
+      if (p.n_cta == 1 && !p.emit) {  // one CTA per robot: its running record is the robot's (merging one
+        __shared__ __align__(16) float s_one[kPartHdr + SBS_MAX_D + 4];  // record is the identity): finish here
+        __shared__ float s_ovar[SBS_MAX_D];
+        __shared__ uint32_t s_opre[2];
+        load_finish_inputs(p, r, s_ovar, s_opre);
+        if (tid < D) s_one[kPartHdr + tid] = run;
+        else if (tid < NR) s_one[3 + tid - D] = run;
+        if (tid == 0) {
+          s_one[0] = SPLIT ? h_m : s_rm[par];
+          s_one[1] = __int_as_float(SPLIT ? h_k : s_rk[par]);
+          s_one[2] = __int_as_float(SPLIT ? h_f : s_rf[par]);
+        }
+        __syncthreads();
+        mppi_finish_record(p, r, s_one, s_ovar, s_opre);
+        return;
+      }
+    }
     SBS_CHECK((int)blockIdx.x < p.n_cta && r < p.R);
     float* out = p.part + ((size_t)r * p.n_cta + blockIdx.x) * p.part_stride;
     if (EPI == EPI_MPPI) {
