@@ -500,7 +500,7 @@ def test_config5_full_size_sampled(B, orc):
         _check_outputs(outs[r], ro, cfg)
 
 
-@pytest.mark.parametrize("K,world", [(10000, 2), (4097, 2), (8192, 4), (1 << 19, 2)])  # (2^19: dynamic tiles per rank)
+@pytest.mark.parametrize("K,world", [(10000, 2), (4097, 2), (8192, 4), (1 << 19, 2), (3 << 18, 2)])  # (2^19: dynamic tiles per rank, tree-aligned slices; 3 * 2^18: not aligned)
 def test_sharded_mppi_records_match_single_gpu(B, orc, K, world):
     """The world > 1 kernels (rank record + rank-order merge) on one GPU: `world`
     contexts each roll out their slice and emit a record, the records are
