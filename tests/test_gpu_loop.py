@@ -128,16 +128,20 @@ def test_fallen_robot_is_frozen(B):
     assert not np.array_equal(a[:n], b[:n])                        # robot 0 advanced
 
 
-@pytest.mark.parametrize("mode", ["mppi", "naive", "cem", "cem-fc"])
+@pytest.mark.parametrize("mode", ["mppi", "naive", "cem", "cem-fc", "mppi-dyn"])
 def test_run_loop_equals_stepwise_calls(B, mode):
     """sbs_run_loop (captured iterations replayed, iteration counter in device memory) is
-    bitwise the same as n x (sbs_step_device + sbs_advance)."""
+    bitwise the same as n x (sbs_step_device + sbs_advance); mppi-dyn: one robot at
+    K = 2^18, where the rollout schedules its tiles dynamically inside the graph."""
     import torch
     R, n = 3, 25
     fc = mode == "cem-fc"
-    mode = "cem" if fc else mode
-    cfg = W.base_config(n_samples=2000, n_elite=200 if mode == "cem" else 1, mode=mode, n_robots=R,
-                        gait_adapt=0 if mode == "mppi" else 1, full_cov=1 if fc else 0)
+    dyn = mode == "mppi-dyn"
+    mode = "cem" if fc else ("mppi" if dyn else mode)
+    if dyn:
+        R, n = 1, 10
+    cfg = W.base_config(n_samples=(1 << 18) if dyn else 2000, n_elite=200 if mode == "cem" else 1, mode=mode,
+                        n_robots=R, gait_adapt=0 if mode == "mppi" else 1, full_cov=1 if fc else 0)
     inputs = [W.robot_input(cfg, r, cmd=(0.3, 0.1 * r, 0), phase=W.q32(0.1 * r)) for r in range(R)]
     lc = W.loop_config()
     cmd = torch.from_numpy(_commands(R)).cuda()
