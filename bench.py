@@ -380,7 +380,12 @@ def run_sbs(args):
                                              label="config3: CEM K_e=1000, K=10000, gait adaptation"),
                  "config5_batched": _time_config(B, W, C, np, torch, W.config5(), steps=20, warmup=3, peak=peak,
                                                  label="config5: 4096 robots x 1024 samples, MPPI (1 GPU)"),
-                 "config5_closed_loop": _time_closed_loop(B, W, C, np, torch, W.config5(), n_iter=50)}
+                 "config5_closed_loop": _time_closed_loop(B, W, C, np, torch, W.config5(), n_iter=50),
+                 # the config-4 sweep below the headline size (BASELINE configs[3]: 64k-4M samples; the
+                 # north star's ">= 50 % of FP32 peak at >= 1M samples")
+                 "config4_sweep": {f"2^{lk}": _time_config(B, W, C, np, torch, W.config4(1 << lk), steps=20, warmup=3,
+                                                           peak=peak, label=f"config4: MPPI, K=2^{lk}")
+                                   for lk in (16, 18, 20, 21)}}
     elif world > 1 and not args.no_other_configs:
         extra = {"config5_robot_sharded": _config5_sharded(B, W, C, np, torch, dist, rank, world, local, flush)}
     if rank == 0:
