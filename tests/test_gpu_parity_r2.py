@@ -5,9 +5,10 @@ reach.
     angle inputs, bit for bit against the oracle (O3-O4; P:236 "theta_k ~ N(theta, C)");
   * Philox4x32-10 against cuRAND's curand_Philox4x32_10 on the device (O1);
   * theta2 within the stated ulp contract;
-  * MPPI at K = 2^16 and 2^18 (more CTA records than the one-pass merge holds: the
-    chunked merge the K = 2^22 bench launch takes) against the oracle (Alg. 4,
-    P:188-201), and the conditioning check of SURVEY 8(c4) over lambda = 1, 10, 100;
+  * MPPI at K = 2^16 (more CTA records than the one-pass merge holds: the chunked merge)
+    and 2^18 (dynamic tiles and the reduction tree the K = 2^22 bench launch takes)
+    against the oracle (Alg. 4), and the conditioning check of SURVEY 8(c4)
+    over lambda = 1, 10, 100;
   * yaw near +-pi (the MUFU sincos and the rint wrap against libm and remainder);
   * CEM with fewer finite costs than elites (Alg. 1, P:91-96; L17, L26);
   * robot sharding: two contexts with robot_offset = one context of all robots, bitwise.
@@ -109,7 +110,7 @@ def test_theta2_ulp_contract(B, orc):
 
 
 # ---------------------------------------------------------------------------
-# a5 at the chunked-merge launch shape, conditioning
+# a5 at the chunked-merge and dynamic-tile launch shapes, conditioning
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("K", [1 << 16, 1 << 18])
 def test_mppi_chunked_merge_against_oracle(B, orc, K):
@@ -277,7 +278,8 @@ def test_checkpoint_after_side_stream_step(B):
 
 
 def test_config4_full_size_update_recomputed(B):
-    """The bench's launch configuration (K = 2^22: 592 CTA records, the chunked merge): the
+    """The bench's launch configuration (K = 2^22: dynamic tiles, 32768 tile records reduced
+    by the fan-in-64 tree): the
     MPPI update (Alg. 4) recomputed in binary64 from the GPU's own costs and
     samples -- the costs are oracle-checked on samples (test_config4_full_size_sampled), the
     samples bitwise (the noise tests) -- must match the kernel's mean, Omega and ESS."""
