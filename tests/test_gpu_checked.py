@@ -5,8 +5,10 @@
   lists, robot outputs, contact tables -- is checked against its allocation's bound and
   traps on a violation), covering every kernel and launch shape the suite reaches;
 * run-to-run bit identity of whole iterations in every mode and launch mode: the
-  cross-CTA arrival counters, the producer / integrator named barriers, cp.async staging
-  and programmatic dependent launch would show a race as a difference between repeats.
+  cross-CTA arrival counters, the dynamic-tile counter and tree-node flags (K = 2^21),
+  the CEM cluster's shared-memory transactions (config 3), the producer / integrator
+  named barriers, cp.async staging and programmatic dependent launch would show a race
+  as a difference between repeats.
 """
 import os
 import subprocess
@@ -51,10 +53,11 @@ def B():
     return binding
 
 
-@pytest.mark.parametrize("which", ["c1", "c2", "c3cem", "c3naive", "c4_64k", "c5_small"])
+@pytest.mark.parametrize("which", ["c1", "c2", "c3cem", "c3naive", "c4_64k", "c4_2m", "c5_small"])
 def test_repeats_are_bit_identical(B, which):
     cfg, inputs = {"c1": W.config1, "c2": W.config2, "c3cem": lambda: W.config3("cem"),
                    "c3naive": lambda: W.config3("naive"), "c4_64k": lambda: W.config4(1 << 16),
+                   "c4_2m": lambda: W.config4(1 << 21),
                    "c5_small": lambda: W.config5(R=64, M=1024)}[which]()
     st = W.initial_distribution(cfg)
     ref = None
