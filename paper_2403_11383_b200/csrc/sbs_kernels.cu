@@ -1799,6 +1799,7 @@ __global__ void __launch_bounds__(SPLIT ? kBlock * kSplitLanes : kBlock, SPLIT ?
     SBS_CTS(3);
     if (tid == 0) dyn_arrive(p, s_pend, n_pend);
     dyn_merge_nodes(p, r, s_red, NR * kRedStride);
+    SBS_CTS(1);  // (DYN: the CTA's node merges done)
     // the last CTA to leave re-arms the tile counter (every CTA has taken its last index)
     if (tid == 0 && atomicAdd(p.dyn_cnt + 1, 1) == (int)gridDim.x - 1) {
       p.dyn_cnt[0] = 0;
