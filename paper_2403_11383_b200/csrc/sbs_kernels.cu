@@ -57,7 +57,18 @@ __device__ unsigned long long g_sbs_bar[4][8];  // integrator warp x chunk: cycl
       g_sbs_cta[blockIdx.x][i] = (i) >= 4 ? (unsigned long long)clock64() : t_; \
     }                                                                           \
   } while (0)
+#define SBS_CTT(i)                                                              \
+  do {                                                                          \
+    if (threadIdx.x == 0 && blockIdx.x < 1024 && blockIdx.y == 0) {             \
+      unsigned long long t_;                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
+      g_sbs_cta[blockIdx.x][i] = t_;                                            \
+    }                                                                           \
+  } while (0)
 #else
+#define SBS_CTT(i) \
+  do {             \
+  } while (0)
 #define SBS_TS(i) \
   do {            \
   } while (0)
@@ -1447,6 +1458,7 @@ static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int
       *c = 0;  // re-armed (nothing else touches it this launch)
     }
     __syncthreads();
+    SBS_CTT(2);  // (timing builds: the node's tiles are in)
     int idx = node;
     for (int l = 1; l <= L; ++l) {
       if (l > 1) {  // arrive at the level-l node; its last arrival merges it
@@ -1459,6 +1471,7 @@ static __device__ void dyn_merge_nodes(const Params& p, int r, float* stage, int
       const float* kids = p.dyn_rec + (size_t)(p.dyn_off[l - 1] + idx * p.dyn_fan) * RL;
       if (l < L) {
         dyn_node_merge(p, kids, nkids, p.dyn_rec + (size_t)(p.dyn_off[l] + idx) * RL, stage, stage_floats);
+        SBS_CTT(l == 1 ? 4 : 5);  // (timing builds: level-1 / upper node merged)
       } else if (p.emit) {  // world > 1: this rank's top-level record(s) (the exchange and rank-order merge follow)
         SBS_TS(5);
         dyn_node_merge(p, kids, nkids, p.emit + (size_t)idx * RL, stage, stage_floats);

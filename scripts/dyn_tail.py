@@ -37,10 +37,14 @@ for lk in (18, 20, 22):
         if it < 5 or a[:, 0].max() - t0 > 50e3:
             continue
         start, loop_end, merged = (a[:, 0] - t0) / 1e3, (a[:, 3] - t0) / 1e3, (a[:, 1] - t0) / 1e3
+        ready, l1, up = (a[:, 2] - t0) / 1e3, (a[:, 4] - t0) / 1e3, (a[:, 5] - t0) / 1e3
+        ok = lambda v: v[(v > 0) & (v < 1e5)]  # slots this launch wrote
         rows.append([start.max(), loop_end.min(), np.median(loop_end), loop_end.max(), merged.max(),
-                     (ts[5] - t0) / 1e3, (ts[6] - t0) / 1e3])
+                     (ts[5] - t0) / 1e3, (ts[6] - t0) / 1e3, ok(ready).max(), ok(l1).max(),
+                     ok(up).max() if ok(up).size else np.nan])
     m = np.median(np.array(rows), axis=0)
     print(f"K=2^{lk} grid {grid}: last CTA start {m[0]:.1f} | tile loops end min {m[1]:.1f} median {m[2]:.1f} "
           f"max {m[3]:.1f} | node merges end max {m[4]:.1f} | root merge {m[5]:.1f} -> {m[6]:.1f} us "
           f"({len(rows)} iterations)")
+    print(f"    last level-1 node ready {m[7]:.1f} merged {m[8]:.1f} | last upper node merged {m[9]:.1f}")
     c.close()
