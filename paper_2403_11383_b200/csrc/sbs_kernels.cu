@@ -2177,12 +2177,6 @@ static __device__ void select_block_small(const float* J, int K, int K_e, int64_
   const int k0 = tid * per;
   const int nk = max(0, min(per, K - k0));
   uint32_t key[kSelKPT];
-#if defined(SBS_TIMING_FIRSTLOAD)  // (timing experiment: the first load alone)
-  if (tid == 0) {
-    const float j0 = *(volatile const float*)&J[0];
-    if (blockIdx.x == 0 && j0 != 12345.f) SBS_TS(kSelTs + 1);
-  }
-#endif
 #pragma unroll
   for (int i = 0; i < kSelKPT; ++i) key[i] = i < nk ? cost_key(J[k0 + i]) : 0xFFFFFFFFu;
   if (blockIdx.x == 0) SBS_TS(kSelTs + 2);
