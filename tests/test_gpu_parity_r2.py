@@ -380,7 +380,7 @@ def test_cem_cluster_path_only_while_the_clusters_fit(B):
 
 
 # ---------------------------------------------------------------------------
-# a5 with dynamic tile scheduling (throughput mode, one robot, several tiles per CTA)
+# a5 with dynamic tile scheduling (throughput mode, one robot, more tiles than CTAs)
 # ---------------------------------------------------------------------------
 def test_dynamic_tiles_are_deterministic_and_match_the_static_split(B, orc, monkeypatch):
     """With dynamic tile scheduling the CTAs take tiles from a counter, so which CTA runs
@@ -460,13 +460,14 @@ def test_sharded_mppi_is_bitwise_independent_of_the_gpu_count(B, K, world):
                 np.testing.assert_array_equal(np.asarray(o[key]), np.asarray(so[0][key]), err_msg=f"iter {it} {key}")
 
 
-def test_dynamic_tiles_ragged_last_tile_and_partial_nodes(B, orc, monkeypatch):
-    """Dynamic tiles with K = 2^18 + 77: a partial last tile (77 samples) and partial tree
-    nodes at every level; repeated runs are bitwise equal, the static split agrees to
-    rounding, and J_min, the effective sample size and the divergence count follow from
-    the GPU's costs in binary64 (Alg. 4; the mean against the oracle at the tree's launch
-    shape: test_mppi_chunked_merge_against_oracle at K = 2^18)."""
-    K = (1 << 18) + 77
+@pytest.mark.parametrize("K", [(1 << 18) + 77, (1 << 17) - 51])
+def test_dynamic_tiles_ragged_last_tile_and_partial_nodes(B, orc, monkeypatch, K):
+    """Dynamic tiles with K = 2^18 + 77 (a partial last tile of 77 samples, partial tree
+    nodes at every level) and K = 2^17 - 51 (1024 tiles over 592 CTAs: between one and
+    two tiles per CTA, the last one partial); repeated runs are bitwise equal, the static
+    split agrees to rounding, and J_min, the effective sample size and the divergence
+    count follow from the GPU's costs in binary64 (Alg. 4; the mean against the oracle at
+    the tree's launch shape: test_mppi_chunked_merge_against_oracle at K = 2^18)."""
     cfg, inputs = W.config4(K)
     st = W.initial_distribution(cfg)
     res = []
