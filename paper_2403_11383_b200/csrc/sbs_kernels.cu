@@ -836,6 +836,19 @@ __device__ __forceinline__ const float* part_rec(const Params& p, int r, int c) 
 
 // cooperative copy of n floats (n % 4 == 0, 16-byte aligned) from L2 to shared
 // memory, 4 independent 16-byte loads in flight per thread
+// records into shared memory by cp.async (L2 -> shared, no register destination: every
+// 16-byte piece of the block's share in flight at once, one L2 round trip); stage_wait
+// completes the calling thread's copies (a barrier then publishes them to the block)
+__device__ __forceinline__ void stage_issue(float* dst, const float* src, int n) {
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  const int n4 = n >> 2;
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) cp_async16(d4 + i, s4 + i);
+}
+__device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// the same through registers, four 16-byte loads in flight per thread: kept for the
+// dynamic-tile kernel's node merges (its build with the cp.async form, measured together
+// with a deferred second-tile fetch, ran K = 2^22 in 1070 instead of 1062 us)
 __device__ __forceinline__ void stage_copy(float* dst, const float* src, int n) {
   const float4* s4 = reinterpret_cast<const float4*>(src);
   float4* d4 = reinterpret_cast<float4*>(dst);
@@ -911,15 +924,29 @@ static __device__ Best merge_argmin(const Params& p, int r, const float* recs = 
   float m = kInf;
   int mk = 0x7fffffff, mf = 0;
   const int nc = recs ? nrec : p.n_cta;
-  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
-    const float* pc = recs ? recs + (size_t)c * p.part_stride : part_rec(p, r, c);
-    const float mc = __ldcg(pc);
-    const int kc = __float_as_int(__ldcg(pc + 1));
-    if (jk_less(mc, kc, m, mk)) {
-      m = mc;
-      mk = kc;
-      mf = __float_as_int(__ldcg(pc + 2));
+  for (int c0 = threadIdx.x; c0 < nc; c0 += 4 * blockDim.x) {  // four headers' loads in flight per thread
+    float mc[4];
+    int kc[4], fc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u * blockDim.x;
+      mc[u] = kInf;
+      kc[u] = 0x7fffffff;
+      fc[u] = 0;
+      if (c < nc) {
+        const float* pc = recs ? recs + (size_t)c * p.part_stride : part_rec(p, r, c);
+        mc[u] = __ldcg(pc);
+        kc[u] = __float_as_int(__ldcg(pc + 1));
+        fc[u] = __float_as_int(__ldcg(pc + 2));
+      }
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (jk_less(mc[u], kc[u], m, mk)) {
+        m = mc[u];
+        mk = kc[u];
+        mf = fc[u];
+      }
   }
   warp_argmin(m, mk, mf);
   if ((threadIdx.x & 31) == 0) {
@@ -960,11 +987,11 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   if (one_pass) {
     // one load round trip: every record, this robot's variance, input phase and iteration counter
     if (recs) {
-      stage_copy(stage, recs, nc * RL);
+      stage_issue(stage, recs, nc * RL);
     } else if (p.part_c_stride == 1) {
-      stage_copy(stage, part_rec(p, r, 0), nc * RL);  // records of a robot are contiguous
+      stage_issue(stage, part_rec(p, r, 0), nc * RL);  // records of a robot are contiguous
     } else {
-      for (int c = 0; c < nc; ++c) stage_copy(stage + c * RL, part_rec(p, r, c), RL);
+      for (int c = 0; c < nc; ++c) stage_issue(stage + c * RL, part_rec(p, r, c), RL);
     }
     if (!EMIT) {
       for (int d = tid; d < D; d += blockDim.x) s_var[d] = p.var[(size_t)r * D + d];
@@ -973,6 +1000,7 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
         s_pre[1] = step_iter(p);
       }
     }
+    stage_wait();
     __syncthreads();
     SBS_TS(7);
     // every thread: the smallest record minimum (the scales' reference, no barrier); warp 0
@@ -1007,17 +1035,19 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
   SBS_TS(8);
   const float beta = one_pass ? bmin : b.m;  // (one pass: b is read after the row sums' barrier)
   const int CH = one_pass ? nc : min(128, max(1, stage_floats / RL));
-  float acc = 0.f;  // thread tid < NR owns row tid: 0..D-1 V, D S, D+1 S2, D+2 sumJ, D+3 nfin
+  float acc = 0.f;  // chunked: thread tid < nh NR owns row tid % NR (0..D-1 V, D S, D+1 S2, D+2 sumJ, D+3 nfin), half tid / NR
+  const int nh = 2 * NR <= (int)blockDim.x ? 2 : 1;
   for (int c0 = 0; c0 < nc; c0 += CH) {
     const int n = min(CH, nc - c0);
     if (!one_pass) {
       if (recs) {
-        stage_copy(stage, recs + (size_t)c0 * RL, n * RL);
+        stage_issue(stage, recs + (size_t)c0 * RL, n * RL);
       } else if (p.part_c_stride == 1) {
-        stage_copy(stage, part_rec(p, r, c0), n * RL);
+        stage_issue(stage, part_rec(p, r, c0), n * RL);
       } else {
-        for (int c = 0; c < n; ++c) stage_copy(stage + c * RL, part_rec(p, r, c0 + c), RL);
+        for (int c = 0; c < n; ++c) stage_issue(stage + c * RL, part_rec(p, r, c0 + c), RL);
       }
+      stage_wait();
       __syncthreads();
     }
     if (one_pass) {  // (row, record-chunk) per thread, each computing its records' scales, then chunk sums
@@ -1062,19 +1092,22 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
       s_sc[c] = (mc < kInf) ? __expf((beta - mc) * p.inv_lambda) : 0.0f;
     }
     __syncthreads();
-    if (tid < NR) {
-      const int col = tid < D ? kPartHdr + tid : 3 + (tid - D);
-      const int kind = tid < D + 1 ? 0 : (tid == D + 1 ? 1 : 2);
+    if (tid < nh * NR) {  // (row, half of the chunk) per thread
+      const int row = tid % NR, h = tid / NR, per = (n + nh - 1) / nh;
+      const int col = row < D ? kPartHdr + row : 3 + (row - D);
+      const int kind = row < D + 1 ? 0 : (row == D + 1 ? 1 : 2);
+      const int c_end = min(n, (h + 1) * per);
       float a0 = 0.f, a1 = 0.f;
-      int c = 0;
-      for (; c + 1 < n; c += 2) {
+      int c = h * per;
+#pragma unroll 4
+      for (; c + 1 < c_end; c += 2) {
         float s0 = s_sc[c], s1 = s_sc[c + 1];
         if (kind == 1) { s0 *= s0; s1 *= s1; }
         if (kind == 2) { s0 = 1.f; s1 = 1.f; }
         a0 = fmaf(stage[c * RL + col], s0, a0);
         a1 = fmaf(stage[(c + 1) * RL + col], s1, a1);
       }
-      if (c < n) {
+      if (c < c_end) {
         float s0 = kind == 2 ? 1.f : s_sc[c];
         if (kind == 1) s0 *= s0;
         a0 = fmaf(stage[c * RL + col], s0, a0);
@@ -1083,7 +1116,11 @@ static __device__ void mppi_merge_block(const Params& p, int r, float* emit, flo
     }
     __syncthreads();
   }
-  if (!one_pass && tid < NR) s_row[0][tid] = acc;
+  if (!one_pass) {  // the halves' sums, in order
+    if (tid < nh * NR) s_part[tid] = acc;
+    __syncthreads();
+    if (tid < NR) s_row[0][tid] = nh == 2 ? s_part[tid] + s_part[NR + tid] : s_part[tid];
+  }
   __syncthreads();
   if (one_pass) b = Best{s_bm[0], s_bk[0], s_bf[0]};  // (warp 0's argmin, ordered by the barriers above)
   SBS_TS(9);
@@ -2516,7 +2553,8 @@ __global__ void __launch_bounds__(32 * 3 * P) sbs_elite_kernel(const __grid_cons
     float a0 = 0.f;  // row tid (2D + 1 <= blockDim = 8D); records summed in block order
     for (int b0 = 0; b0 < (int)gridDim.x; b0 += kChunk) {
       const int nb = min(kChunk, (int)gridDim.x - b0);
-      stage_copy(s_stage, p.epart + ((size_t)r * gridDim.x + b0) * kEPartStride, nb * kEPartStride);
+      stage_issue(s_stage, p.epart + ((size_t)r * gridDim.x + b0) * kEPartStride, nb * kEPartStride);
+      stage_wait();
       __syncthreads();
       if (tid < 2 * D + 1)
         for (int b = 0; b < nb; ++b) a0 += s_stage[b * kEPartStride + tid];

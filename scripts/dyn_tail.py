@@ -15,7 +15,7 @@ L.sbs_debug_cta_p4.argtypes = [C.POINTER(C.c_uint64)]
 L.sbs_debug_ts_p4.argtypes = [C.POINTER(C.c_uint64)]
 n_sm = torch.cuda.get_device_properties(0).multi_processor_count
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for lk in (18, 20, 22):
+for lk in [int(a) for a in sys.argv[1:]] or (18, 20, 22):
     cfg, inputs = W.config4(1 << lk)
     c = B.Controller(cfg)
     c.set_reference(0, inputs[0]["xref"])
@@ -38,13 +38,16 @@ for lk in (18, 20, 22):
             continue
         start, loop_end, merged = (a[:, 0] - t0) / 1e3, (a[:, 3] - t0) / 1e3, (a[:, 1] - t0) / 1e3
         ready, l1, up = (a[:, 2] - t0) / 1e3, (a[:, 4] - t0) / 1e3, (a[:, 5] - t0) / 1e3
-        ok = lambda v: v[(v > 0) & (v < 1e5)]  # slots this launch wrote
-        rows.append([start.max(), loop_end.min(), np.median(loop_end), loop_end.max(), merged.max(),
-                     (ts[5] - t0) / 1e3, (ts[6] - t0) / 1e3, ok(ready).max(), ok(l1).max(),
-                     ok(up).max() if ok(up).size else np.nan])
+        def last(v):  # latest of the slots this launch wrote (static split: none)
+            v = v[(v > 0) & (v < 1e5)]
+            return v.max() if v.size else np.nan
+        rows.append([start.max(), loop_end.min(), np.median(loop_end), loop_end.max(), last(merged),
+                     (ts[5] - t0) / 1e3, (ts[6] - t0) / 1e3, last(ready), last(l1), last(up),
+                     (ts[8] - t0) / 1e3, (ts[9] - t0) / 1e3, (ts[10] - t0) / 1e3])
     m = np.median(np.array(rows), axis=0)
     print(f"K=2^{lk} grid {grid}: last CTA start {m[0]:.1f} | tile loops end min {m[1]:.1f} median {m[2]:.1f} "
           f"max {m[3]:.1f} | node merges end max {m[4]:.1f} | root merge {m[5]:.1f} -> {m[6]:.1f} us "
           f"({len(rows)} iterations)")
-    print(f"    last level-1 node ready {m[7]:.1f} merged {m[8]:.1f} | last upper node merged {m[9]:.1f}")
+    print(f"    last level-1 node ready {m[7]:.1f} merged {m[8]:.1f} | last upper node merged {m[9]:.1f}"
+          f" | static merge: argmin {m[10]:.1f} sums {m[11]:.1f} mean written {m[12]:.1f}")
     c.close()

@@ -5,8 +5,9 @@ reach.
     angle inputs, bit for bit against the oracle (O3-O4; P:236 "theta_k ~ N(theta, C)");
   * Philox4x32-10 against cuRAND's curand_Philox4x32_10 on the device (O1);
   * theta2 within the stated ulp contract;
-  * MPPI at K = 2^16 (more CTA records than the one-pass merge holds: the chunked merge)
-    and 2^18 (dynamic tiles and the reduction tree the K = 2^22 bench launch takes)
+  * MPPI at K = 2^16 and 2^17 with the static split (more CTA records than the one-pass
+    merge holds: the chunked merge), and at 2^18 with dynamic tiles and the reduction
+    tree the K = 2^22 bench launch takes
     against the oracle (Alg. 4), and the conditioning check of SURVEY 8(c4)
     over lambda = 1, 10, 100;
   * yaw near +-pi (the MUFU sincos and the rint wrap against libm and remainder);
@@ -112,8 +113,14 @@ def test_theta2_ulp_contract(B, orc):
 # ---------------------------------------------------------------------------
 # a5 at the chunked-merge and dynamic-tile launch shapes, conditioning
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("K", [1 << 16, 1 << 18])
-def test_mppi_chunked_merge_against_oracle(B, orc, K):
+@pytest.mark.parametrize("K,dyn", [(1 << 16, None), (1 << 17, "0"), (1 << 18, None)])
+def test_mppi_chunked_merge_against_oracle(B, orc, K, dyn, monkeypatch):
+    """K = 2^16 (one tile per CTA) and 2^17 with SBS_DYN=0: 512 / 592 CTA records, more
+    than one staged merge holds (the chunked merge); K = 2^18: dynamic tiles and the
+    reduction tree."""
+    monkeypatch.delenv("SBS_DYN", raising=False)
+    if dyn is not None:
+        monkeypatch.setenv("SBS_DYN", dyn)
     cfg, inputs = W.config4(K)
     st = W.initial_distribution(cfg)
     c = _ctrl(B, cfg, inputs, st)
