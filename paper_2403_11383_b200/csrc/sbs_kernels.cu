@@ -846,9 +846,8 @@ __device__ __forceinline__ void stage_issue(float* dst, const float* src, int n)
   for (int i = threadIdx.x; i < n4; i += blockDim.x) cp_async16(d4 + i, s4 + i);
 }
 __device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-// the same through registers, four 16-byte loads in flight per thread: kept for the
-// dynamic-tile kernel's node merges (its build with the cp.async form, measured together
-// with a deferred second-tile fetch, ran K = 2^22 in 1070 instead of 1062 us)
+// the same through registers, four 16-byte loads in flight per thread (the dynamic-tile
+// kernel's node merges, whose headline build it is)
 __device__ __forceinline__ void stage_copy(float* dst, const float* src, int n) {
   const float4* s4 = reinterpret_cast<const float4*>(src);
   float4* d4 = reinterpret_cast<float4*>(dst);
